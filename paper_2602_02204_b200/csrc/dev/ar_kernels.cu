@@ -1,0 +1,374 @@
+// K2-K4: the non-GEMM kernels of one batched AR step (Thinker / Talker).
+//
+//   embed            token (+ talker conditioning) -> fp32 residual rows
+//   rmsnorm          fp32 residual -> bf16 GEMM input (no gain; folded away)
+//   rope_kv          fp32 QKV -> RoPE(q,k) -> q bf16 rows, k/v into paged KV
+//   attention        paged-KV causal attention for mixed decode / chunked-
+//                    prefill entries (GQA), pages staged by 1-D TMA bulk copies
+//   final_gather     final RMSNorm of DECODE rows -> hidden rows (bf16),
+//                    also written to the sequence's hidden ring (Thinker)
+//   argmax           greedy id + top-2 margin over the valid vocabulary
+//
+// All per-row work depends only on that row's own inputs (batch invariance,
+// SURVEY §0.7a). Replaces StageModel::prefill/decode (registry.hpp:79-89;
+// mock semantics reference_pipeline.hpp:96-154).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "ar_kernels.h"
+#include "ptx.cuh"
+
+namespace omni_dev {
+
+// ---------------------------------------------------------------------------
+// Embedding.  Thinker: x = E[tok].  Talker prefill token j:
+//   cond_j = E_t[tok] + (W_h h_j) (precomputed GEMM rows in `hproj`), stored
+//   to the sequence's conditioning table, x = cond_j.  Talker decode step m:
+//   x = E_c[prev] + cond_{m/4}.
+// ---------------------------------------------------------------------------
+__global__ void embed_kernel(const ArStepDev s, const __nv_bfloat16* __restrict__ emb,
+                             const __nv_bfloat16* __restrict__ emb2, const float* __restrict__ hproj,
+                             float* __restrict__ cond_table, int cond_rows, int d, int start_id,
+                             float* __restrict__ x) {
+  const int r = blockIdx.x;
+  const ArRowDesc rd = s.rows[r];
+  const ArEntryDesc ed = s.entries[rd.entry];
+  const int tok = rd.token < 0 ? start_id : rd.token;
+  float* xr = x + (size_t)r * d;
+  if (emb2 == nullptr) {  // thinker
+    const __nv_bfloat16* e = emb + (size_t)tok * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = bf2f(e[i]);
+    return;
+  }
+  float* cond = cond_table + ((size_t)ed.slot * cond_rows + rd.cond_row) * d;
+  if (!ed.is_decode) {  // talker prefill: build conditioning row j
+    const __nv_bfloat16* et = emb + (size_t)tok * d;
+    const float* hp = hproj + (size_t)r * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      const float c = bf2f(et[i]) + hp[i];
+      cond[i] = c;
+      xr[i] = c;
+    }
+  } else {
+    const __nv_bfloat16* ec = emb2 + (size_t)tok * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = bf2f(ec[i]) + cond[i];
+  }
+}
+
+// Talker: gather the upstream FIX16 hidden rows (2-byte aligned inside the
+// packed connector payload) into an aligned bf16 GEMM input.
+__global__ void gather_cond_kernel(const ArStepDev s, int d, __nv_bfloat16* __restrict__ out) {
+  const int r = blockIdx.x;
+  const uint64_t src = s.rows[r].cond_src;
+  __nv_bfloat16* o = out + (size_t)r * d;
+  if (src == 0) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = __float2bfloat16_rn(0.f);
+    return;
+  }
+  const unsigned short* p = reinterpret_cast<const unsigned short*>(src);
+  unsigned short* q = reinterpret_cast<unsigned short*>(o);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) q[i] = p[i];
+}
+
+// ---------------------------------------------------------------------------
+// RMSNorm without gain: y = bf16(x / sqrt(mean(x^2) + eps)).  One CTA/row.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) t += red[i];  // fixed order: deterministic
+  return t;
+}
+
+__global__ void rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
+                               __nv_bfloat16* __restrict__ y) {
+  __shared__ float red[32];
+  const float* xr = x + (size_t)blockIdx.x * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+  const float tot = block_sum(ss, red);
+  const float inv = rsqrtf(tot / d + eps);
+  __nv_bfloat16* yr = y + (size_t)blockIdx.x * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) yr[i] = f2bf(xr[i] * inv);
+}
+
+// ---------------------------------------------------------------------------
+// RoPE (rotate-half, pairs (i, i+64) of a 128-dim head) on fp32 QKV, then
+// q -> bf16 rows, k/v -> bf16 paged KV at the row's position.
+// KV page layout: [page][layer][k|v][kv_head][16 tokens][head_dim].
+// ---------------------------------------------------------------------------
+__global__ void rope_kv_kernel(const ArStepDev s, const float* __restrict__ qkv, int n_heads,
+                               int n_kv, const float2* __restrict__ rope, int layer, int n_layers,
+                               __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv) {
+  constexpr int HD = kHeadDim, HALF = kHeadDim / 2;
+  const int r = blockIdx.x;
+  const ArRowDesc rd = s.rows[r];
+  const ArEntryDesc ed = s.entries[rd.entry];
+  const int pos = rd.pos;
+  const int page = s.page_table[rd.entry * s.max_pages + pos / kPageTokens];
+  const int slot_tok = pos % kPageTokens;
+  const int width = (n_heads + 2 * n_kv) * HD;
+  const float* row = qkv + (size_t)r * width;
+  // heads: [0, n_heads) q, [n_heads, n_heads + n_kv) k, then v
+  for (int t = threadIdx.x; t < (n_heads + 2 * n_kv) * HALF; t += blockDim.x) {
+    const int h = t / HALF, i = t % HALF;
+    const float a = row[h * HD + i], b = row[h * HD + i + HALF];
+    float o0 = a, o1 = b;
+    if (h < n_heads + n_kv) {
+      const float2 cs = rope[(size_t)pos * HALF + i];  // (cos, sin)
+      o0 = a * cs.x - b * cs.y;
+      o1 = b * cs.x + a * cs.y;
+    }
+    if (h < n_heads) {
+      __nv_bfloat16* q = q_out + (size_t)r * n_heads * HD + h * HD;
+      q[i] = f2bf(o0);
+      q[i + HALF] = f2bf(o1);
+    } else {
+      const int is_v = h >= n_heads + n_kv;
+      const int kh = is_v ? h - n_heads - n_kv : h - n_heads;
+      __nv_bfloat16* dst =
+          kv + ((((size_t)page * n_layers + layer) * 2 + is_v) * n_kv + kh) * kPageTokens * HD +
+          (size_t)slot_tok * HD;
+      dst[i] = f2bf(o0);
+      dst[i + HALF] = f2bf(o1);
+    }
+  }
+  (void)ed;
+}
+
+// ---------------------------------------------------------------------------
+// Paged causal attention. Grid (entry, kv_head); 8 warps. Each CTA owns the
+// q_len x group query vectors of one entry that share a KV head; K/V pages of
+// the entry's context are staged into smem with 1-D bulk TMA copies (double
+// buffered, mbarrier-tracked) and every warp runs an online softmax for its
+// query vectors with lanes splitting the 128 head dims.
+// ---------------------------------------------------------------------------
+constexpr int kAttnWarps = 8;
+
+__global__ void __launch_bounds__(kAttnWarps * 32)
+    attention_kernel(const ArStepDev s, const __nv_bfloat16* __restrict__ q, int n_heads, int n_kv,
+                     int layer, int n_layers, const __nv_bfloat16* __restrict__ kv,
+                     __nv_bfloat16* __restrict__ out, float scale) {
+  constexpr int HD = kHeadDim;
+  constexpr int PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB per K or V page slice
+  __shared__ __align__(128) __nv_bfloat16 sk[2][kPageTokens * HD];
+  __shared__ __align__(128) __nv_bfloat16 sv[2][kPageTokens * HD];
+  __shared__ __align__(8) uint64_t bar[2];
+
+  const int e = blockIdx.x, kh = blockIdx.y;
+  const ArEntryDesc ed = s.entries[e];
+  const int group = n_heads / n_kv;
+  const int nq = ed.q_len * group;  // query vectors in this CTA
+  const int ctx = ed.pos0 + ed.q_len;
+  const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
+  const int warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int p, int buf) {
+    const int page = s.page_table[e * s.max_pages + p];
+    const __nv_bfloat16* kp =
+        kv + ((((size_t)page * n_layers + layer) * 2 + 0) * n_kv + kh) * kPageTokens * HD;
+    const __nv_bfloat16* vp =
+        kv + ((((size_t)page * n_layers + layer) * 2 + 1) * n_kv + kh) * kPageTokens * HD;
+    mbar_expect_tx(&bar[buf], 2 * PAGE_BYTES);
+    bulk_load(sk[buf], kp, PAGE_BYTES, &bar[buf]);
+    bulk_load(sv[buf], vp, PAGE_BYTES, &bar[buf]);
+  };
+
+  // Per-warp state for up to kMaxQPerWarp query vectors (processed in waves).
+  constexpr int kMaxQPerWarp = 4;
+  const int n_waves = (nq + kAttnWarps * kMaxQPerWarp - 1) / (kAttnWarps * kMaxQPerWarp);
+  for (int wave = 0; wave < n_waves; ++wave) {
+    // the whole CTA sweeps the pages once per wave of query vectors; query
+    // vectors are dealt round-robin so small (decode) entries use all warps
+    const int q0 = wave * kAttnWarps * kMaxQPerWarp;
+    float m[kMaxQPerWarp], l[kMaxQPerWarp], acc[kMaxQPerWarp][4], qv[kMaxQPerWarp][4];
+    int qpos[kMaxQPerWarp];
+#pragma unroll
+    for (int j = 0; j < kMaxQPerWarp; ++j) {
+      m[j] = -INFINITY;
+      l[j] = 0.f;
+      qpos[j] = -1;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[j][t] = 0.f, qv[j][t] = 0.f;
+      const int qi = q0 + j * kAttnWarps + warp;
+      if (qi < nq) {
+        const int tok = qi / group, hq = kh * group + qi % group;
+        const __nv_bfloat16* qp = q + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) qv[j][t] = bf2f(qp[lane * 4 + t]) * scale;
+        qpos[j] = ed.pos0 + tok;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) issue(0, 0);
+    for (int p = 0; p < n_pages; ++p) {
+      const int buf = p & 1;
+      if (threadIdx.x == 0 && p + 1 < n_pages) issue(p + 1, buf ^ 1);
+      mbar_wait(&bar[buf], (p >> 1) & 1);
+      const int kbase = p * kPageTokens;
+      for (int jk = 0; jk < kPageTokens; ++jk) {
+        const int kpos = kbase + jk;
+        if (kpos >= ctx) break;
+        float kr[4], vr[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          kr[t] = bf2f(sk[buf][jk * HD + lane * 4 + t]);
+          vr[t] = bf2f(sv[buf][jk * HD + lane * 4 + t]);
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxQPerWarp; ++j) {
+          if (qpos[j] < 0 || kpos > qpos[j]) continue;  // warp-uniform
+          float dot = qv[j][0] * kr[0] + qv[j][1] * kr[1] + qv[j][2] * kr[2] + qv[j][3] * kr[3];
+          dot = warp_sum(dot);
+          const float mn = fmaxf(m[j], dot);
+          const float corr = __expf(m[j] - mn);
+          const float pj = __expf(dot - mn);
+          l[j] = l[j] * corr + pj;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc[j][t] = acc[j][t] * corr + pj * vr[t];
+          m[j] = mn;
+        }
+      }
+      __syncthreads();  // everyone done with `buf` before it is refilled
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxQPerWarp; ++j) {
+      const int qi = q0 + j * kAttnWarps + warp;
+      if (qi >= nq) continue;
+      const int tok = qi / group, hq = kh * group + qi % group;
+      __nv_bfloat16* op = out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD;
+      const float inv = 1.f / l[j];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) op[lane * 4 + t] = f2bf(acc[j][t] * inv);
+    }
+    // phases of bar[] advance once per page per wave; re-init for next wave
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Final norm of DECODE rows -> compact hidden rows (+ hidden ring for the
+// thinker, row `out_index` of the sequence's slot).
+// ---------------------------------------------------------------------------
+__global__ void final_gather_kernel(const ArStepDev s, const float* __restrict__ x, int d, float eps,
+                                    __nv_bfloat16* __restrict__ hout, __nv_bfloat16* __restrict__ ring,
+                                    int ring_rows) {
+  __shared__ float red[32];
+  const int e = s.dec_entries[blockIdx.x];
+  const ArEntryDesc ed = s.entries[e];
+  const float* xr = x + (size_t)ed.row0 * d;  // decode entries have exactly one row
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+  const float tot = block_sum(ss, red);
+  const float inv = rsqrtf(tot / d + eps);
+  __nv_bfloat16* h = hout + (size_t)blockIdx.x * d;
+  __nv_bfloat16* rg = ring ? ring + ((size_t)ed.slot * ring_rows + ed.out_index) * d : nullptr;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const __nv_bfloat16 v = f2bf(xr[i] * inv);
+    h[i] = v;
+    if (rg) rg[i] = v;
+  }
+}
+
+// Greedy id over [lo, hi) of the logits row; ties -> lowest id. Also the
+// top-2 margin used by the teacher-forced parity rule.
+__global__ void argmax_kernel(const float* __restrict__ logits, int ld, int lo, int hi,
+                              int* __restrict__ tok_out, float* __restrict__ margin_out) {
+  const float* row = logits + (size_t)blockIdx.x * ld;
+  float b1 = -INFINITY, b2 = -INFINITY;
+  int i1 = 0x7fffffff;
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const float v = row[i];
+    if (v > b1 || (v == b1 && i < i1)) {
+      b2 = b1;
+      b1 = v;
+      i1 = i;
+    } else if (v > b2) {
+      b2 = v;
+    }
+  }
+  // warp merge (blockDim == 32)
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
+    const float ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+    const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+    if (ob1 > b1 || (ob1 == b1 && oi1 < i1)) {
+      b2 = fmaxf(b1, ob2);
+      b1 = ob1;
+      i1 = oi1;
+    } else {
+      b2 = fmaxf(b2, ob1);
+    }
+  }
+  if (threadIdx.x == 0) {
+    tok_out[blockIdx.x] = i1;
+    margin_out[blockIdx.x] = b1 - b2;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,
+                         const __nv_bfloat16* emb2, const float* hproj, float* cond_table,
+                         int cond_rows, int d, int start_id, float* x, cudaStream_t st) {
+  embed_kernel<<<n_rows, 256, 0, st>>>(s, emb, emb2, hproj, cond_table, cond_rows, d, start_id, x);
+  return cudaGetLastError();
+}
+cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloat16* out,
+                               cudaStream_t st) {
+  gather_cond_kernel<<<n_rows, 256, 0, st>>>(s, d, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_rmsnorm(const float* x, int rows, int d, float eps, __nv_bfloat16* y,
+                           cudaStream_t st) {
+  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, d, eps, y);
+  return cudaGetLastError();
+}
+cudaError_t launch_rope_kv(const ArStepDev& s, int n_rows, const float* qkv, int n_heads, int n_kv,
+                           const float2* rope, int layer, int n_layers, __nv_bfloat16* q_out,
+                           __nv_bfloat16* kv, cudaStream_t st) {
+  rope_kv_kernel<<<n_rows, 256, 0, st>>>(s, qkv, n_heads, n_kv, rope, layer, n_layers, q_out, kv);
+  return cudaGetLastError();
+}
+cudaError_t launch_attention(const ArStepDev& s, int n_entries, const __nv_bfloat16* q,
+                             int n_heads, int n_kv, int layer, int n_layers,
+                             const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st) {
+  dim3 grid(n_entries, n_kv);
+  attention_kernel<<<grid, kAttnWarps * 32, 0, st>>>(s, q, n_heads, n_kv, layer, n_layers, kv, out,
+                                                     rsqrtf((float)kHeadDim));
+  return cudaGetLastError();
+}
+cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,
+                                __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
+                                cudaStream_t st) {
+  if (n_dec == 0) return cudaSuccess;
+  final_gather_kernel<<<n_dec, 256, 0, st>>>(s, x, d, eps, hout, ring, ring_rows);
+  return cudaGetLastError();
+}
+cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
+                          cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  argmax_kernel<<<n, 32, 0, st>>>(logits, ld, lo, hi, tok, margin);
+  return cudaGetLastError();
+}
+
+}  // namespace omni_dev

@@ -1,0 +1,59 @@
+// Device step descriptor shared by the AR kernels and the host runtime.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace omni_dev {
+
+constexpr int kHeadDim = 128;
+constexpr int kPageTokens = 16;
+
+struct ArEntryDesc {  // one IterationBatch entry (ar_engine.hpp:56-70)
+  int32_t slot;       // resident slot of the sequence (hidden ring / cond table row)
+  int32_t q_len;      // span
+  int32_t pos0;       // first KV position
+  int32_t row0;       // first flattened token row
+  int32_t is_decode;
+  int32_t out_index;  // decode: emitted index k
+  int32_t dec_row;    // decode: row in the compact decode output, else -1
+  int32_t pad;
+};
+
+struct ArRowDesc {  // one token row of the step
+  int32_t entry;
+  int32_t pos;
+  int32_t token;     // -1 = stage start id
+  int32_t cond_row;  // talker conditioning row j
+  uint64_t cond_src; // talker prefill: device address of the upstream hidden row
+};
+
+struct ArStepDev {
+  const ArEntryDesc* entries;
+  const ArRowDesc* rows;
+  const int32_t* page_table;   // [n_entries][max_pages]
+  const int32_t* dec_entries;  // [n_dec] entry index of each decode row
+  int32_t max_pages;
+};
+
+cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,
+                         const __nv_bfloat16* emb2, const float* hproj, float* cond_table,
+                         int cond_rows, int d, int start_id, float* x, cudaStream_t st);
+cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloat16* out,
+                               cudaStream_t st);
+cudaError_t launch_rmsnorm(const float* x, int rows, int d, float eps, __nv_bfloat16* y,
+                           cudaStream_t st);
+cudaError_t launch_rope_kv(const ArStepDev& s, int n_rows, const float* qkv, int n_heads, int n_kv,
+                           const float2* rope, int layer, int n_layers, __nv_bfloat16* q_out,
+                           __nv_bfloat16* kv, cudaStream_t st);
+cudaError_t launch_attention(const ArStepDev& s, int n_entries, const __nv_bfloat16* q,
+                             int n_heads, int n_kv, int layer, int n_layers,
+                             const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st);
+cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,
+                                __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
+                                cudaStream_t st);
+cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
+                          cudaStream_t st);
+
+}  // namespace omni_dev

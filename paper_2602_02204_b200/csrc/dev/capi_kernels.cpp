@@ -1,0 +1,159 @@
+// C-ABI: process-level entry points and kernel-level test/bench hooks.
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.h"
+#include "gemm.h"
+#include "kernels.h"
+#include "omni_dev.h"
+
+namespace omni_dev {
+
+namespace {
+thread_local std::string g_last_error;
+
+void require_gpu() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw DevError(OMNI_E_NOGPU, "no CUDA device visible (libomni_dev has no CPU fallback)");
+  int dev = 0, major = 0;
+  OMNI_CUDA(cudaGetDevice(&dev));
+  OMNI_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+  if (major != 10) throw DevError(OMNI_E_NOGPU, "libomni_dev is built for sm_100a only");
+}
+
+void run_test_gemm(uint64_t W, int N, int K, uint64_t X, int M, int epi, uint64_t out, int ldo,
+                   uint64_t gate, int ldg, int gate_off, int rpg, int* splits_out, int iters,
+                   float* ms, int max_splits = 8) {
+  require_gpu();
+  OMNI_REQUIRE(N > 0 && K > 0 && M > 0, OMNI_E_BADARG, "gemm: empty shape");
+  const int N_pad = (N + 127) / 128 * 128;
+  GemmWeight w;
+  GemmInput x;
+  OMNI_REQUIRE(gemm_make_weight(w, reinterpret_cast<const __nv_bfloat16*>(W), N, N_pad, K, max_splits),
+               OMNI_E_BADARG, "gemm: weight tensor map (N, K multiples of 128 / 64?)");
+  OMNI_REQUIRE(gemm_make_input(x, reinterpret_cast<const __nv_bfloat16*>(X), M, K), OMNI_E_BADARG,
+               "gemm: input tensor map");
+  GemmEpilogue e;
+  e.out = reinterpret_cast<void*>(out);
+  e.ldo = ldo;
+  e.gate = reinterpret_cast<const float*>(gate);
+  e.ldg = ldg;
+  e.gate_off = gate_off;
+  e.rows_per_group = rpg;
+  if (splits_out) *splits_out = w.splits;
+  if (iters <= 0) {
+    OMNI_CUDA(gemm_run(w, x, M, epi, e, 0));
+    OMNI_CUDA(cudaDeviceSynchronize());
+    return;
+  }
+  // Time a CUDA graph of `iters` launches so host launch cost is excluded.
+  cudaStream_t cs;
+  OMNI_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  OMNI_CUDA(gemm_run(w, x, M, epi, e, cs));  // warm-up (also sets smem attributes)
+  OMNI_CUDA(cudaStreamSynchronize(cs));
+  cudaGraph_t g;
+  cudaGraphExec_t ge;
+  OMNI_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < iters; ++i) OMNI_CUDA(gemm_run(w, x, M, epi, e, cs));
+  OMNI_CUDA(cudaStreamEndCapture(cs, &g));
+  OMNI_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  OMNI_CUDA(cudaGraphLaunch(ge, cs));
+  OMNI_CUDA(cudaStreamSynchronize(cs));
+  cudaEvent_t a, b;
+  OMNI_CUDA(cudaEventCreate(&a));
+  OMNI_CUDA(cudaEventCreate(&b));
+  OMNI_CUDA(cudaEventRecord(a, cs));
+  OMNI_CUDA(cudaGraphLaunch(ge, cs));
+  OMNI_CUDA(cudaEventRecord(b, cs));
+  OMNI_CUDA(cudaEventSynchronize(b));
+  float t = 0;
+  OMNI_CUDA(cudaEventElapsedTime(&t, a, b));
+  *ms = t / iters;
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
+}  // namespace
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+}  // namespace omni_dev
+
+using namespace omni_dev;
+
+extern "C" {
+
+int omni_abi_version(void) { return OMNI_ABI_VERSION; }
+const char* omni_last_error(void) { return g_last_error.c_str(); }
+
+omni_status omni_device_count(int32_t* n) {
+  return guarded([&] {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+    *n = c;
+  });
+}
+
+omni_status omni_mem_alloc(int32_t dev, uint64_t bytes, uint64_t* dev_ptr) {
+  return guarded([&] {
+    require_gpu();
+    OMNI_CUDA(cudaSetDevice(dev));
+    void* p = nullptr;
+    OMNI_CUDA(cudaMalloc(&p, bytes ? bytes : 1));
+    *dev_ptr = reinterpret_cast<uint64_t>(p);
+  });
+}
+omni_status omni_mem_free(uint64_t dev_ptr) {
+  return guarded([&] { OMNI_CUDA(cudaFree(reinterpret_cast<void*>(dev_ptr))); });
+}
+omni_status omni_mem_h2d(uint64_t dst, const void* src, uint64_t bytes) {
+  return guarded([&] {
+    OMNI_CUDA(cudaMemcpy(reinterpret_cast<void*>(dst), src, bytes, cudaMemcpyHostToDevice));
+  });
+}
+omni_status omni_mem_d2h(void* dst, uint64_t src, uint64_t bytes) {
+  return guarded([&] {
+    OMNI_CUDA(cudaMemcpy(dst, reinterpret_cast<const void*>(src), bytes, cudaMemcpyDeviceToHost));
+  });
+}
+omni_status omni_mem_set(uint64_t dst, int32_t byte, uint64_t bytes) {
+  return guarded([&] { OMNI_CUDA(cudaMemset(reinterpret_cast<void*>(dst), byte, bytes)); });
+}
+omni_status omni_device_sync(void) {
+  return guarded([&] { OMNI_CUDA(cudaDeviceSynchronize()); });
+}
+
+omni_status omni_k_gemm(uint64_t W, int32_t N, int32_t K, uint64_t X, int32_t M, int32_t epi,
+                        uint64_t out, int32_t ldo, uint64_t gate, int32_t ldg, int32_t gate_off,
+                        int32_t rows_per_group, int32_t max_splits, int32_t* splits) {
+  return guarded([&] {
+    run_test_gemm(W, N, K, X, M, epi, out, ldo, gate, ldg, gate_off, rows_per_group, splits, 0,
+                  nullptr, max_splits);
+  });
+}
+
+omni_status omni_k_gemm_time(uint64_t W, int32_t N, int32_t K, uint64_t X, int32_t M, int32_t epi,
+                             uint64_t out, int32_t ldo, int32_t max_splits, int32_t iters,
+                             float* ms) {
+  return guarded([&] {
+    run_test_gemm(W, N, K, X, M, epi, out, ldo, 0, 0, 0, 1, nullptr, iters, ms, max_splits);
+  });
+}
+
+omni_status omni_k_fill_weights(uint64_t dst, int64_t n, uint64_t seed, uint32_t tensor_id,
+                                float scale) {
+  return guarded([&] {
+    require_gpu();
+    OMNI_CUDA(fill_weights(reinterpret_cast<__nv_bfloat16*>(dst), n, n, 1, seed, tensor_id, scale, 0));
+    OMNI_CUDA(cudaDeviceSynchronize());
+  });
+}
+
+}  // extern "C"

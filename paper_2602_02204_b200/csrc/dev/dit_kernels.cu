@@ -1,0 +1,189 @@
+// K6: non-GEMM kernels of the token-local DiT denoise step (Code2Wav / image
+// branch). Sequence = the S samples of ONE conditioning token, so a token's
+// output never depends on its neighbours, its chunk, or its batch
+// (chunking transparency, diffusion_engine.hpp:25-27; test_diffusion.cpp:50-65).
+// Replaces the closed-form denoise() of diffusion_engine.hpp:28-43.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "dit_kernels.h"
+#include "ptx.cuh"
+#include "rng.h"
+
+namespace omni_dev {
+
+// x0[row, ch] ~ N(0,1) keyed by (request, global token position, sample, ch).
+__global__ void dit_noise_kernel(const DitTokDesc* __restrict__ toks, int S, int C, uint64_t seed,
+                                 float* __restrict__ x, int rows) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)rows * C) return;
+  const int r = (int)(i / C), ch = (int)(i % C);
+  const DitTokDesc t = toks[r / S];
+  const int s = r % S;
+  x[i] = static_cast<float>(irwin4(noise_hash(seed, t.rid, (uint32_t)t.pos, (uint32_t)s, (uint32_t)ch))) *
+         kNoiseMult;
+}
+
+// cvec[p] = bf16(silu(tok_emb[id_p] + t_emb[step]))
+__global__ void dit_cond_kernel(const DitTokDesc* __restrict__ toks, const __nv_bfloat16* __restrict__ tok_emb,
+                                const __nv_bfloat16* __restrict__ t_emb, int step, int d,
+                                __nv_bfloat16* __restrict__ cvec) {
+  const int p = blockIdx.x;
+  const __nv_bfloat16* e = tok_emb + (size_t)toks[p].id * d;
+  const __nv_bfloat16* te = t_emb + (size_t)step * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = bf2f(e[i]) + bf2f(te[i]);
+    cvec[(size_t)p * d + i] = f2bf(v / (1.f + expf(-v)));
+  }
+}
+
+__global__ void dit_to_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = f2bf(x[i]);
+}
+
+__global__ void dit_add_pos_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ pos_emb,
+                                   int S, int d, int rows) {
+  const int r = blockIdx.x;
+  const __nv_bfloat16* pe = pos_emb + (size_t)(r % S) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) h[(size_t)r * d + i] += bf2f(pe[i]);
+}
+
+__device__ __forceinline__ float block_sum2(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  return t;
+}
+
+// a = bf16(LN(h) * (1 + scale) + shift); mod == nullptr -> plain LN.
+// LN without affine params, eps 1e-6, two-pass (mean, then centred variance).
+__global__ void dit_ln_mod_kernel(const float* __restrict__ h, int d, const float* __restrict__ mod,
+                                  int ld_mod, int shift_off, int scale_off, int S,
+                                  __nv_bfloat16* __restrict__ a) {
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const float* hr = h + (size_t)r * d;
+  float s = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s += hr[i];
+  const float mean = block_sum2(s, red) / d;
+  float v = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float t = hr[i] - mean;
+    v += t * t;
+  }
+  const float inv = rsqrtf(block_sum2(v, red) / d + 1e-6f);
+  const float* mr = mod ? mod + (size_t)(r / S) * ld_mod : nullptr;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float y = (hr[i] - mean) * inv;
+    if (mr) y = y * (1.f + mr[scale_off + i]) + mr[shift_off + i];
+    a[(size_t)r * d + i] = f2bf(y);
+  }
+}
+
+// Attention among the S samples of one token, one CTA per (token, head).
+__global__ void __launch_bounds__(128)
+    dit_attn_kernel(const __nv_bfloat16* __restrict__ qkv, int d, int n_heads,
+                    __nv_bfloat16* __restrict__ out) {
+  constexpr int S = kDitSamples, HD = 128;
+  __shared__ float sq[S][HD + 1], sk[S][HD + 1], sv[S][HD];
+  __shared__ float sp[S][S + 1];
+  const int p = blockIdx.x, h = blockIdx.y;
+  const size_t row0 = (size_t)p * S;
+  const int ld = 3 * d;
+  for (int t = threadIdx.x; t < S * HD; t += blockDim.x) {
+    const int i = t / HD, c = t % HD;
+    const __nv_bfloat16* rp = qkv + (row0 + i) * ld + h * HD + c;
+    sq[i][c] = bf2f(rp[0]);
+    sk[i][c] = bf2f(rp[d]);
+    sv[i][c] = bf2f(rp[2 * d]);
+  }
+  __syncthreads();
+  const float scale = rsqrtf((float)HD);
+  for (int t = threadIdx.x; t < S * S; t += blockDim.x) {
+    const int i = t / S, j = t % S;
+    float acc = 0.f;
+    for (int c = 0; c < HD; ++c) acc += sq[i][c] * sk[j][c];
+    sp[i][j] = acc * scale;
+  }
+  __syncthreads();
+  if (threadIdx.x < S) {
+    const int i = threadIdx.x;
+    float m = -INFINITY;
+    for (int j = 0; j < S; ++j) m = fmaxf(m, sp[i][j]);
+    float l = 0.f;
+    for (int j = 0; j < S; ++j) {
+      const float e = expf(sp[i][j] - m);
+      sp[i][j] = e;
+      l += e;
+    }
+    const float inv = 1.f / l;
+    for (int j = 0; j < S; ++j) sp[i][j] *= inv;
+  }
+  __syncthreads();
+  const int c = threadIdx.x;  // one head dim per thread
+  for (int i = 0; i < S; ++i) {
+    float acc = 0.f;
+    for (int j = 0; j < S; ++j) acc += sp[i][j] * sv[j][c];
+    out[(row0 + i) * d + h * HD + c] = f2bf(acc);
+  }
+}
+
+// x += dt * v; on the final step also quantise channel 0 to an int32 sample.
+__global__ void dit_euler_kernel(float* __restrict__ x, const float* __restrict__ v, int C, int rows,
+                                 float dt, int last, int32_t* __restrict__ samples) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)rows * C) return;
+  const float nx = x[i] + dt * v[i];
+  x[i] = nx;
+  if (last && (i % C) == 0) {
+    float q = rintf(kSampleScale * nx);
+    q = fminf(fmaxf(q, -64.f), 63.f);
+    samples[i / C] = (int32_t)q;
+  }
+}
+
+// ---------------------------------------------------------------------------
+cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t seed, float* x,
+                      cudaStream_t st) {
+  const int rows = n_tok * S;
+  const int64_t n = (int64_t)rows * C;
+  dit_noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(toks, S, C, seed, x, rows);
+  return cudaGetLastError();
+}
+cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
+                     const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st) {
+  dit_cond_kernel<<<n_tok, 256, 0, st>>>(toks, tok_emb, t_emb, step, d, cvec);
+  return cudaGetLastError();
+}
+cudaError_t dit_to_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
+  dit_to_bf16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, y);
+  return cudaGetLastError();
+}
+cudaError_t dit_add_pos(float* h, const __nv_bfloat16* pos_emb, int S, int d, int rows, cudaStream_t st) {
+  dit_add_pos_kernel<<<rows, 256, 0, st>>>(h, pos_emb, S, d, rows);
+  return cudaGetLastError();
+}
+cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod, int ld_mod, int shift_off,
+                       int scale_off, int S, __nv_bfloat16* a, cudaStream_t st) {
+  dit_ln_mod_kernel<<<rows, 256, 0, st>>>(h, d, mod, ld_mod, shift_off, scale_off, S, a);
+  return cudaGetLastError();
+}
+cudaError_t dit_attn(const __nv_bfloat16* qkv, int n_tok, int d, int n_heads, __nv_bfloat16* out,
+                     cudaStream_t st) {
+  dim3 grid(n_tok, n_heads);
+  dit_attn_kernel<<<grid, 128, 0, st>>>(qkv, d, n_heads, out);
+  return cudaGetLastError();
+}
+cudaError_t dit_euler(float* x, const float* v, int C, int rows, float dt, int last, int32_t* samples,
+                      cudaStream_t st) {
+  const int64_t n = (int64_t)rows * C;
+  dit_euler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, v, C, rows, dt, last, samples);
+  return cudaGetLastError();
+}
+
+}  // namespace omni_dev

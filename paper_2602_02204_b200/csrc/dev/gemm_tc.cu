@@ -1,0 +1,291 @@
+// K1: batch-invariant tcgen05/TMA bf16 GEMM  Y[M,N] = X[M,K] · W[N,K]^T.
+//
+// Swap-AB: the weight tile (128 output features) is the MMA "A" operand
+// (M=128), the token tile (BN = 16..256 tokens) the "B" operand, so a decode
+// batch of 1..16 rows still issues full-height MMAs while W streams from HBM
+// exactly once.  Operands are staged by TMA (SWIZZLE_128B) into a STAGES-deep
+// mbarrier ring; one elected thread issues tcgen05.mma into a TMEM accumulator
+// (128 lanes x BN fp32 columns); all four warps drain TMEM with tcgen05.ld and
+// apply the fused epilogue.
+//
+// Batch invariance (SURVEY §0.7a, §7 hard part 1): the split-K factor is a
+// property of the weight (fixed at load time from (N, K)), the split CTAs of
+// a tile form one thread-block cluster and reduce their fp32 partials over
+// DSMEM in fixed rank order, and every output element depends only on its
+// own row of X — so a row's bits are identical for any batch size M.
+//
+// Replaces the per-sequence StageModel::prefill/decode loop
+// (ar_engine.hpp:308-337, reference_pipeline.hpp:96-154) for the dense
+// projections; reused by the DiT (diffusion_engine.hpp:28-43 replacement).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace omni_dev {
+
+namespace {
+
+constexpr int kBlockM = 128;  // weight rows per tile (MMA M)
+constexpr int kBlockK = 64;   // 128-byte swizzle atom of bf16
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float silu(float x) { return x / (1.f + expf(-x)); }
+
+// Applies the fused epilogue to `ncols` finished accumulator columns held in
+// smem as acc[c * 128 + row] (fp32), column c = token tok0 + c.  Thread `row`
+// owns output feature row `row` of the tile; SWIGLU pairs row f (gate) with
+// row f + 64 (up) of the same tile.
+template <int EPI>
+__device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int row, int tok0,
+                                         int ncols, const float* acc) {
+  __syncthreads();
+  if constexpr (EPI == EPI_SWIGLU) {
+    if (row < 64) {
+      const int f = n_tile * 64 + row;
+      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
+      for (int c = 0; c < ncols; ++c) {
+        const float g = acc[c * 128 + row], u = acc[c * 128 + row + 64];
+        out[(size_t)(tok0 + c) * a.ldo + f] = f2bf(silu(g) * u);
+      }
+    }
+  } else {
+    const int n = n_tile * kBlockM + row;
+    if (n >= a.n_valid) return;
+    for (int c = 0; c < ncols; ++c) {
+      const int tok = tok0 + c;
+      const float v = acc[c * 128 + row];
+      if constexpr (EPI == EPI_BF16) {
+        static_cast<__nv_bfloat16*>(a.out)[(size_t)tok * a.ldo + n] = f2bf(v);
+      } else if constexpr (EPI == EPI_F32) {
+        static_cast<float*>(a.out)[(size_t)tok * a.ldo + n] = v;
+      } else if constexpr (EPI == EPI_RESID) {
+        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n;
+        *r = *r + v;
+      } else if constexpr (EPI == EPI_GATED_RESID) {
+        const float g = a.gate[(size_t)(tok / a.rows_per_group) * a.ldg + a.gate_off + n];
+        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n;
+        *r = *r + g * v;
+      } else if constexpr (EPI == EPI_GELU) {
+        static_cast<__nv_bfloat16*>(a.out)[(size_t)tok * a.ldo + n] = f2bf(gelu_tanh(v));
+      }
+    }
+  }
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                   GemmArgs a) {
+  constexpr uint32_t kABytes = kBlockM * kBlockK * 2;
+  constexpr uint32_t kBBytes = BN * kBlockK * 2;
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  constexpr uint32_t kIdesc = idesc_bf16_f32(kBlockM, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * kABytes;
+  constexpr size_t kPipe = (size_t)STAGES * (kABytes + kBBytes);
+  constexpr size_t kEpi = (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (kPipe > kEpi ? kPipe : kEpi));
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
+  const int kb_per = (a.K / kBlockK) / a.splits;
+  const int kb0 = split * kb_per;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmW);
+    prefetch_tmap(&tmX);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
+      const uint64_t pol_x = policy_evict_last();   // activations: shared by all n-tiles
+      for (int i = 0; i < kb_per; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kABytes + kBBytes);
+        const int kx = (kb0 + i) * kBlockK;
+        tma_load_2d(sA + s * kABytes, &tmW, &full[s], kx, n_tile * kBlockM, pol_w);
+        tma_load_2d(sB + s * kBBytes, &tmX, &full[s], kx, m_tile * BN, pol_x);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      for (int i = 0; i < kb_per; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint64_t ad = sdesc_k_sw128(smem_addr(sA + s * kABytes));
+        const uint64_t bd = sdesc_k_sw128(smem_addr(sB + s * kBBytes));
+#pragma unroll
+        for (int k = 0; k < kBlockK / 16; ++k) {
+          // +32 bytes per K=16 step inside the 128-byte swizzle atom (>>4 encoded)
+          tc_mma_bf16(tmem, ad + 2 * k, bd + 2 * k, kIdesc, (i | k) != 0);
+        }
+        tc_commit(&empty[s]);
+      }
+      tc_commit(done);
+    }
+  }
+  __syncwarp();
+
+  // ---- epilogue: TMEM -> smem (fp32, column-major) -> [cluster split-K
+  // reduction over DSMEM in fixed rank order] -> fused op -------------------
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int row = warp * 32 + lane;  // TMEM lane == output feature within tile
+  const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const int m0 = m_tile * BN;
+  const int cols = min(BN, a.M - m0);           // live token columns
+  const int chunks = (cols + 15) / 16;
+  float* red = reinterpret_cast<float*>(smem);  // pipeline smem is free now
+  for (int c = 0; c < chunks; ++c) {
+    float v[16];
+    tmem_ld16(trow + c * 16, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) red[(c * 16 + j) * 128 + row] = v[j];
+  }
+  if (a.splits == 1) {
+    epi_cols<EPI>(a, n_tile, row, m0, cols, red);
+  } else {
+    // The split CTAs of this tile form one cluster (rank == split). Each
+    // reduces a slice of token columns across all ranks, in rank order, so
+    // the sum order never depends on the batch.
+    cluster_sync();
+    const int S = a.splits;
+    const int per = (cols + S - 1) / S;
+    const int c0 = split * per;
+    const int c1 = min(cols, c0 + per);
+    float* fin = red + BN * 128;
+    const uint32_t red_s = smem_addr(red);
+    for (int c = c0; c < c1; ++c) {
+      const uint32_t off = static_cast<uint32_t>((c * 128 + row) * 4);
+      float acc = 0.f;
+      for (int z = 0; z < S; ++z) acc += dsmem_ld_f32(dsmem_map(red_s + off, z));
+      fin[(c - c0) * 128 + row] = acc;
+    }
+    if (c1 > c0) epi_cols<EPI>(a, n_tile, row, m0 + c0, c1 - c0, fin);
+    cluster_sync();  // keep our partial alive until every rank has read it
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_free<kTmemCols>(tmem);
+}
+
+template <int BN>
+constexpr int stages_for() {
+  // two CTAs per SM for the skinny decode tiles, deep rings for the wide ones
+  return BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4;
+}
+template <int BN>
+constexpr size_t epi_smem_for() {
+  return (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
+}
+template <int BN>
+constexpr size_t smem_for() {
+  constexpr size_t pipe = stages_for<BN>() * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
+  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256;
+}
+
+template <int BN, int EPI>
+cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
+                      cudaStream_t st) {
+  auto kern = gemm_tc_kernel<BN, stages_for<BN>(), EPI>;
+  constexpr size_t smem = smem_for<BN>();
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(w.N_pad / kBlockM, (a.M + BN - 1) / BN, a.splits);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = a.splits;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, w.tmap, x.tmap_for(BN), a);
+}
+
+template <int EPI>
+cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
+                       cudaStream_t st) {
+  const int bn = gemm_block_n(a.M);
+  switch (bn) {
+    case 16: return launch_bn<16, EPI>(w, x, a, st);
+    case 32: return launch_bn<32, EPI>(w, x, a, st);
+    case 64: return launch_bn<64, EPI>(w, x, a, st);
+    case 128: return launch_bn<128, EPI>(w, x, a, st);
+    default: return launch_bn<256, EPI>(w, x, a, st);
+  }
+}
+
+}  // namespace
+
+int gemm_block_n(int M) {
+  return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
+}
+
+cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, const GemmEpilogue& e,
+                     cudaStream_t st) {
+  if (M <= 0) return cudaSuccess;
+  if (M > x.rows_cap || w.K != x.K) return cudaErrorInvalidValue;
+  GemmArgs a{};
+  a.M = M;
+  a.N = w.N_pad;
+  a.K = w.K;
+  a.n_valid = w.N;
+  a.splits = w.splits;
+  a.out = e.out;
+  a.ldo = e.ldo;
+  a.gate = e.gate;
+  a.ldg = e.ldg;
+  a.gate_off = e.gate_off;
+  a.rows_per_group = e.rows_per_group > 0 ? e.rows_per_group : 1;
+  if (w.splits > 8 || (a.K / kBlockK) % w.splits != 0) return cudaErrorInvalidValue;
+  switch (epi) {
+    case EPI_BF16: return launch_epi<EPI_BF16>(w, x, a, st);
+    case EPI_F32: return launch_epi<EPI_F32>(w, x, a, st);
+    case EPI_RESID: return launch_epi<EPI_RESID>(w, x, a, st);
+    case EPI_GATED_RESID: return launch_epi<EPI_GATED_RESID>(w, x, a, st);
+    case EPI_SWIGLU: return launch_epi<EPI_SWIGLU>(w, x, a, st);
+    case EPI_GELU: return launch_epi<EPI_GELU>(w, x, a, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace omni_dev

@@ -1,0 +1,113 @@
+// K5: connector gather/pack of thinker hidden rows into the reference wire
+// layout (payload.hpp:142-166) — one launch packs every chunk an iteration
+// emits, straight into the consumer's device arena (local or NVLink peer).
+//
+// Blob of a chunk with n rows:  [u8 dtype=2 FIX16][u8 rank=2][u32 n][u32 1+d]
+// then n x (1+d) little-endian u16: col 0 = token id, cols 1..d = bf16 bits
+// of hidden row (begin + r). Replaces the per-row byte loop of the thinker's
+// pack_chunk (reference_pipeline.hpp:113-123) + encode_payload + stash
+// (connector.hpp:214-236).
+//
+// Every thread produces one aligned 16-byte word of the blob. Interior words
+// (8 hidden elements of one row) are assembled from two 128-bit loads of the
+// 16-B aligned hidden ring with a funnel shift — the row start moves by one
+// u16 per row because of the token column — so both sides of the copy are
+// 128-bit vector accesses; header / token-column / row-crossing words take a
+// scalar path.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "pack_kernels.h"
+#include "ptx.cuh"
+
+namespace omni_dev {
+
+namespace {
+
+__device__ __forceinline__ uint32_t u16_at(const PackChunkDesc& c, const __nv_bfloat16* ring, int d,
+                                           int ring_rows, int64_t u) {
+  // u = u16 slot index within the blob; slots 0..4 are the 10-byte header.
+  if (u < 5) {
+    const uint32_t n = (uint32_t)(c.end - c.begin), w = (uint32_t)(d + 1);
+    switch (u) {
+      case 0: return 2u | (2u << 8);  // dtype FIX16, rank 2
+      case 1: return n & 0xFFFFu;
+      case 2: return n >> 16;
+      case 3: return w & 0xFFFFu;
+      default: return w >> 16;
+    }
+  }
+  const int64_t e = u - 5;
+  const int64_t r = e / (d + 1), col = e % (d + 1);
+  if (col == 0) return (uint32_t)c.tokens_dev[r] & 0xFFFFu;
+  const unsigned short* row =
+      reinterpret_cast<const unsigned short*>(ring + ((size_t)c.slot * ring_rows + c.begin + r) * d);
+  return row[col - 1];
+}
+
+__global__ void pack_hidden_kernel(const PackChunkDesc* __restrict__ chunks,
+                                   const __nv_bfloat16* __restrict__ ring, int d, int ring_rows,
+                                   uint8_t* __restrict__ dst_base) {
+  const PackChunkDesc c = chunks[blockIdx.y];
+  const int64_t rows = c.end - c.begin;
+  const int64_t total_u16 = 5 + rows * (d + 1);
+  const int64_t words = (total_u16 + 7) / 8;
+  uint4* out = reinterpret_cast<uint4*>(dst_base + c.dst_offset);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < words;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u0 = 8 * k;
+    uint32_t w[4];
+    bool fast = false;
+    if (u0 >= 5 && u0 + 7 < total_u16) {
+      const int64_t e0 = u0 - 5;
+      const int64_t r = e0 / (d + 1), col0 = e0 % (d + 1);
+      if (col0 >= 1 && col0 + 7 <= d) {  // 8 hidden values of one row
+        fast = true;
+        const int h0 = (int)col0 - 1;
+        const uint4* src = reinterpret_cast<const uint4*>(
+            ring + ((size_t)c.slot * ring_rows + c.begin + r) * d + (h0 & ~7));
+        const uint4 lo = __ldg(src);
+        const uint4 hi = (h0 & 7) ? __ldg(src + 1) : make_uint4(0, 0, 0, 0);
+        const uint32_t v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        const int sh = h0 & 7;  // start element inside the 16-element window
+        const int q = sh >> 1;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          uint32_t a = 0, b = 0;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)  // select v[q + m], v[q + m + 1] without local memory
+            if (q == t) a = v[t + m], b = v[t + m + 1 < 8 ? t + m + 1 : 7];
+          w[m] = (sh & 1) ? __funnelshift_r(a, b, 16) : a;
+        }
+      }
+    }
+    if (!fast) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int64_t ua = u0 + 2 * m, ub = ua + 1;
+        const uint32_t lo16 = ua < total_u16 ? u16_at(c, ring, d, ring_rows, ua) : 0u;
+        const uint32_t hi16 = ub < total_u16 ? u16_at(c, ring, d, ring_rows, ub) : 0u;
+        w[m] = lo16 | (hi16 << 16);
+      }
+    }
+    out[k] = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+}  // namespace
+
+uint64_t pack_blob_bytes(int rows, int d) { return 10ull + 2ull * (uint64_t)rows * (uint64_t)(d + 1); }
+
+cudaError_t launch_pack_hidden(const PackChunkDesc* chunks_dev, int n_chunks, int max_rows,
+                               const __nv_bfloat16* ring, int d, int ring_rows, uint8_t* dst_base,
+                               cudaStream_t st) {
+  if (n_chunks == 0) return cudaSuccess;
+  const int64_t words = (pack_blob_bytes(max_rows, d) + 15) / 16;
+  const int threads = 256;
+  const int bx = (int)((words + threads - 1) / threads);
+  dim3 grid(bx < 1 ? 1 : bx, n_chunks);
+  pack_hidden_kernel<<<grid, threads, 0, st>>>(chunks_dev, ring, d, ring_rows, dst_base);
+  return cudaGetLastError();
+}
+
+}  // namespace omni_dev

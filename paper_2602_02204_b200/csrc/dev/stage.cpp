@@ -1,0 +1,832 @@
+// Host runtime of libomni_dev: stage construction (random-init weights
+// materialised on device), paged-KV bookkeeping, and the batched AR / DiT
+// step drivers behind the C ABI (include/omni_dev.h).
+#include "stage.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "common.h"
+#include "kernels.h"
+
+using namespace omni_dev;
+
+namespace {
+
+constexpr float kNormEps = 1e-6f;
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+template <typename T>
+T* dev_alloc(omni_stage* st, size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess)
+    throw DevError(OMNI_E_OOM, std::string("cudaMalloc ") + std::to_string(count * sizeof(T)) +
+                                   " bytes: " + cudaGetErrorString(e));
+  st->allocs.push_back(p);
+  return static_cast<T*>(p);
+}
+
+DevTensor make_weight(omni_stage* st, const std::string& name, int64_t rows, int64_t rows_pad,
+                      int64_t cols, uint32_t tid, float scale) {
+  DevTensor t;
+  t.rows = rows;
+  t.rows_pad = rows_pad;
+  t.cols = cols;
+  t.p = dev_alloc<__nv_bfloat16>(st, (size_t)rows_pad * cols);
+  OMNI_CUDA(fill_weights(t.p, rows_pad, rows, cols, st->seed, tid, scale, st->stream));
+  st->weight_bytes += (uint64_t)rows * cols * 2;
+  st->named[name] = t;
+  return t;
+}
+
+DevTensor make_swiglu(omni_stage* st, const std::string& name, int64_t ff, int64_t cols,
+                      uint32_t tid_gate, uint32_t tid_up, float scale) {
+  DevTensor t;
+  t.rows = t.rows_pad = 2 * ff;
+  t.cols = cols;
+  t.p = dev_alloc<__nv_bfloat16>(st, (size_t)2 * ff * cols);
+  OMNI_CUDA(fill_swiglu(t.p, ff, cols, st->seed, tid_gate, tid_up, scale, st->stream));
+  st->weight_bytes += (uint64_t)2 * ff * cols * 2;
+  st->named[name] = t;
+  return t;
+}
+
+GemmWeight gemm_of(const DevTensor& t, int max_splits) {
+  GemmWeight g;
+  OMNI_REQUIRE(gemm_make_weight(g, t.p, (int)t.rows, (int)t.rows_pad, (int)t.cols, max_splits),
+               OMNI_E_BADARG, "weight tensor map encode failed");
+  return g;
+}
+
+GemmInput input_of(const __nv_bfloat16* p, int rows_cap, int K) {
+  GemmInput x;
+  OMNI_REQUIRE(gemm_make_input(x, p, rows_cap, K), OMNI_E_BADARG, "input tensor map encode failed");
+  return x;
+}
+
+void staging_reserve(Staging& s, size_t bytes) {
+  if (bytes <= s.cap) return;
+  if (s.in_use) OMNI_CUDA(cudaEventSynchronize(s.in_use));
+  if (s.host) cudaFreeHost(s.host);
+  if (s.dev) cudaFree(s.dev);
+  size_t cap = std::max<size_t>(bytes, 64 * 1024);
+  OMNI_CUDA(cudaMallocHost(&s.host, cap));
+  OMNI_CUDA(cudaMalloc(&s.dev, cap));
+  s.cap = cap;
+  if (!s.in_use) OMNI_CUDA(cudaEventCreateWithFlags(&s.in_use, cudaEventDisableTiming));
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw DevError(OMNI_E_NOGPU, "no CUDA device visible (libomni_dev has no CPU fallback)");
+}
+
+void ensure_idle(omni_stage* st) {
+  OMNI_REQUIRE(!st->pending, OMNI_E_BADARG,
+               "stage has an unfinished step; call omni_stage_wait/omni_stage_query first");
+}
+
+// ---------------------------------------------------------------------------
+// construction
+// ---------------------------------------------------------------------------
+void build_ar(omni_stage* st) {
+  const auto& m = st->m;
+  OMNI_REQUIRE(m.head_dim == kHeadDim, OMNI_E_BADARG, "head_dim must be 128");
+  OMNI_REQUIRE(m.n_heads % m.n_kv_heads == 0, OMNI_E_BADARG, "n_heads % n_kv_heads != 0");
+  OMNI_REQUIRE(m.d_model % 128 == 0 && m.d_ff % 128 == 0, OMNI_E_BADARG, "dims must be multiples of 128");
+  const int d = m.d_model, L = m.n_layers, H = m.n_heads, KVH = m.n_kv_heads, ff = m.d_ff;
+  const bool talker = m.kind == OMNI_MODEL_TALKER;
+  const float s_d = 1.f / std::sqrt((float)d);
+
+  st->emb = make_weight(st, "embed", 256, 256, d, 1, 1.0f);  // byte-valued token ids
+  st->vocab_pad = round_up(m.vocab, 128);
+  st->lm = make_weight(st, "lm_head", m.vocab, st->vocab_pad, d, 2, 4.0f * s_d);
+  st->glm = gemm_of(st->lm, 8);
+  if (talker) {
+    OMNI_REQUIRE(m.cond_dim % 64 == 0 && m.cond_dim > 0, OMNI_E_BADARG, "talker cond_dim");
+    st->emb2 = make_weight(st, "embed_codec", m.vocab + 1, m.vocab + 1, d, 3, 1.0f);
+    st->whid = make_weight(st, "w_hid", d, d, m.cond_dim, 4, 1.f / std::sqrt((float)m.cond_dim));
+    st->ghid = gemm_of(st->whid, 8);
+    st->start_id = m.vocab;  // codec start id
+    st->argmax_lo = 0;
+  } else {
+    st->start_id = 0;  // reserved id 0 is the thinker start token
+    st->argmax_lo = 1; // outputs live in [1, 255] like token_of (reference_pipeline.hpp:34)
+  }
+  st->argmax_hi = m.vocab;
+  const int qkv_rows = (H + 2 * KVH) * kHeadDim;
+  st->layers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    auto& ly = st->layers[l];
+    const uint32_t b = 16u * (l + 1);
+    const std::string p = "L" + std::to_string(l) + ".";
+    ly.wqkv = make_weight(st, p + "wqkv", qkv_rows, qkv_rows, d, b + 0, s_d);
+    ly.wo = make_weight(st, p + "wo", d, d, H * kHeadDim, b + 1, 1.f / std::sqrt((float)(H * kHeadDim)));
+    ly.wgu = make_swiglu(st, p + "wgu", ff, d, b + 2, b + 3, s_d);
+    ly.wd = make_weight(st, p + "wd", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
+    ly.gqkv = gemm_of(ly.wqkv, 8);
+    ly.go = gemm_of(ly.wo, 8);
+    ly.ggu = gemm_of(ly.wgu, 8);
+    ly.gd = gemm_of(ly.wd, 8);
+  }
+
+  // activations
+  const int R = st->rows_cap = std::max(16, st->lim.max_batch_tokens);
+  st->x = dev_alloc<float>(st, (size_t)R * d);
+  st->xn = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
+  st->qkv = dev_alloc<float>(st, (size_t)R * qkv_rows);
+  st->q = dev_alloc<__nv_bfloat16>(st, (size_t)R * H * kHeadDim);
+  st->attn = dev_alloc<__nv_bfloat16>(st, (size_t)R * H * kHeadDim);
+  st->act = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
+  st->hbuf = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
+  st->logits = dev_alloc<float>(st, (size_t)R * st->vocab_pad);
+  st->d_tok = dev_alloc<int32_t>(st, R);
+  st->d_margin = dev_alloc<float>(st, R);
+  st->in_xn = input_of(st->xn, R, d);
+  st->in_attn = input_of(st->attn, R, H * kHeadDim);
+  st->in_act = input_of(st->act, R, ff);
+  st->in_hbuf = input_of(st->hbuf, R, d);
+  if (talker) {
+    st->condin = dev_alloc<__nv_bfloat16>(st, (size_t)R * m.cond_dim);
+    st->hproj = dev_alloc<float>(st, (size_t)R * d);
+    st->in_cond = input_of(st->condin, R, m.cond_dim);
+    st->cond_table = dev_alloc<float>(st, (size_t)st->lim.max_resident * st->cond_rows * d);
+  } else {
+    st->ring = dev_alloc<__nv_bfloat16>(st, (size_t)st->lim.max_resident * st->ring_rows * d);
+  }
+  // paged KV: [page][layer][k|v][kv_head][16][128] bf16
+  st->max_pages = (st->lim.max_seq_len + kPageTokens - 1) / kPageTokens;
+  int pages = st->lim.kv_pages > 0 ? st->lim.kv_pages : st->lim.max_resident * st->max_pages;
+  st->kv = dev_alloc<__nv_bfloat16>(st, (size_t)pages * L * 2 * KVH * kPageTokens * kHeadDim);
+  st->free_pages.resize(pages);
+  for (int i = 0; i < pages; ++i) st->free_pages[i] = pages - 1 - i;
+  st->free_slots.resize(st->lim.max_resident);
+  for (int i = 0; i < st->lim.max_resident; ++i) st->free_slots[i] = st->lim.max_resident - 1 - i;
+  // RoPE table (theta 10000, rotate-half), computed in double, stored fp32
+  std::vector<float2> rt((size_t)st->lim.max_seq_len * (kHeadDim / 2));
+  for (int pos = 0; pos < st->lim.max_seq_len; ++pos)
+    for (int i = 0; i < kHeadDim / 2; ++i) {
+      const double inv = std::pow(10000.0, -(double)i / (kHeadDim / 2));
+      const double a = pos * inv;
+      rt[(size_t)pos * (kHeadDim / 2) + i] = make_float2((float)std::cos(a), (float)std::sin(a));
+    }
+  st->rope = dev_alloc<float2>(st, rt.size());
+  OMNI_CUDA(cudaMemcpyAsync(st->rope, rt.data(), rt.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                            st->stream));
+  OMNI_CUDA(cudaMallocHost(&st->h_tok, R * sizeof(int32_t)));
+  OMNI_CUDA(cudaMallocHost(&st->h_margin, R * sizeof(float)));
+  OMNI_CUDA(cudaStreamSynchronize(st->stream));
+}
+
+void build_dit(omni_stage* st) {
+  const auto& m = st->m;
+  OMNI_REQUIRE(m.head_dim == 128 && m.dit_samples == kDitSamples, OMNI_E_BADARG,
+               "DiT needs head_dim 128 and 16 samples per token");
+  OMNI_REQUIRE(m.dit_channels % 64 == 0 && m.dit_channels <= 128, OMNI_E_BADARG, "DiT channels");
+  const int d = m.d_model, L = m.n_layers, C = m.dit_channels, ff = m.d_ff;
+  const float s_d = 1.f / std::sqrt((float)d);
+  st->w_in = make_weight(st, "w_in", d, d, C, 1, 1.f / std::sqrt((float)C));
+  st->pos_emb = make_weight(st, "pos_emb", kDitSamples, kDitSamples, d, 2, 0.5f);
+  st->tok_emb = make_weight(st, "tok_emb", m.vocab, m.vocab, d, 3, 1.0f);
+  st->t_emb = make_weight(st, "t_emb", m.dit_steps, m.dit_steps, d, 4, 1.0f);
+  st->w_out = make_weight(st, "w_out", C, round_up(C, 128), d, 5, s_d);
+  st->w_mod = make_weight(st, "w_mod", (int64_t)L * 6 * d, (int64_t)L * 6 * d, d, 6, 0.5f * s_d);
+  st->g_in = gemm_of(st->w_in, 1);
+  st->g_out = gemm_of(st->w_out, 1);
+  st->g_mod = gemm_of(st->w_mod, 1);
+  st->dlayers.resize(L);
+  for (int l = 0; l < L; ++l) {
+    auto& ly = st->dlayers[l];
+    const uint32_t b = 16u * (l + 1);
+    const std::string p = "L" + std::to_string(l) + ".";
+    ly.wqkv = make_weight(st, p + "wqkv", 3 * d, 3 * d, d, b + 1, s_d);
+    ly.wo = make_weight(st, p + "wo", d, d, d, b + 2, s_d);
+    ly.w1 = make_weight(st, p + "w1", ff, ff, d, b + 3, s_d);
+    ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
+    ly.gqkv = gemm_of(ly.wqkv, 1);
+    ly.go = gemm_of(ly.wo, 1);
+    ly.g1 = gemm_of(ly.w1, 1);
+    ly.g2 = gemm_of(ly.w2, 1);
+  }
+  const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
+  const int R = st->drows_cap = T * kDitSamples;
+  st->dx = dev_alloc<float>(st, (size_t)R * C);
+  st->dxin = dev_alloc<__nv_bfloat16>(st, (size_t)R * C);
+  st->dh = dev_alloc<float>(st, (size_t)R * d);
+  st->da = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
+  st->dqkv = dev_alloc<__nv_bfloat16>(st, (size_t)R * 3 * d);
+  st->dout = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
+  st->du = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
+  st->dv = dev_alloc<float>(st, (size_t)R * C);
+  st->dcvec = dev_alloc<__nv_bfloat16>(st, (size_t)T * d);
+  st->dmod = dev_alloc<float>(st, (size_t)T * L * 6 * d);
+  st->dsamples = dev_alloc<int32_t>(st, R);
+  st->din_x = input_of(st->dxin, R, C);
+  st->din_a = input_of(st->da, R, d);
+  st->din_o = input_of(st->dout, R, d);
+  st->din_u = input_of(st->du, R, ff);
+  st->din_c = input_of(st->dcvec, T, d);
+  OMNI_CUDA(cudaMallocHost(&st->h_samples, (size_t)R * sizeof(int32_t)));
+  OMNI_CUDA(cudaStreamSynchronize(st->stream));
+}
+
+void destroy_stage(omni_stage* st) {
+  if (!st) return;
+  cudaSetDevice(st->dev);
+  if (st->stream) cudaStreamSynchronize(st->stream);
+  for (void* p : st->allocs) cudaFree(p);
+  for (Staging* s : {&st->desc, &st->pack}) {
+    if (s->host) cudaFreeHost(s->host);
+    if (s->dev) cudaFree(s->dev);
+    if (s->in_use) cudaEventDestroy(s->in_use);
+  }
+  if (st->h_tok) cudaFreeHost(st->h_tok);
+  if (st->h_margin) cudaFreeHost(st->h_margin);
+  if (st->h_samples) cudaFreeHost(st->h_samples);
+  for (cudaEvent_t e : {st->ev_start, st->ev_done, st->ev_link})
+    if (e) cudaEventDestroy(e);
+  if (st->stream) cudaStreamDestroy(st->stream);
+  delete st;
+}
+
+// ---------------------------------------------------------------------------
+// AR step
+// ---------------------------------------------------------------------------
+SeqSlot& seq_for(omni_stage* st, uint64_t id) {
+  auto it = st->seqs.find(id);
+  if (it != st->seqs.end()) return it->second;
+  OMNI_REQUIRE(!st->free_slots.empty(), OMNI_E_OOM, "no free resident slot on stage");
+  SeqSlot s;
+  s.slot = st->free_slots.back();
+  st->free_slots.pop_back();
+  return st->seqs.emplace(id, std::move(s)).first->second;
+}
+
+void ensure_pages(omni_stage* st, SeqSlot& s, int upto) {
+  const int need = (upto + kPageTokens - 1) / kPageTokens;
+  OMNI_REQUIRE(need <= st->max_pages, OMNI_E_OOM,
+               "sequence longer than max_seq_len (" + std::to_string(st->lim.max_seq_len) + ")");
+  while ((int)s.pages.size() < need) {
+    OMNI_REQUIRE(!st->free_pages.empty(), OMNI_E_OOM, "paged-KV pool exhausted");
+    s.pages.push_back(st->free_pages.back());
+    st->free_pages.pop_back();
+  }
+}
+
+size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
+
+void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* margin_out) {
+  ensure_idle(st);
+  const int ne = b->n_entries;
+  OMNI_REQUIRE(ne >= 0, OMNI_E_BADARG, "n_entries < 0");
+  const bool talker = st->m.kind == OMNI_MODEL_TALKER;
+  int n_rows = 0;
+  for (int e = 0; e < ne; ++e) {
+    OMNI_REQUIRE(b->span[e] >= 1, OMNI_E_BADARG, "entry span < 1");
+    OMNI_REQUIRE(b->phase[e] != OMNI_PHASE_DECODE || b->span[e] == 1, OMNI_E_BADARG,
+                 "decode entries feed exactly one token");
+    n_rows += b->span[e];
+  }
+  OMNI_REQUIRE(n_rows <= st->rows_cap, OMNI_E_BADARG,
+               "batch of " + std::to_string(n_rows) + " tokens exceeds max_batch_tokens");
+  if (talker) OMNI_REQUIRE(b->cond_row != nullptr, OMNI_E_BADARG, "talker step needs cond_row");
+
+  // descriptor blob: entries | rows | page table | decode entry list
+  const size_t off_rows = align16((size_t)ne * sizeof(ArEntryDesc));
+  const size_t off_pt = off_rows + align16((size_t)n_rows * sizeof(ArRowDesc));
+  const size_t off_dec = off_pt + align16((size_t)ne * st->max_pages * sizeof(int32_t));
+  const size_t total = off_dec + align16((size_t)ne * sizeof(int32_t));
+  staging_reserve(st->desc, total);
+  auto* ents = reinterpret_cast<ArEntryDesc*>(st->desc.host);
+  auto* rows = reinterpret_cast<ArRowDesc*>(st->desc.host + off_rows);
+  auto* pt = reinterpret_cast<int32_t*>(st->desc.host + off_pt);
+  auto* dec = reinterpret_cast<int32_t*>(st->desc.host + off_dec);
+  std::vector<int> dec_list;
+  int r = 0, n_prefill_rows = 0;
+  for (int e = 0; e < ne; ++e) {
+    SeqSlot& s = seq_for(st, b->seq_id[e]);
+    ensure_pages(st, s, b->pos0[e] + b->span[e]);
+    const bool is_dec = b->phase[e] == OMNI_PHASE_DECODE;
+    ArEntryDesc& ed = ents[e];
+    ed.slot = s.slot;
+    ed.q_len = b->span[e];
+    ed.pos0 = b->pos0[e];
+    ed.row0 = r;
+    ed.is_decode = is_dec ? 1 : 0;
+    ed.out_index = is_dec ? b->out_index[e] : -1;
+    ed.dec_row = is_dec ? (int)dec_list.size() : -1;
+    ed.pad = 0;
+    if (is_dec) {
+      if (!talker)
+        OMNI_REQUIRE(ed.out_index >= 0 && ed.out_index < st->ring_rows, OMNI_E_BADARG,
+                     "thinker out_index outside the 64-row hidden ring");
+      dec[dec_list.size()] = e;
+      dec_list.push_back(e);
+    }
+    for (size_t k = 0; k < s.pages.size() && (int)k < st->max_pages; ++k)
+      pt[(size_t)e * st->max_pages + k] = s.pages[k];
+    for (int t = 0; t < b->span[e]; ++t, ++r) {
+      ArRowDesc& rd = rows[r];
+      rd.entry = e;
+      rd.pos = b->pos0[e] + t;
+      rd.token = b->tokens[r];
+      rd.cond_row = talker ? b->cond_row[r] : 0;
+      rd.cond_src = (talker && !is_dec && b->cond_src) ? b->cond_src[r] : 0;
+      if (talker) {
+        OMNI_REQUIRE(rd.cond_row >= 0 && rd.cond_row < st->cond_rows, OMNI_E_BADARG,
+                     "talker cond_row outside the 64-row conditioning table");
+        if (!is_dec) {
+          OMNI_REQUIRE(rd.cond_src != 0, OMNI_E_BADARG, "talker prefill token without hidden row");
+          ++n_prefill_rows;
+        }
+      }
+      OMNI_REQUIRE(rd.token >= -1 && rd.token < (talker && is_dec ? st->m.vocab : 256),
+                   OMNI_E_BADARG, "input token id out of range");
+    }
+  }
+  const int n_dec = (int)dec_list.size();
+  cudaStream_t s = st->stream;
+  OMNI_CUDA(cudaEventRecord(st->ev_start, s));
+  OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, total, cudaMemcpyHostToDevice, s));
+  OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
+  ArStepDev sd;
+  sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
+  sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + off_rows);
+  sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + off_pt);
+  sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + off_dec);
+  sd.max_pages = st->max_pages;
+
+  const auto& m = st->m;
+  const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
+  if (n_rows > 0) {
+    if (talker && n_prefill_rows > 0) {
+      OMNI_CUDA(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
+      GemmEpilogue e;
+      e.out = st->hproj;
+      e.ldo = d;
+      OMNI_CUDA(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
+    }
+    OMNI_CUDA(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
+                           st->cond_table, st->cond_rows, d, st->start_id, st->x, s));
+    for (int l = 0; l < L; ++l) {
+      const auto& ly = st->layers[l];
+      OMNI_CUDA(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
+      GemmEpilogue e;
+      e.out = st->qkv;
+      e.ldo = (H + 2 * KVH) * kHeadDim;
+      OMNI_CUDA(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_F32, e, s));
+      OMNI_CUDA(launch_rope_kv(sd, n_rows, st->qkv, H, KVH, st->rope, l, L, st->q, st->kv, s));
+      OMNI_CUDA(launch_attention(sd, ne, st->q, H, KVH, l, L, st->kv, st->attn, s));
+      e.out = st->x;
+      e.ldo = d;
+      OMNI_CUDA(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID, e, s));
+      OMNI_CUDA(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
+      e.out = st->act;
+      e.ldo = m.d_ff;
+      OMNI_CUDA(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
+      e.out = st->x;
+      e.ldo = d;
+      OMNI_CUDA(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID, e, s));
+    }
+    if (n_dec > 0) {
+      OMNI_CUDA(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
+                                    talker ? nullptr : st->ring, st->ring_rows, s));
+      GemmEpilogue e;
+      e.out = st->logits;
+      e.ldo = st->vocab_pad;
+      OMNI_CUDA(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
+      OMNI_CUDA(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
+                              st->d_tok, st->d_margin, s));
+      OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      OMNI_CUDA(cudaMemcpyAsync(st->h_margin, st->d_margin, n_dec * sizeof(float),
+                                cudaMemcpyDeviceToHost, s));
+    }
+  }
+  OMNI_CUDA(cudaEventRecord(st->ev_done, s));
+  st->pending = true;
+  st->pending_kind = 1;
+  st->pending_dec_entries = std::move(dec_list);
+  st->pending_entries = ne;
+  st->user_tok = tok_out;
+  st->user_margin = margin_out;
+}
+
+// ---------------------------------------------------------------------------
+// DiT step
+// ---------------------------------------------------------------------------
+void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
+  const auto& m = st->m;
+  const int d = m.d_model, L = m.n_layers, C = m.dit_channels, S = kDitSamples, T = m.dit_steps;
+  const int rows = n_tok * S;
+  const int ld_mod = L * 6 * d;
+  cudaStream_t s = st->stream;
+  OMNI_CUDA(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, s));
+  for (int t = 0; t < T; ++t) {
+    OMNI_CUDA(dit_cond(toks_dev, n_tok, st->tok_emb.p, st->t_emb.p, t, d, st->dcvec, s));
+    GemmEpilogue e;
+    e.out = st->dmod;
+    e.ldo = ld_mod;
+    OMNI_CUDA(gemm_run(st->g_mod, st->din_c, n_tok, EPI_F32, e, s));
+    OMNI_CUDA(dit_to_bf16(st->dx, (int64_t)rows * C, st->dxin, s));
+    e.out = st->dh;
+    e.ldo = d;
+    OMNI_CUDA(gemm_run(st->g_in, st->din_x, rows, EPI_F32, e, s));
+    OMNI_CUDA(dit_add_pos(st->dh, st->pos_emb.p, S, d, rows, s));
+    for (int l = 0; l < L; ++l) {
+      const auto& ly = st->dlayers[l];
+      const int base = l * 6 * d;
+      OMNI_CUDA(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 0, base + d, S, st->da, s));
+      e = GemmEpilogue{};
+      e.out = st->dqkv;
+      e.ldo = 3 * d;
+      OMNI_CUDA(gemm_run(ly.gqkv, st->din_a, rows, EPI_BF16, e, s));
+      OMNI_CUDA(dit_attn(st->dqkv, n_tok, d, m.n_heads, st->dout, s));
+      e = GemmEpilogue{};
+      e.out = st->dh;
+      e.ldo = d;
+      e.gate = st->dmod;
+      e.ldg = ld_mod;
+      e.gate_off = base + 2 * d;
+      e.rows_per_group = S;
+      OMNI_CUDA(gemm_run(ly.go, st->din_o, rows, EPI_GATED_RESID, e, s));
+      OMNI_CUDA(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 3 * d, base + 4 * d, S, st->da, s));
+      GemmEpilogue e1;
+      e1.out = st->du;
+      e1.ldo = m.d_ff;
+      OMNI_CUDA(gemm_run(ly.g1, st->din_a, rows, EPI_GELU, e1, s));
+      e.gate_off = base + 5 * d;
+      OMNI_CUDA(gemm_run(ly.g2, st->din_u, rows, EPI_GATED_RESID, e, s));
+    }
+    OMNI_CUDA(dit_ln_mod(st->dh, rows, d, nullptr, 0, 0, 0, S, st->da, s));
+    GemmEpilogue eo;
+    eo.out = st->dv;
+    eo.ldo = C;
+    OMNI_CUDA(gemm_run(st->g_out, st->din_a, rows, EPI_F32, eo, s));
+    OMNI_CUDA(dit_euler(st->dx, st->dv, C, rows, 1.f / T, t == T - 1, samples_dev, s));
+  }
+}
+
+void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
+  ensure_idle(st);
+  OMNI_REQUIRE(st->m.kind == OMNI_MODEL_DIT, OMNI_E_BADARG, "not a DiT stage");
+  int64_t n_tok = 0;
+  for (int j = 0; j < b->n_jobs; ++j) {
+    OMNI_REQUIRE(b->n_tokens[j] >= 0 && b->token_offset[j] >= 0, OMNI_E_BADARG, "bad DiT job");
+    n_tok += b->n_tokens[j];
+  }
+  const size_t bytes = align16((size_t)n_tok * sizeof(DitTokDesc));
+  staging_reserve(st->desc, bytes);
+  auto* toks = reinterpret_cast<DitTokDesc*>(st->desc.host);
+  int64_t k = 0;
+  for (int j = 0; j < b->n_jobs; ++j)
+    for (int i = 0; i < b->n_tokens[j]; ++i, ++k) {
+      const int id = b->tokens[k];
+      OMNI_REQUIRE(id >= 0 && id < st->m.vocab, OMNI_E_BADARG,
+                   "DiT conditioning id out of range (the reference demands I32 codec tokens, "
+                   "diffusion_engine.hpp:29-30)");
+      toks[k] = DitTokDesc{b->request_id[j], b->token_offset[j] + i, id};
+    }
+  cudaStream_t s = st->stream;
+  OMNI_CUDA(cudaEventRecord(st->ev_start, s));
+  if (n_tok > 0) {
+    OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, bytes, cudaMemcpyHostToDevice, s));
+    OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
+    const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
+    for (int64_t t0 = 0; t0 < n_tok; t0 += st->tok_cap) {
+      const int nt = (int)std::min<int64_t>(st->tok_cap, n_tok - t0);
+      dit_chunk(st, toks_dev + t0, nt, st->dsamples);
+      const int64_t nsamp = (int64_t)nt * kDitSamples;
+      OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
+                                cudaMemcpyDeviceToHost, s));
+      if (n_tok > st->tok_cap) {  // multi-chunk: land each chunk before reusing h_samples
+        OMNI_CUDA(cudaStreamSynchronize(s));
+        std::memcpy(samples_out + t0 * kDitSamples, st->h_samples, nsamp * sizeof(int32_t));
+      }
+    }
+  }
+  OMNI_CUDA(cudaEventRecord(st->ev_done, s));
+  st->pending = true;
+  st->pending_kind = 2;
+  st->user_samples = (n_tok > st->tok_cap) ? nullptr : samples_out;
+  st->pending_samples = n_tok * kDitSamples;
+}
+
+void finish_pending(omni_stage* st) {
+  if (!st->pending) return;
+  st->pending = false;
+  if (st->pending_kind == 1) {
+    if (st->user_tok || st->user_margin) {
+      for (int e = 0; e < st->pending_entries; ++e) {
+        if (st->user_tok) st->user_tok[e] = -1;
+        if (st->user_margin) st->user_margin[e] = 0.f;
+      }
+      for (size_t i = 0; i < st->pending_dec_entries.size(); ++i) {
+        const int e = st->pending_dec_entries[i];
+        if (st->user_tok) st->user_tok[e] = st->h_tok[i];
+        if (st->user_margin) st->user_margin[e] = st->h_margin[i];
+      }
+    }
+  } else if (st->pending_kind == 2 && st->user_samples) {
+    std::memcpy(st->user_samples, st->h_samples, st->pending_samples * sizeof(int32_t));
+  }
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, st->ev_start, st->ev_done) == cudaSuccess) st->last_step_us = ms * 1e3f;
+}
+
+std::mutex g_init_mu;
+
+}  // namespace
+
+struct omni_arena {
+  int dev = 0;
+  uint8_t* base = nullptr;
+  uint64_t bytes = 0;
+};
+
+extern "C" {
+
+omni_status omni_init(int32_t n_dev, const int32_t* dev_ids) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_init_mu);
+    require_device();
+    std::vector<int> ids;
+    if (n_dev <= 0) ids.push_back(0);
+    for (int i = 0; i < n_dev; ++i) ids.push_back(dev_ids[i]);
+    for (int a : ids) {
+      OMNI_CUDA(cudaSetDevice(a));
+      int major = 0;
+      OMNI_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, a));
+      OMNI_REQUIRE(major == 10, OMNI_E_NOGPU, "libomni_dev is built for sm_100a only");
+      for (int b : ids) {
+        if (a == b) continue;
+        int can = 0;
+        OMNI_CUDA(cudaDeviceCanAccessPeer(&can, a, b));
+        if (can) {
+          cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+          if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+          else OMNI_CUDA(e);
+        }
+      }
+    }
+    OMNI_CUDA(cudaSetDevice(ids[0]));
+  });
+}
+
+omni_status omni_model_default(int32_t kind, omni_model_desc* out) {
+  return guarded([&] {
+    omni_model_desc m{};
+    m.kind = kind;
+    m.head_dim = 128;
+    if (kind == OMNI_MODEL_THINKER || kind == OMNI_MODEL_TALKER) {
+      m.d_model = 2048;
+      m.n_layers = kind == OMNI_MODEL_THINKER ? 8 : 4;
+      m.n_heads = 16;
+      m.n_kv_heads = 4;
+      m.d_ff = 8192;
+      m.vocab = kind == OMNI_MODEL_THINKER ? 256 : 64;
+      m.cond_dim = kind == OMNI_MODEL_TALKER ? 2048 : 0;
+    } else if (kind == OMNI_MODEL_DIT) {
+      m.d_model = 1024;
+      m.n_layers = 4;
+      m.n_heads = 8;
+      m.n_kv_heads = 8;
+      m.d_ff = 4096;
+      m.vocab = 256;
+      m.dit_channels = 64;
+      m.dit_samples = 16;
+      m.dit_steps = 4;
+    } else {
+      throw DevError(OMNI_E_BADARG, "unknown model kind");
+    }
+    *out = m;
+  });
+}
+
+omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_limits* limits,
+                              int32_t dev, uint64_t weight_seed, omni_stage** out) {
+  omni_stage* st = nullptr;
+  omni_status rc = guarded([&] {
+    require_device();
+    OMNI_REQUIRE(model && limits && out, OMNI_E_BADARG, "null argument");
+    st = new omni_stage();
+    st->m = *model;
+    st->lim = *limits;
+    st->dev = dev;
+    st->seed = weight_seed;
+    if (st->lim.max_batch_tokens <= 0) st->lim.max_batch_tokens = 256;
+    if (st->lim.max_resident <= 0) st->lim.max_resident = 64;
+    if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;
+    if (st->lim.dit_max_tokens <= 0) st->lim.dit_max_tokens = 512;
+    OMNI_CUDA(cudaSetDevice(dev));
+    OMNI_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+    OMNI_CUDA(cudaEventCreate(&st->ev_start));
+    OMNI_CUDA(cudaEventCreate(&st->ev_done));
+    OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_link, cudaEventDisableTiming));
+    if (model->kind == OMNI_MODEL_DIT) build_dit(st);
+    else if (model->kind == OMNI_MODEL_THINKER || model->kind == OMNI_MODEL_TALKER) build_ar(st);
+    else throw DevError(OMNI_E_BADARG, "unknown model kind");
+    *out = st;
+  });
+  if (rc != OMNI_OK && st) destroy_stage(st);
+  return rc;
+}
+
+omni_status omni_stage_destroy(omni_stage* st) {
+  return guarded([&] { destroy_stage(st); });
+}
+
+omni_status omni_stage_weight_bytes(const omni_stage* st, uint64_t* bytes) {
+  return guarded([&] { *bytes = st->weight_bytes; });
+}
+
+omni_status omni_stage_tensor(const omni_stage* st, const char* name, uint64_t* dev_ptr, int64_t* rows,
+                              int64_t* cols) {
+  return guarded([&] {
+    const std::string n(name ? name : "");
+    auto it = st->named.find(n);
+    if (it != st->named.end()) {
+      *dev_ptr = reinterpret_cast<uint64_t>(it->second.p);
+      if (rows) *rows = it->second.rows_pad;
+      if (cols) *cols = it->second.cols;
+      return;
+    }
+    if (n == "buf.logits") {
+      *dev_ptr = reinterpret_cast<uint64_t>(st->logits);
+      if (rows) *rows = st->rows_cap;
+      if (cols) *cols = st->vocab_pad;
+      return;
+    }
+    if (n == "buf.dit_x") {
+      *dev_ptr = reinterpret_cast<uint64_t>(st->dx);
+      if (rows) *rows = st->drows_cap;
+      if (cols) *cols = st->m.dit_channels;
+      return;
+    }
+    if (n == "buf.x") {
+      *dev_ptr = reinterpret_cast<uint64_t>(st->x);
+      if (rows) *rows = st->rows_cap;
+      if (cols) *cols = st->m.d_model;
+      return;
+    }
+    throw DevError(OMNI_E_BADARG, "unknown tensor " + n);
+  });
+}
+
+omni_status omni_ar_step(omni_stage* st, const omni_ar_batch* batch, int32_t* token_out,
+                         float* margin_out) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && batch, OMNI_E_BADARG, "null argument");
+    OMNI_REQUIRE(st->m.kind != OMNI_MODEL_DIT, OMNI_E_BADARG, "omni_ar_step on a DiT stage");
+    OMNI_CUDA(cudaSetDevice(st->dev));
+    ar_step(st, batch, token_out, margin_out);
+  });
+}
+
+omni_status omni_seq_release(omni_stage* st, uint64_t seq_id) {
+  return guarded([&] {
+    auto it = st->seqs.find(seq_id);
+    if (it == st->seqs.end()) return;
+    // Pages may still be read by an in-flight step on this stage's stream;
+    // stream order makes reuse by a later step safe.
+    for (int p : it->second.pages) st->free_pages.push_back(p);
+    st->free_slots.push_back(it->second.slot);
+    st->seqs.erase(it);
+  });
+}
+
+omni_status omni_seq_hidden_row(omni_stage* st, uint64_t seq_id, int32_t index, uint64_t* dev_ptr) {
+  return guarded([&] {
+    OMNI_REQUIRE(st->ring != nullptr, OMNI_E_BADARG, "stage has no hidden ring (not a thinker)");
+    auto it = st->seqs.find(seq_id);
+    OMNI_REQUIRE(it != st->seqs.end(), OMNI_E_BADARG, "unknown sequence");
+    OMNI_REQUIRE(index >= 0 && index < st->ring_rows, OMNI_E_BADARG, "hidden row index");
+    *dev_ptr = reinterpret_cast<uint64_t>(
+        st->ring + ((size_t)it->second.slot * st->ring_rows + index) * st->m.d_model);
+  });
+}
+
+omni_status omni_dit_step(omni_stage* st, const omni_dit_batch* batch, int32_t* samples_out) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && batch, OMNI_E_BADARG, "null argument");
+    OMNI_CUDA(cudaSetDevice(st->dev));
+    dit_step(st, batch, samples_out);
+  });
+}
+
+omni_status omni_stage_query(omni_stage* st) {
+  omni_status rc = OMNI_OK;
+  omni_status g = guarded([&] {
+    if (!st->pending) return;
+    cudaError_t e = cudaEventQuery(st->ev_done);
+    if (e == cudaErrorNotReady) {
+      rc = OMNI_EAGAIN;
+      return;
+    }
+    OMNI_CUDA(e);
+    finish_pending(st);
+  });
+  return g != OMNI_OK ? g : rc;
+}
+
+omni_status omni_stage_wait(omni_stage* st) {
+  return guarded([&] {
+    if (!st->pending) return;
+    OMNI_CUDA(cudaEventSynchronize(st->ev_done));
+    finish_pending(st);
+  });
+}
+
+omni_status omni_stage_last_step_us(omni_stage* st, float* us) {
+  return guarded([&] { *us = st->last_step_us; });
+}
+
+omni_status omni_arena_create(int32_t dev, uint64_t bytes, omni_arena** out) {
+  return guarded([&] {
+    require_device();
+    auto* a = new omni_arena();
+    a->dev = dev;
+    a->bytes = bytes;
+    OMNI_CUDA(cudaSetDevice(dev));
+    cudaError_t e = cudaMalloc(&a->base, bytes);
+    if (e != cudaSuccess) {
+      delete a;
+      throw DevError(OMNI_E_OOM, "arena allocation failed");
+    }
+    *out = a;
+  });
+}
+
+omni_status omni_arena_destroy(omni_arena* a) {
+  return guarded([&] {
+    if (!a) return;
+    cudaSetDevice(a->dev);
+    cudaDeviceSynchronize();
+    cudaFree(a->base);
+    delete a;
+  });
+}
+
+omni_status omni_arena_base(const omni_arena* a, uint64_t* dev_ptr, uint64_t* bytes) {
+  return guarded([&] {
+    *dev_ptr = reinterpret_cast<uint64_t>(a->base);
+    if (bytes) *bytes = a->bytes;
+  });
+}
+
+uint64_t omni_pack_bytes(int32_t rows, int32_t d) { return pack_blob_bytes(rows, d); }
+
+omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* seq_id,
+                             const int32_t* begin, const int32_t* end, const int32_t* tokens,
+                             uint64_t dst_base, const uint64_t* dst_offset) {
+  return guarded([&] {
+    OMNI_REQUIRE(src->ring != nullptr, OMNI_E_BADARG, "pack source is not a thinker stage");
+    if (n_chunks <= 0) return;
+    OMNI_CUDA(cudaSetDevice(src->dev));
+    int total_rows = 0, max_rows = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      OMNI_REQUIRE(begin[c] >= 0 && end[c] >= begin[c] && end[c] <= src->ring_rows, OMNI_E_BADARG,
+                   "pack row range");
+      OMNI_REQUIRE(dst_offset[c] % 16 == 0, OMNI_E_BADARG, "pack destination must be 16-B aligned");
+      total_rows += end[c] - begin[c];
+      max_rows = std::max(max_rows, end[c] - begin[c]);
+    }
+    const size_t off_tok = align16((size_t)n_chunks * sizeof(PackChunkDesc));
+    const size_t total = off_tok + align16((size_t)std::max(1, total_rows) * sizeof(int32_t));
+    if (src->pack.in_use) OMNI_CUDA(cudaEventSynchronize(src->pack.in_use));
+    staging_reserve(src->pack, total);
+    auto* cd = reinterpret_cast<PackChunkDesc*>(src->pack.host);
+    auto* tk = reinterpret_cast<int32_t*>(src->pack.host + off_tok);
+    const auto* tk_dev = reinterpret_cast<const int32_t*>(src->pack.dev + off_tok);
+    int at = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+      auto it = src->seqs.find(seq_id[c]);
+      OMNI_REQUIRE(it != src->seqs.end(), OMNI_E_BADARG, "pack of unknown sequence");
+      cd[c] = PackChunkDesc{it->second.slot, begin[c], end[c], 0, dst_offset[c], tk_dev + at};
+      for (int r = begin[c]; r < end[c]; ++r, ++at) tk[at] = tokens[at];
+    }
+    cudaStream_t s = src->stream;
+    OMNI_CUDA(cudaMemcpyAsync(src->pack.dev, src->pack.host, total, cudaMemcpyHostToDevice, s));
+    OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));
+    OMNI_CUDA(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(src->pack.dev), n_chunks,
+                                 max_rows, src->ring, src->m.d_model, src->ring_rows,
+                                 reinterpret_cast<uint8_t*>(dst_base), s));
+  });
+}
+
+omni_status omni_stage_after(omni_stage* dst, omni_stage* src) {
+  return guarded([&] {
+    OMNI_CUDA(cudaSetDevice(src->dev));
+    OMNI_CUDA(cudaEventRecord(src->ev_link, src->stream));
+    OMNI_CUDA(cudaSetDevice(dst->dev));
+    OMNI_CUDA(cudaStreamWaitEvent(dst->stream, src->ev_link, 0));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// Device-side stage runtime (one model instance on one GPU). Internal.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "ar_kernels.h"
+#include "dit_kernels.h"
+#include "gemm.h"
+#include "omni_dev.h"
+#include "pack_kernels.h"
+
+namespace omni_dev {
+
+struct DevTensor {
+  __nv_bfloat16* p = nullptr;
+  int64_t rows = 0, rows_pad = 0, cols = 0;
+};
+
+struct ArLayer {
+  DevTensor wqkv, wo, wgu, wd;
+  GemmWeight gqkv, go, ggu, gd;
+};
+
+struct DitLayer {
+  DevTensor wqkv, wo, w1, w2;
+  GemmWeight gqkv, go, g1, g2;
+};
+
+struct SeqSlot {
+  int slot = -1;
+  std::vector<int> pages;
+};
+
+// Pinned host staging + device mirror for per-step descriptors.
+struct Staging {
+  uint8_t* host = nullptr;
+  uint8_t* dev = nullptr;
+  size_t cap = 0;
+  cudaEvent_t in_use = nullptr;  // last copy that read `host`
+};
+
+}  // namespace omni_dev
+
+struct omni_stage {
+  omni_model_desc m{};
+  omni_stage_limits lim{};
+  int dev = 0;
+  uint64_t seed = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_link = nullptr;
+  std::vector<void*> allocs;
+  std::unordered_map<std::string, omni_dev::DevTensor> named;
+  uint64_t weight_bytes = 0;
+
+  // ---- AR model ----
+  omni_dev::DevTensor emb, emb2, lm, whid;
+  omni_dev::GemmWeight glm, ghid;
+  std::vector<omni_dev::ArLayer> layers;
+  int vocab_pad = 0, start_id = 0, argmax_lo = 0, argmax_hi = 0;
+  int rows_cap = 0, max_pages = 0, ring_rows = 64, cond_rows = 64;
+  float* x = nullptr;
+  __nv_bfloat16* xn = nullptr;
+  float* qkv = nullptr;
+  __nv_bfloat16* q = nullptr;
+  __nv_bfloat16* attn = nullptr;
+  __nv_bfloat16* act = nullptr;
+  __nv_bfloat16* hbuf = nullptr;
+  __nv_bfloat16* condin = nullptr;
+  float* hproj = nullptr;
+  float* logits = nullptr;
+  int32_t* d_tok = nullptr;
+  float* d_margin = nullptr;
+  float* cond_table = nullptr;
+  __nv_bfloat16* ring = nullptr;
+  __nv_bfloat16* kv = nullptr;
+  float2* rope = nullptr;
+  omni_dev::GemmInput in_xn, in_attn, in_act, in_hbuf, in_cond;
+  std::unordered_map<uint64_t, omni_dev::SeqSlot> seqs;
+  std::vector<int> free_slots, free_pages;
+
+  // ---- DiT model ----
+  omni_dev::DevTensor w_in, pos_emb, tok_emb, t_emb, w_out, w_mod;
+  omni_dev::GemmWeight g_in, g_out, g_mod;
+  std::vector<omni_dev::DitLayer> dlayers;
+  int tok_cap = 0, drows_cap = 0;
+  float *dx = nullptr, *dh = nullptr, *dv = nullptr, *dmod = nullptr;
+  __nv_bfloat16 *dxin = nullptr, *da = nullptr, *dqkv = nullptr, *dout = nullptr, *du = nullptr,
+                *dcvec = nullptr;
+  int32_t* dsamples = nullptr;
+  omni_dev::GemmInput din_x, din_a, din_o, din_u, din_c;
+
+  // ---- step staging / results ----
+  omni_dev::Staging desc, pack;
+  int32_t* h_tok = nullptr;
+  float* h_margin = nullptr;
+  int32_t* h_samples = nullptr;
+  bool pending = false;
+  int pending_kind = 0;  // 1 = AR, 2 = DiT
+  std::vector<int> pending_dec_entries;
+  int pending_entries = 0;
+  int32_t* user_tok = nullptr;
+  float* user_margin = nullptr;
+  int32_t* user_samples = nullptr;
+  int64_t pending_samples = 0;
+  float last_step_us = 0.f;
+};
