@@ -21,7 +21,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-CXX = os.environ.get("CXX", "g++")
+CXX = "g++"  # PATH g++ (an env CXX wrapper in this image drops libstdc++)
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 JSON_INC = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,0 +1,516 @@
+// B200 stage plugins over the libomni_dev C ABI (include/omni_dev.h).
+//
+//   thinker_forward  StageModel: host keeps the reference's length semantics
+//                    (fold_prompt / target_length, reference_pipeline.hpp:24-32,
+//                    98-103); every iteration is ONE omni_ar_step; chunks are
+//                    FIX16 {n, 1+d} payloads packed on device (omni_pack_hidden)
+//                    into the consumer's arena — one pack launch per iteration.
+//   talker_forward   StageModel: target_len = 4 x |prompt| (:133-135); prefill
+//                    rows read the thinker hidden rows straight from the arena.
+//   ar_forward       thinker model whose chunks are plain I32 tokens (:227-234).
+//   process_input    Talker preprocess over device chunks (:159-190 semantics).
+//   Thinker2Talker / Talker2Vocoder   transfers (:192-223).
+//   denoise          DiffusionModel: ONE omni_dit_step per diffusion iteration.
+#include "omni/b200_pipeline.hpp"
+
+#include <algorithm>
+#include <unordered_map>
+
+#include "omni/errors.hpp"
+
+namespace omni {
+
+namespace {
+
+void dev_ok(omni_status s, const char* what) {
+  if (s != OMNI_OK) throw DeviceError(std::string(what) + ": " + omni_last_error());
+}
+
+uint32_t mix(uint32_t h, uint32_t t) { return h * 1000003u + t + 1u; }  // reference_pipeline.hpp:20-22
+
+// First-fit allocator over a device arena; blocks are owned per request and
+// released when the request leaves the pipeline (connector cleanup).
+class Arena {
+ public:
+  Arena(int dev, uint64_t bytes) : bytes_(bytes) {
+    dev_ok(omni_arena_create(dev, bytes, &arena_), "omni_arena_create");
+    dev_ok(omni_arena_base(arena_, &base_, nullptr), "omni_arena_base");
+    free_[0] = bytes;
+  }
+  ~Arena() { omni_arena_destroy(arena_); }
+  uint64_t base() const { return base_; }
+  uint64_t alloc(uint64_t rid, uint64_t n) {
+    n = (n + 255) & ~uint64_t(255);
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second < n) continue;
+      const uint64_t off = it->first, rest = it->second - n;
+      free_.erase(it);
+      if (rest) free_[off + n] = rest;
+      owned_[rid].push_back({off, n});
+      return off;
+    }
+    throw RegionFull("hidden-state arena exhausted (" + std::to_string(bytes_) + " bytes)");
+  }
+  void release(uint64_t rid) {
+    auto it = owned_.find(rid);
+    if (it == owned_.end()) return;
+    for (auto [off, n] : it->second) {
+      auto nx = free_.emplace(off, n).first;
+      if (auto after = std::next(nx); after != free_.end() && nx->first + nx->second == after->first) {
+        nx->second += after->second;
+        free_.erase(after);
+      }
+      if (nx != free_.begin()) {
+        auto before = std::prev(nx);
+        if (before->first + before->second == nx->first) {
+          before->second += nx->second;
+          free_.erase(nx);
+        }
+      }
+    }
+    owned_.erase(it);
+  }
+
+ private:
+  omni_arena* arena_ = nullptr;
+  uint64_t base_ = 0, bytes_ = 0;
+  std::map<uint64_t, uint64_t> free_;
+  std::unordered_map<uint64_t, std::vector<std::pair<uint64_t, uint64_t>>> owned_;
+};
+
+struct ArStage {
+  std::string name;
+  int kind = OMNI_MODEL_THINKER;
+  int dev = 0;
+  omni_model_desc model{};
+  omni_stage* st = nullptr;
+  bool pack_hidden = false;  // thinker_forward: FIX16 device chunks
+  std::unique_ptr<Arena> arena;
+  ArStage* upstream = nullptr;  // talker: the stage whose arena it reads
+  Tracer* tracer = nullptr;
+  // step arrays (kept alive until the step completes)
+  std::vector<uint64_t> seq_id, cond_src;
+  std::vector<int32_t> phase, span, pos0, out_index, tokens, cond_row, tok_out;
+  std::vector<float> margin_out;
+  bool in_flight = false;
+  double dev_ms = 0;
+  uint64_t steps = 0;
+  // deferred packs of the current iteration
+  struct Pack {
+    uint64_t rid;
+    int32_t begin, end;
+    uint64_t offset;
+  };
+  std::vector<Pack> packs;
+  std::vector<int32_t> pack_tokens;
+
+  ~ArStage() {
+    if (st) omni_stage_destroy(st);
+  }
+
+  void launch(std::vector<BatchSlot>& slots) {
+    const size_t n = slots.size();
+    seq_id.resize(n);
+    phase.resize(n);
+    span.resize(n);
+    pos0.resize(n);
+    out_index.resize(n);
+    tok_out.assign(n, -1);
+    margin_out.assign(n, 0.f);
+    tokens.clear();
+    cond_src.clear();
+    cond_row.clear();
+    const bool talker = kind == OMNI_MODEL_TALKER;
+    bool reads_rows = false;
+    for (size_t i = 0; i < n; ++i) {
+      const BatchSlot& b = slots[i];
+      const SeqState& s = *b.seq;
+      seq_id[i] = b.request_id;
+      phase[i] = b.phase == Phase::DECODE ? OMNI_PHASE_DECODE : OMNI_PHASE_PREFILL;
+      span[i] = static_cast<int32_t>(b.span);
+      pos0[i] = static_cast<int32_t>(b.pos0);
+      out_index[i] = b.out_index;
+      if (b.phase == Phase::PREFILL) {
+        for (uint32_t t = 0; t < b.span; ++t) {
+          const size_t j = b.pos0 + t;
+          tokens.push_back(s.prompt[j]);
+          if (talker) {
+            if (j >= s.prompt_rows.size()) throw ForwardError("talker prompt row without a hidden row");
+            cond_src.push_back(s.prompt_rows[j]);
+            cond_row.push_back(static_cast<int32_t>(j));
+            reads_rows = true;
+          }
+        }
+      } else {
+        const int32_t k = b.out_index;
+        tokens.push_back(k == 0 ? -1 : s.emitted[static_cast<size_t>(k - 1)]);
+        if (talker) {
+          cond_src.push_back(0);
+          cond_row.push_back(k / 4);  // row j = m / 4 (reference_pipeline.hpp:137-139)
+        }
+      }
+      if (tracer && b.phase == Phase::DECODE)
+        tracer->out += "D " + name + " " + std::to_string(tracer->now()) + " " + std::to_string(b.request_id) +
+                       " " + std::to_string(b.out_index) + "\n";
+    }
+    if (reads_rows && upstream) dev_ok(omni_stage_after(st, upstream->st), "omni_stage_after");
+    omni_ar_batch batch{};
+    batch.n_entries = static_cast<int32_t>(n);
+    batch.seq_id = seq_id.data();
+    batch.phase = phase.data();
+    batch.span = span.data();
+    batch.pos0 = pos0.data();
+    batch.out_index = out_index.data();
+    batch.tokens = tokens.data();
+    if (talker) {
+      batch.cond_src = cond_src.data();
+      batch.cond_row = cond_row.data();
+    }
+    dev_ok(omni_ar_step(st, &batch, tok_out.data(), margin_out.data()), "omni_ar_step");
+    in_flight = true;
+  }
+
+  bool ready() {
+    const omni_status s = omni_stage_query(st);
+    if (s == OMNI_EAGAIN) return false;
+    dev_ok(s, "omni_stage_query");
+    return true;
+  }
+
+  void collect(std::vector<BatchSlot>& slots, std::vector<int32_t>& out) {
+    dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    in_flight = false;
+    float us = 0;
+    omni_stage_last_step_us(st, &us);
+    dev_ms += us / 1e3;
+    ++steps;
+    for (size_t i = 0; i < slots.size(); ++i) {
+      out[i] = tok_out[i];
+      if (slots[i].phase == Phase::DECODE && tok_out[i] < 0) throw ForwardError("device step returned no token");
+    }
+  }
+
+  Payload pack_chunk(const SeqState& s, size_t b, size_t e) {
+    if (tracer)
+      tracer->out += "K " + name + " " + std::to_string(tracer->now()) + " " + std::to_string(s.request_id) +
+                     " " + std::to_string(b) + " " + std::to_string(e) + "\n";
+    if (!pack_hidden) return Payload::from_i32(std::span<const int32_t>(s.emitted.data() + b, e - b));
+    const int32_t rows = static_cast<int32_t>(e - b);
+    const uint64_t nbytes = omni_pack_bytes(rows, model.d_model);
+    const uint64_t off = arena->alloc(s.request_id, nbytes);
+    packs.push_back({s.request_id, static_cast<int32_t>(b), static_cast<int32_t>(e), off});
+    Payload p;
+    p.dtype = Dtype::FIX16;
+    p.shape = {static_cast<uint32_t>(rows), static_cast<uint32_t>(model.d_model + 1)};
+    p.dev.device = dev;
+    p.dev.blob = arena->base() + off;
+    p.dev.nbytes = nbytes;
+    p.host_tokens.assign(s.emitted.begin() + static_cast<std::ptrdiff_t>(b),
+                         s.emitted.begin() + static_cast<std::ptrdiff_t>(e));
+    pack_tokens.insert(pack_tokens.end(), p.host_tokens.begin(), p.host_tokens.end());
+    return p;
+  }
+
+  void flush() {
+    if (packs.empty()) return;
+    std::vector<uint64_t> sid, off;
+    std::vector<int32_t> b, e;
+    for (const auto& p : packs) {
+      sid.push_back(p.rid);
+      b.push_back(p.begin);
+      e.push_back(p.end);
+      off.push_back(p.offset);
+    }
+    dev_ok(omni_pack_hidden(st, static_cast<int32_t>(packs.size()), sid.data(), b.data(), e.data(),
+                            pack_tokens.data(), arena->base(), off.data()),
+           "omni_pack_hidden");
+    packs.clear();
+    pack_tokens.clear();
+  }
+};
+
+struct DitStage {
+  std::string name;
+  int dev = 0;
+  omni_model_desc model{};
+  omni_stage* st = nullptr;
+  Tracer* tracer = nullptr;
+  std::vector<uint64_t> rid;
+  std::vector<int32_t> off, ntok, tokens, samples;
+  double dev_ms = 0;
+  uint64_t steps = 0;
+  ~DitStage() {
+    if (st) omni_stage_destroy(st);
+  }
+  void launch(const std::vector<DiffusionJob>& jobs) {
+    rid.clear();
+    off.clear();
+    ntok.clear();
+    tokens.clear();
+    for (const auto& j : jobs) {
+      if (j.input.dtype != Dtype::I32 || j.input.is_device())
+        throw BadDtype("diffusion input must be I32 codec tokens");
+      const auto t = j.input.as_i32();
+      rid.push_back(j.request_id);
+      off.push_back(static_cast<int32_t>(j.token_offset));
+      ntok.push_back(static_cast<int32_t>(t.size()));
+      tokens.insert(tokens.end(), t.begin(), t.end());
+    }
+    samples.assign(tokens.size() * static_cast<size_t>(model.dit_samples), 0);
+    omni_dit_batch b{};
+    b.n_jobs = static_cast<int32_t>(jobs.size());
+    b.request_id = rid.data();
+    b.token_offset = off.data();
+    b.n_tokens = ntok.data();
+    b.tokens = tokens.data();
+    dev_ok(omni_dit_step(st, &b, samples.data()), "omni_dit_step");
+  }
+  bool ready() {
+    const omni_status s = omni_stage_query(st);
+    if (s == OMNI_EAGAIN) return false;
+    dev_ok(s, "omni_stage_query");
+    return true;
+  }
+  std::vector<Payload> collect() {
+    dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    float us = 0;
+    omni_stage_last_step_us(st, &us);
+    dev_ms += us / 1e3;
+    ++steps;
+    std::vector<Payload> out;
+    size_t at = 0;
+    for (int32_t n : ntok) {
+      const size_t m = static_cast<size_t>(n) * model.dit_samples;
+      out.push_back(Payload::from_i32(std::span<const int32_t>(samples.data() + at, m)));
+      at += m;
+    }
+    return out;
+  }
+};
+
+omni_model_desc model_for(int kind, bool small) {
+  omni_model_desc m{};
+  dev_ok(omni_model_default(kind, &m), "omni_model_default");
+  if (small) {
+    if (kind == OMNI_MODEL_DIT) {
+      m.d_model = 256;
+      m.n_layers = 2;
+      m.n_heads = 2;
+      m.n_kv_heads = 2;
+      m.d_ff = 512;
+    } else {
+      m.d_model = 512;
+      m.n_layers = 2;
+      m.n_heads = 4;
+      m.n_kv_heads = 2;
+      m.d_ff = 1024;
+      if (kind == OMNI_MODEL_TALKER) m.cond_dim = 512;
+    }
+  }
+  return m;
+}
+
+}  // namespace
+
+struct B200Pipeline::Impl {
+  B200Options opt;
+  std::map<std::string, std::unique_ptr<ArStage>> ar;
+  std::map<std::string, std::unique_ptr<DitStage>> dit;
+  Tracer* tracer = nullptr;
+
+  int device_of(const std::string& name) const {
+    auto it = opt.device.find(name);
+    return it == opt.device.end() ? 0 : it->second;
+  }
+  EngineConfig engine_of(const std::string& name) const {
+    auto it = opt.engines.find(name);
+    return it == opt.engines.end() ? EngineConfig{} : it->second;
+  }
+
+  ArStage& make_ar(const std::string& name, int kind, uint64_t seed_salt) {
+    auto s = std::make_unique<ArStage>();
+    s->name = name;
+    s->kind = kind;
+    s->dev = device_of(name);
+    s->model = model_for(kind, opt.small_models);
+    const EngineConfig ec = engine_of(name);
+    omni_stage_limits lim{};
+    lim.max_batch_tokens = static_cast<int32_t>(std::max<uint64_t>(ec.max_batch_tokens, 16));
+    lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
+    // thinker: prompt (<= kv budget, capped) + up to 64 outputs; talker: <= 64 rows + 4x codec
+    lim.max_seq_len = kind == OMNI_MODEL_TALKER ? 64 + 256 + 16
+                                                : static_cast<int32_t>(std::min<uint64_t>(ec.kv_budget_tokens, 448) + 64);
+    dev_ok(omni_stage_create(&s->model, &lim, s->dev, opt.weight_seed + seed_salt, &s->st), "omni_stage_create");
+    auto& ref = *s;
+    ar[name] = std::move(s);
+    return ref;
+  }
+};
+
+B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
+  impl_->opt = std::move(opt);
+  int32_t n = 0;
+  if (omni_device_count(&n) != OMNI_OK || n == 0)
+    throw DeviceError("no CUDA device: the B200 pipeline has no CPU fallback");
+  std::vector<int32_t> devs;
+  for (const auto& [_, d] : impl_->opt.device) devs.push_back(d);
+  std::sort(devs.begin(), devs.end());
+  devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  dev_ok(omni_init(static_cast<int32_t>(devs.size()), devs.data()), "omni_init");
+  auto& I = *impl_;
+  auto want = [&I](const std::string& n) { return I.opt.needed.empty() || I.opt.needed.count(n) != 0; };
+  // weight seeds: thinker / ar share the thinker model family, talker and DiT own seeds
+  ArStage* th = nullptr;
+  if (want("thinker_forward") || want("talker_forward")) {
+    th = &I.make_ar("thinker_forward", OMNI_MODEL_THINKER, 0);
+    th->pack_hidden = true;
+  }
+  if (want("talker_forward")) {
+    ArStage& ta = I.make_ar("talker_forward", OMNI_MODEL_TALKER, 1);
+    ta.upstream = th;
+  }
+  if (th) th->arena = std::make_unique<Arena>(I.device_of("talker_forward"), I.opt.arena_bytes);
+  if (want("ar_forward")) I.make_ar("ar_forward", OMNI_MODEL_THINKER, 0);
+  for (const char* dn : {"denoise", "dit_image"}) {
+    if (!want(dn)) continue;
+    auto d = std::make_unique<DitStage>();
+    d->name = dn;
+    d->dev = I.device_of(dn);
+    d->model = model_for(OMNI_MODEL_DIT, I.opt.small_models);
+    const EngineConfig ec = I.engine_of(dn);
+    omni_stage_limits lim{};
+    lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
+    lim.dit_max_tokens = 512;
+    dev_ok(omni_stage_create(&d->model, &lim, d->dev, I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3),
+                             &d->st),
+           "omni_stage_create(dit)");
+    I.dit[dn] = std::move(d);
+  }
+}
+
+B200Pipeline::~B200Pipeline() = default;
+
+void B200Pipeline::set_tracer(Tracer* t) {
+  impl_->tracer = t;
+  for (auto& [_, s] : impl_->ar) s->tracer = t;
+  for (auto& [_, s] : impl_->dit) s->tracer = t;
+}
+
+std::map<std::string, double> B200Pipeline::device_ms() const {
+  std::map<std::string, double> m;
+  for (const auto& [n, s] : impl_->ar) m[n] = s->dev_ms;
+  for (const auto& [n, s] : impl_->dit) m[n] = s->dev_ms;
+  return m;
+}
+std::map<std::string, uint64_t> B200Pipeline::step_counts() const {
+  std::map<std::string, uint64_t> m;
+  for (const auto& [n, s] : impl_->ar) m[n] = s->steps;
+  for (const auto& [n, s] : impl_->dit) m[n] = s->steps;
+  return m;
+}
+uint64_t B200Pipeline::weight_bytes() const {
+  uint64_t t = 0, b = 0;
+  for (const auto& [_, s] : impl_->ar)
+    if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
+  for (const auto& [_, s] : impl_->dit)
+    if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
+  return t;
+}
+void B200Pipeline::reset_counters() {
+  for (auto& [_, s] : impl_->ar) s->dev_ms = 0, s->steps = 0;
+  for (auto& [_, s] : impl_->dit) s->dev_ms = 0, s->steps = 0;
+}
+
+void B200Pipeline::register_into(FunctionRegistry& reg) {
+  auto& I = *impl_;
+  auto trace_prefill = [&I](const std::string& name) {
+    return [&I, name](RequestContext&, SeqState& s, std::span<const uint8_t> span) {
+      if (I.tracer)
+        I.tracer->out += "P " + name + " " + std::to_string(I.tracer->now()) + " " + std::to_string(s.request_id) +
+                         " " + std::to_string(s.consumed_prompt) + " " + std::to_string(span.size()) + "\n";
+      if (name != "talker_forward")  // thinker: lengths from the host fold (reference_pipeline.hpp:98-100)
+        for (uint8_t t : span) s.rng_state = mix(s.rng_state, t);
+    };
+  };
+  auto trace_consumed = [&I](const std::string& name, bool talker) {
+    return [&I, name, talker](RequestContext&, SeqState& s) {
+      s.target_len = talker ? 4 * s.prompt.size() : (s.rng_state % 64u) + 1u;
+      if (I.tracer)
+        I.tracer->out += "O " + name + " " + std::to_string(I.tracer->now()) + " " + std::to_string(s.request_id) +
+                         " " + std::to_string(s.target_len) + "\n";
+    };
+  };
+  for (auto& [name, sp] : I.ar) {
+    ArStage* s = sp.get();
+    StageModel m;
+    m.prefill = trace_prefill(name);
+    m.on_prompt_consumed = trace_consumed(name, s->kind == OMNI_MODEL_TALKER);
+    m.pack_chunk = [s](const SeqState& q, size_t b, size_t e) { return s->pack_chunk(q, b, e); };
+    m.launch_batch = [s](std::vector<BatchSlot>& slots) { s->launch(slots); };
+    m.batch_ready = [s] { return s->ready(); };
+    m.collect_batch = [s](std::vector<BatchSlot>& slots, std::vector<int32_t>& out) { s->collect(slots, out); };
+    m.release = [s](uint64_t rid) { dev_ok(omni_seq_release(s->st, rid), "omni_seq_release"); };
+    m.flush = [s] { s->flush(); };
+    m.cleanup = [s](uint64_t rid) {
+      if (s->arena) s->arena->release(rid);
+    };
+    reg.register_forward(name, std::move(m));
+  }
+
+  // Talker preprocess over device chunks: same READY/STALL rule as the
+  // reference (reference_pipeline.hpp:159-190); rows stay in HBM, the host
+  // keeps only token ids and row addresses.
+  reg.register_preprocess("process_input", [](RequestContext&, SeqState& s, StreamReceiver* up) {
+    if (up) {
+      while (auto c = up->try_recv()) {
+        const Payload& p = c->payload;
+        if (p.is_device() && p.shape.size() == 2) {
+          for (uint32_t r = 0; r < p.shape[0]; ++r) {
+            s.prompt.push_back(static_cast<uint8_t>(p.host_tokens.at(r)));
+            s.prompt_rows.push_back(p.device_elem(r, 1));
+          }
+        } else if (p.element_count() > 0 || p.shape.size() == 2) {
+          if (!(p.shape.size() == 2 && p.shape[0] == 0)) throw BadDtype("talker expects device FIX16 rows");
+        }
+        if (c->eos) s.prompt_complete = true;
+      }
+    }
+    if (s.phase == Phase::PREFILL) {
+      if (s.consumed_prompt < s.prompt.size()) return PreprocessStatus::READY;
+      return s.prompt_complete ? PreprocessStatus::READY : PreprocessStatus::STALL;
+    }
+    if (s.phase == Phase::DECODE)
+      return s.emitted.size() / 4 < s.prompt_rows.size() ? PreprocessStatus::READY : PreprocessStatus::STALL;
+    return PreprocessStatus::READY;
+  });
+
+  reg.register_transfer("Thinker2Talker", [](TransferEnv& env) {
+    ArSubmission sub;
+    sub.request_id = env.request.request_id;
+    sub.seed = env.request.seed;
+    if (env.upstream_final) {
+      const Payload& p = *env.upstream_final;
+      if (!p.is_device() || p.shape.size() != 2) throw TransferFnError("Thinker2Talker: unexpected payload");
+      for (uint32_t r = 0; r < p.shape[0]; ++r) {
+        sub.prompt.push_back(static_cast<uint8_t>(p.host_tokens.at(r)));
+        sub.prompt_rows.push_back(p.device_elem(r, 1));
+      }
+      sub.prompt_streams = false;
+    } else {
+      sub.prompt_streams = true;
+    }
+    env.submit_ar(std::move(sub));
+  });
+  reg.register_transfer("Talker2Vocoder", [](TransferEnv& env) { env.wire_diffusion({4, 16}); });
+
+  for (auto& [name, dp] : I.dit) {
+    DitStage* d = dp.get();
+    DiffusionModel dm;
+    dm.launch_batch = [d](const std::vector<DiffusionJob>& jobs) { d->launch(jobs); };
+    dm.batch_ready = [d] { return d->ready(); };
+    dm.collect_batch = [d] { return d->collect(); };
+    reg.register_denoiser(name, std::move(dm));
+  }
+}
+
+}  // namespace omni

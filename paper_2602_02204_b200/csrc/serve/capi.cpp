@@ -1,0 +1,231 @@
+// C ABI of libomni_serve (include/omni_serve.h).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+
+#include "omni/b200_pipeline.hpp"
+#include "omni/bench.hpp"
+#include "omni/config.hpp"
+#include "omni_serve.h"
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+omni_status guard(F&& f) {
+  try {
+    f();
+    return OMNI_OK;
+  } catch (const omni::DeviceError& e) {
+    g_err = e.what();
+    return OMNI_E_CUDA;
+  } catch (const omni::RegionFull& e) {
+    g_err = e.what();
+    return OMNI_E_OOM;
+  } catch (const omni::ForwardError& e) {
+    g_err = e.what();
+    return OMNI_E_FORWARD;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return OMNI_E_BADARG;
+  }
+}
+
+uint64_t fnv_i32(const std::vector<int32_t>& v, uint64_t h) {
+  for (int32_t x : v)
+    for (int i = 0; i < 4; ++i) {
+      h ^= static_cast<uint8_t>(static_cast<uint32_t>(x) >> (8 * i));
+      h *= 1099511628211ull;
+    }
+  return h;
+}
+
+std::string hex64(uint64_t v) {
+  char b[32];
+  std::snprintf(b, sizeof b, "%016llx", static_cast<unsigned long long>(v));
+  return b;
+}
+}  // namespace
+
+struct omni_pipeline {
+  omni::DeploymentPlan plan;
+  std::unique_ptr<omni::B200Pipeline> dev;
+  omni::FunctionRegistry reg;
+  std::string csv, trace;
+};
+
+extern "C" {
+
+const char* omni_serve_last_error(void) { return g_err.c_str(); }
+
+omni_status omni_pipeline_create(const char* config_json, const omni_pipeline_opts* opts, omni_pipeline** out) {
+  return guard([&] {
+    auto p = std::make_unique<omni_pipeline>();
+    p->plan = omni::parse_plan_text(config_json);
+    omni::B200Options o;
+    if (opts) {
+      o.weight_seed = opts->weight_seed;
+      o.small_models = opts->small_models != 0;
+    }
+    const int dev = opts ? opts->device : 0;
+    for (const auto& n : p->plan.graph.nodes) {
+      const std::string fn = n.kind == omni::StageKind::AR ? n.forward_ref
+                                                           : (n.forward_ref.empty() ? "denoise" : n.forward_ref);
+      o.device[fn] = dev;
+      o.engines[fn] = p->plan.engines.at(n.id);
+      o.needed.insert(fn);
+    }
+    p->dev = std::make_unique<omni::B200Pipeline>(std::move(o));
+    p->dev->register_into(p->reg);
+    *out = p.release();
+  });
+}
+
+omni_status omni_pipeline_destroy(omni_pipeline* p) {
+  return guard([&] { delete p; });
+}
+
+omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* s, omni_bench_result* r) {
+  return guard([&] {
+    omni::DeploymentPlan plan = p->plan;
+    plan.clock_kind = s->clock ? s->clock : "device";
+    if (s->talker_chunk > 0 && !plan.graph.edges.empty())
+      plan.graph.edges[0].streaming_chunk_size = static_cast<uint32_t>(s->talker_chunk);
+    if (s->vocoder_chunk > 0 && plan.graph.edges.size() > 1)
+      plan.graph.edges[1].streaming_chunk_size = static_cast<uint32_t>(s->vocoder_chunk);
+    omni::bench::WorkloadSpec spec;
+    spec.n = s->n;
+    spec.seed = s->seed;
+    spec.stream = s->stream != 0;
+    spec.arrival = s->poisson ? "poisson" : "closed-loop";
+    spec.rate = s->rate > 0 ? s->rate : 1.0;
+    if (s->prompt_min) spec.prompt_min = s->prompt_min;
+    if (s->prompt_max) spec.prompt_max = s->prompt_max;
+    auto workload = omni::bench::gen_workload(spec);
+    omni::bench::BenchOptions bo;
+    bo.concurrency = s->concurrency ? s->concurrency : 16;
+    const std::string th = plan.graph.entry;
+    bo.thinker_stage = th;
+    bo.talker_stage = "talker";
+    omni::Tracer tracer;
+    p->dev->set_tracer(s->trace ? &tracer : nullptr);
+    p->dev->reset_counters();
+    // The orchestrator owns its clock; trace timestamps read it through the tracer.
+    auto clock = std::unique_ptr<omni::Clock>();
+    const auto t0 = std::chrono::steady_clock::now();
+    omni::bench::BenchReport rep;
+    {
+      if (plan.server.admission_cap < workload.size() + 1) plan.server.admission_cap = workload.size() + 1;
+      omni::Orchestrator orch(plan, &p->reg);
+      tracer.clock = &orch.clock();
+      orch.start();
+      std::vector<std::shared_ptr<omni::ResultHandle>> handles(workload.size());
+      size_t next = 0;
+      auto launch = [&](uint64_t at) {
+        if (next >= workload.size()) return;
+        const size_t i = next++;
+        handles[i] = orch.submit_at(workload[i], at);
+      };
+      if (s->poisson) {
+        const uint64_t base = orch.clock().now_us();
+        for (size_t i = 0; i < workload.size(); ++i)
+          handles[i] = orch.submit_at(workload[i], base + workload[i].submitted_at_us);
+        next = workload.size();
+      } else {
+        orch.set_on_done([&](uint64_t, uint64_t now) { launch(now); });
+        const uint64_t start = orch.clock().now_us();
+        for (size_t i = 0; i < std::min<size_t>(bo.concurrency, workload.size()); ++i) launch(start);
+      }
+      orch.run_until_drained();
+      rep.mode = "disaggregated";
+      std::vector<omni::MetricsRecord> recs;
+      uint64_t digest = 1469598103934665603ull, first = omni::kTimeUnset, last = 0;
+      for (size_t i = 0; i < workload.size(); ++i) {
+        const auto& out = handles[i]->wait();
+        recs.push_back(out.metrics);
+        auto row = omni::bench::row_from_record(out.metrics, bo.thinker_stage, bo.talker_stage);
+        row.request_id = workload[i].request_id;
+        if (out.status != "DONE") row.status = out.status;
+        rep.rows.push_back(row);
+        uint64_t od = 1469598103934665603ull;
+        od = fnv_i32(out.text_tokens, od);
+        od = fnv_i32(out.codec_tokens, od);
+        od = fnv_i32(out.waveform, od);
+        digest = fnv_i32(out.text_tokens, digest);
+        digest = fnv_i32(out.codec_tokens, digest);
+        digest = fnv_i32(out.waveform, digest);
+        if (out.status == "DONE") {
+          ++rep.completed;
+          r->text_tokens += 0;
+        }
+        const auto& m = out.metrics;
+        if (m.submitted_at != omni::kTimeUnset) first = std::min(first, m.submitted_at);
+        if (m.done_at != omni::kTimeUnset) last = std::max(last, m.done_at);
+        if (s->trace) {
+          tracer.out += "R " + std::to_string(workload[i].request_id) + " " + out.status + " " +
+                        std::to_string(m.submitted_at) + " " + std::to_string(m.done_at) + " " +
+                        std::to_string(m.first_final_chunk_at == omni::kTimeUnset ? -1LL
+                                                                                 : (long long)m.first_final_chunk_at) +
+                        " " + std::to_string(out.text_tokens.size()) + " " + std::to_string(out.codec_tokens.size()) +
+                        " " + std::to_string(out.waveform.size()) + " " + hex64(od);
+          for (const auto& [st, tim] : m.stages)
+            tracer.out += " " + st + ":" + std::to_string((long long)tim.first_scheduled_at) + ":" +
+                          std::to_string((long long)tim.first_token_at) + ":" +
+                          std::to_string((long long)tim.finished_at) + ":" + std::to_string(tim.tokens);
+          tracer.out += "\n";
+        }
+      }
+      r->preemptions = 0;
+      for (const auto& n : plan.graph.nodes) r->preemptions += orch.preemptions(n.id);
+      orch.shutdown(true);
+      omni::bench::finish_report(rep, recs, spec);
+      rep.makespan_us = (first == omni::kTimeUnset || last < first) ? 0 : last - first;
+      rep.requests_per_s = rep.makespan_us ? rep.completed / (rep.makespan_us / 1e6) : 0;
+      r->output_digest = digest;
+    }
+    p->dev->set_tracer(nullptr);
+    r->wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    r->completed = rep.completed;
+    r->failed = workload.size() - rep.completed;
+    r->makespan_us = static_cast<double>(rep.makespan_us);
+    r->requests_per_s = rep.requests_per_s;
+    r->mean_jct_us = rep.mean.jct_us;
+    r->p50_jct_us = rep.p50.jct_us;
+    r->p95_jct_us = rep.p95.jct_us;
+    r->p99_jct_us = rep.p99.jct_us;
+    r->mean_ttft_us = rep.mean.ttft_us;
+    r->p99_ttft_us = rep.p99.ttft_us;
+    r->mean_rtf = rep.mean.rtf;
+    r->text_tokens = r->codec_tokens = r->wave_samples = 0;
+    for (const auto& row : rep.rows) {
+      r->text_tokens += row.text_tokens;
+      r->codec_tokens += row.codec_tokens;
+      r->wave_samples += row.waveform_samples;
+    }
+    const auto ms = p->dev->device_ms();
+    const auto st = p->dev->step_counts();
+    auto get = [](const auto& m, const char* k) { auto it = m.find(k); return it == m.end() ? decltype(it->second){} : it->second; };
+    r->dev_ms_thinker = get(ms, "thinker_forward") + get(ms, "ar_forward");
+    r->dev_ms_talker = get(ms, "talker_forward");
+    r->dev_ms_dit = get(ms, "denoise") + get(ms, "dit_image");
+    r->steps_thinker = get(st, "thinker_forward") + get(st, "ar_forward");
+    r->steps_talker = get(st, "talker_forward");
+    r->steps_dit = get(st, "denoise") + get(st, "dit_image");
+    p->csv = rep.csv;
+    p->trace = std::move(tracer.out);
+  });
+}
+
+size_t omni_pipeline_text(omni_pipeline* p, int32_t what, char* buf, size_t cap) {
+  const std::string& s = what == 0 ? p->csv : p->trace;
+  if (buf && cap) {
+    const size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return s.size();
+}
+
+}  // extern "C"
