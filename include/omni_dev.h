@@ -193,6 +193,9 @@ omni_status omni_mem_h2d(uint64_t dst_dev, const void* src, uint64_t bytes);
 omni_status omni_mem_d2h(void* dst, uint64_t src_dev, uint64_t bytes);
 omni_status omni_mem_set(uint64_t dst_dev, int32_t byte, uint64_t bytes);
 omni_status omni_device_sync(void);
+/* Process-wide counters: kernels launched by libomni_dev, bytes copied
+ * host->device / device->host by the step / pack entry points. */
+omni_status omni_dev_counters(uint64_t* launches, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 
 /* ------------------------------------------------------------------------ */
 /* Kernel-level entry points (parity tests / microbenchmarks). All pointers */
@@ -211,6 +214,12 @@ omni_status omni_k_fill_weights(uint64_t dst, int64_t n, uint64_t seed, uint32_t
 omni_status omni_k_gemm_time(uint64_t W, int32_t N, int32_t K, uint64_t X, int32_t M,
                              int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits,
                              int32_t iters, float* ms);
+
+/* CUDA-event time per launch of a graph of `iters` GEMMs cycling over n_w
+ * distinct weight copies (footprint > L2 => every launch streams HBM). */
+omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, int32_t K, uint64_t X,
+                                   int32_t M, int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits,
+                                   int32_t iters, float* ms);
 
 #ifdef __cplusplus
 }

@@ -84,6 +84,11 @@ void run_test_gemm(uint64_t W, int N, int K, uint64_t X, int M, int epi, uint64_
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
+DevCounters& counters() {
+  static DevCounters c;
+  return c;
+}
+
 }  // namespace omni_dev
 
 using namespace omni_dev;
@@ -98,6 +103,15 @@ omni_status omni_device_count(int32_t* n) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
     *n = c;
+  });
+}
+
+omni_status omni_dev_counters(uint64_t* launches, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  return guarded([&] {
+    const auto& c = counters();
+    if (launches) *launches = c.launches;
+    if (h2d_bytes) *h2d_bytes = c.h2d_bytes;
+    if (d2h_bytes) *d2h_bytes = c.d2h_bytes;
   });
 }
 
@@ -144,6 +158,52 @@ omni_status omni_k_gemm_time(uint64_t W, int32_t N, int32_t K, uint64_t X, int32
                              float* ms) {
   return guarded([&] {
     run_test_gemm(W, N, K, X, M, epi, out, ldo, 0, 0, 0, 1, nullptr, iters, ms, max_splits);
+  });
+}
+
+omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, int32_t K, uint64_t X,
+                                   int32_t M, int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits,
+                                   int32_t iters, float* ms) {
+  return guarded([&] {
+    require_gpu();
+    OMNI_REQUIRE(n_w > 0 && iters > 0, OMNI_E_BADARG, "gemm_time_multi: empty");
+    const int N_pad = (N + 127) / 128 * 128;
+    std::vector<GemmWeight> ws(n_w);
+    for (int i = 0; i < n_w; ++i)
+      OMNI_REQUIRE(gemm_make_weight(ws[i], reinterpret_cast<const __nv_bfloat16*>(Ws[i]), N, N_pad, K, max_splits),
+                   OMNI_E_BADARG, "weight tensor map");
+    GemmInput x;
+    OMNI_REQUIRE(gemm_make_input(x, reinterpret_cast<const __nv_bfloat16*>(X), M, K), OMNI_E_BADARG, "input map");
+    GemmEpilogue e;
+    e.out = reinterpret_cast<void*>(out);
+    e.ldo = ldo;
+    cudaStream_t cs;
+    OMNI_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int i = 0; i < n_w; ++i) OMNI_CUDA(gemm_run(ws[i], x, M, epi, e, cs));
+    OMNI_CUDA(cudaStreamSynchronize(cs));
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    OMNI_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < iters; ++i) OMNI_CUDA(gemm_run(ws[i % n_w], x, M, epi, e, cs));
+    OMNI_CUDA(cudaStreamEndCapture(cs, &g));
+    OMNI_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    OMNI_CUDA(cudaGraphLaunch(ge, cs));
+    OMNI_CUDA(cudaStreamSynchronize(cs));
+    cudaEvent_t a, b;
+    OMNI_CUDA(cudaEventCreate(&a));
+    OMNI_CUDA(cudaEventCreate(&b));
+    OMNI_CUDA(cudaEventRecord(a, cs));
+    OMNI_CUDA(cudaGraphLaunch(ge, cs));
+    OMNI_CUDA(cudaEventRecord(b, cs));
+    OMNI_CUDA(cudaEventSynchronize(b));
+    float t = 0;
+    OMNI_CUDA(cudaEventElapsedTime(&t, a, b));
+    *ms = t / iters;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
   });
 }
 

@@ -27,6 +27,19 @@ void set_last_error(const std::string& msg);
                                                   __FILE__ + ":" + std::to_string(__LINE__)); \
   } while (0)
 
+// Counters of device work issued by this library (bench evidence: how many
+// of OUR kernels ran and how many bytes crossed PCIe).
+struct DevCounters {
+  uint64_t launches = 0, h2d_bytes = 0, d2h_bytes = 0;
+};
+DevCounters& counters();
+
+#define OMNI_KERNEL(expr)          \
+  do {                             \
+    OMNI_CUDA(expr);               \
+    ++::omni_dev::counters().launches; \
+  } while (0)
+
 #define OMNI_REQUIRE(cond, code, msg)                          \
   do {                                                         \
     if (!(cond)) throw ::omni_dev::DevError((code), (msg));    \

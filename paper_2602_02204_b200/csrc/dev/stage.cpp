@@ -39,7 +39,7 @@ DevTensor make_weight(omni_stage* st, const std::string& name, int64_t rows, int
   t.rows_pad = rows_pad;
   t.cols = cols;
   t.p = dev_alloc<__nv_bfloat16>(st, (size_t)rows_pad * cols);
-  OMNI_CUDA(fill_weights(t.p, rows_pad, rows, cols, st->seed, tid, scale, st->stream));
+  OMNI_KERNEL(fill_weights(t.p, rows_pad, rows, cols, st->seed, tid, scale, st->stream));
   st->weight_bytes += (uint64_t)rows * cols * 2;
   st->named[name] = t;
   return t;
@@ -51,7 +51,7 @@ DevTensor make_swiglu(omni_stage* st, const std::string& name, int64_t ff, int64
   t.rows = t.rows_pad = 2 * ff;
   t.cols = cols;
   t.p = dev_alloc<__nv_bfloat16>(st, (size_t)2 * ff * cols);
-  OMNI_CUDA(fill_swiglu(t.p, ff, cols, st->seed, tid_gate, tid_up, scale, st->stream));
+  OMNI_KERNEL(fill_swiglu(t.p, ff, cols, st->seed, tid_gate, tid_up, scale, st->stream));
   st->weight_bytes += (uint64_t)2 * ff * cols * 2;
   st->named[name] = t;
   return t;
@@ -355,6 +355,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
   OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, total, cudaMemcpyHostToDevice, s));
+  counters().h2d_bytes += total;
   OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
   ArStepDev sd;
   sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
@@ -367,44 +368,45 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   if (n_rows > 0) {
     if (talker && n_prefill_rows > 0) {
-      OMNI_CUDA(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
+      OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
       GemmEpilogue e;
       e.out = st->hproj;
       e.ldo = d;
-      OMNI_CUDA(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
+      OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
     }
-    OMNI_CUDA(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
+    OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
                            st->cond_table, st->cond_rows, d, st->start_id, st->x, s));
     for (int l = 0; l < L; ++l) {
       const auto& ly = st->layers[l];
-      OMNI_CUDA(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
+      OMNI_KERNEL(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
       GemmEpilogue e;
       e.out = st->qkv;
       e.ldo = (H + 2 * KVH) * kHeadDim;
-      OMNI_CUDA(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_F32, e, s));
-      OMNI_CUDA(launch_rope_kv(sd, n_rows, st->qkv, H, KVH, st->rope, l, L, st->q, st->kv, s));
-      OMNI_CUDA(launch_attention(sd, ne, st->q, H, KVH, l, L, st->kv, st->attn, s));
+      OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_F32, e, s));
+      OMNI_KERNEL(launch_rope_kv(sd, n_rows, st->qkv, H, KVH, st->rope, l, L, st->q, st->kv, s));
+      OMNI_KERNEL(launch_attention(sd, ne, st->q, H, KVH, l, L, st->kv, st->attn, s));
       e.out = st->x;
       e.ldo = d;
-      OMNI_CUDA(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID, e, s));
-      OMNI_CUDA(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
+      OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID, e, s));
+      OMNI_KERNEL(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
       e.out = st->act;
       e.ldo = m.d_ff;
-      OMNI_CUDA(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
+      OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
       e.out = st->x;
       e.ldo = d;
-      OMNI_CUDA(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID, e, s));
+      OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID, e, s));
     }
     if (n_dec > 0) {
-      OMNI_CUDA(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
+      OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
                                     talker ? nullptr : st->ring, st->ring_rows, s));
       GemmEpilogue e;
       e.out = st->logits;
       e.ldo = st->vocab_pad;
-      OMNI_CUDA(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
-      OMNI_CUDA(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
+      OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
+      OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
                               st->d_tok, st->d_margin, s));
       OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      counters().d2h_bytes += n_dec * (sizeof(int32_t) + sizeof(float));
       OMNI_CUDA(cudaMemcpyAsync(st->h_margin, st->d_margin, n_dec * sizeof(float),
                                 cudaMemcpyDeviceToHost, s));
     }
@@ -427,27 +429,27 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
   const int rows = n_tok * S;
   const int ld_mod = L * 6 * d;
   cudaStream_t s = st->stream;
-  OMNI_CUDA(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, s));
+  OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, s));
   for (int t = 0; t < T; ++t) {
-    OMNI_CUDA(dit_cond(toks_dev, n_tok, st->tok_emb.p, st->t_emb.p, t, d, st->dcvec, s));
+    OMNI_KERNEL(dit_cond(toks_dev, n_tok, st->tok_emb.p, st->t_emb.p, t, d, st->dcvec, s));
     GemmEpilogue e;
     e.out = st->dmod;
     e.ldo = ld_mod;
-    OMNI_CUDA(gemm_run(st->g_mod, st->din_c, n_tok, EPI_F32, e, s));
-    OMNI_CUDA(dit_to_bf16(st->dx, (int64_t)rows * C, st->dxin, s));
+    OMNI_KERNEL(gemm_run(st->g_mod, st->din_c, n_tok, EPI_F32, e, s));
+    OMNI_KERNEL(dit_to_bf16(st->dx, (int64_t)rows * C, st->dxin, s));
     e.out = st->dh;
     e.ldo = d;
-    OMNI_CUDA(gemm_run(st->g_in, st->din_x, rows, EPI_F32, e, s));
-    OMNI_CUDA(dit_add_pos(st->dh, st->pos_emb.p, S, d, rows, s));
+    OMNI_KERNEL(gemm_run(st->g_in, st->din_x, rows, EPI_F32, e, s));
+    OMNI_KERNEL(dit_add_pos(st->dh, st->pos_emb.p, S, d, rows, s));
     for (int l = 0; l < L; ++l) {
       const auto& ly = st->dlayers[l];
       const int base = l * 6 * d;
-      OMNI_CUDA(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 0, base + d, S, st->da, s));
+      OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 0, base + d, S, st->da, s));
       e = GemmEpilogue{};
       e.out = st->dqkv;
       e.ldo = 3 * d;
-      OMNI_CUDA(gemm_run(ly.gqkv, st->din_a, rows, EPI_BF16, e, s));
-      OMNI_CUDA(dit_attn(st->dqkv, n_tok, d, m.n_heads, st->dout, s));
+      OMNI_KERNEL(gemm_run(ly.gqkv, st->din_a, rows, EPI_BF16, e, s));
+      OMNI_KERNEL(dit_attn(st->dqkv, n_tok, d, m.n_heads, st->dout, s));
       e = GemmEpilogue{};
       e.out = st->dh;
       e.ldo = d;
@@ -455,21 +457,21 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
       e.ldg = ld_mod;
       e.gate_off = base + 2 * d;
       e.rows_per_group = S;
-      OMNI_CUDA(gemm_run(ly.go, st->din_o, rows, EPI_GATED_RESID, e, s));
-      OMNI_CUDA(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 3 * d, base + 4 * d, S, st->da, s));
+      OMNI_KERNEL(gemm_run(ly.go, st->din_o, rows, EPI_GATED_RESID, e, s));
+      OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 3 * d, base + 4 * d, S, st->da, s));
       GemmEpilogue e1;
       e1.out = st->du;
       e1.ldo = m.d_ff;
-      OMNI_CUDA(gemm_run(ly.g1, st->din_a, rows, EPI_GELU, e1, s));
+      OMNI_KERNEL(gemm_run(ly.g1, st->din_a, rows, EPI_GELU, e1, s));
       e.gate_off = base + 5 * d;
-      OMNI_CUDA(gemm_run(ly.g2, st->din_u, rows, EPI_GATED_RESID, e, s));
+      OMNI_KERNEL(gemm_run(ly.g2, st->din_u, rows, EPI_GATED_RESID, e, s));
     }
-    OMNI_CUDA(dit_ln_mod(st->dh, rows, d, nullptr, 0, 0, 0, S, st->da, s));
+    OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, nullptr, 0, 0, 0, S, st->da, s));
     GemmEpilogue eo;
     eo.out = st->dv;
     eo.ldo = C;
-    OMNI_CUDA(gemm_run(st->g_out, st->din_a, rows, EPI_F32, eo, s));
-    OMNI_CUDA(dit_euler(st->dx, st->dv, C, rows, 1.f / T, t == T - 1, samples_dev, s));
+    OMNI_KERNEL(gemm_run(st->g_out, st->din_a, rows, EPI_F32, eo, s));
+    OMNI_KERNEL(dit_euler(st->dx, st->dv, C, rows, 1.f / T, t == T - 1, samples_dev, s));
   }
 }
 
@@ -497,6 +499,7 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
   if (n_tok > 0) {
     OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, bytes, cudaMemcpyHostToDevice, s));
+    counters().h2d_bytes += bytes;
     OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
     const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
     for (int64_t t0 = 0; t0 < n_tok; t0 += st->tok_cap) {
@@ -505,6 +508,7 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
       const int64_t nsamp = (int64_t)nt * kDitSamples;
       OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
+      counters().d2h_bytes += nsamp * sizeof(int32_t);
       if (n_tok > st->tok_cap) {  // multi-chunk: land each chunk before reusing h_samples
         OMNI_CUDA(cudaStreamSynchronize(s));
         std::memcpy(samples_out + t0 * kDitSamples, st->h_samples, nsamp * sizeof(int32_t));
@@ -813,8 +817,9 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
     }
     cudaStream_t s = src->stream;
     OMNI_CUDA(cudaMemcpyAsync(src->pack.dev, src->pack.host, total, cudaMemcpyHostToDevice, s));
+    counters().h2d_bytes += total;
     OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));
-    OMNI_CUDA(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(src->pack.dev), n_chunks,
+    OMNI_KERNEL(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(src->pack.dev), n_chunks,
                                  max_rows, src->ring, src->m.d_model, src->ring_rows,
                                  reinterpret_cast<uint8_t*>(dst_base), s));
   });
