@@ -142,125 +142,164 @@ __global__ void rope_kv_kernel(const ArStepDev s, const float* __restrict__ qkv,
 }
 
 // ---------------------------------------------------------------------------
-// Paged causal attention. Grid (entry, kv_head); 8 warps. Each CTA owns the
-// q_len x group query vectors of one entry that share a KV head; K/V pages of
-// the entry's context are staged into smem with 1-D bulk TMA copies (double
-// buffered, mbarrier-tracked) and every warp runs an online softmax for its
-// query vectors with lanes splitting the 128 head dims.
+// Paged causal attention (K3). Grid (query block, kv_head), 8 warps.
+// A query block is up to kAttnQTok tokens of one entry (decode: 1 token) and
+// holds their `group` query heads that share the KV head. The block's causal
+// context [0, pos0 + tok0 + ntok) is staged into smem in 128-key chunks by
+// 1-D bulk TMA copies of whole 16-token pages (double buffered, one mbarrier
+// per chunk). Each warp owns query vectors; QK^T has lanes split KEYS (rotated
+// column order -> conflict-free smem), the chunk softmax merges online, P.V
+// has lanes split the 128 head dims.
 // ---------------------------------------------------------------------------
 constexpr int kAttnWarps = 8;
+constexpr int kAttnChunk = 128;                        // keys per staged chunk
+constexpr int kAttnPagesPerChunk = kAttnChunk / kPageTokens;
+constexpr int kAttnQMax = kAttnQTok * 8;               // query vectors per block (group <= 8)
+
+struct AttnSmem {
+  __nv_bfloat16 k[2][kAttnChunk * kHeadDim];
+  __nv_bfloat16 v[2][kAttnChunk * kHeadDim];
+  float2 q[kAttnQMax][kHeadDim / 2];
+  float p[kAttnWarps][kAttnChunk];
+  uint64_t bar[2];
+};
 
 __global__ void __launch_bounds__(kAttnWarps * 32)
     attention_kernel(const ArStepDev s, const __nv_bfloat16* __restrict__ q, int n_heads, int n_kv,
                      int layer, int n_layers, const __nv_bfloat16* __restrict__ kv,
                      __nv_bfloat16* __restrict__ out, float scale) {
   constexpr int HD = kHeadDim;
-  constexpr int PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB per K or V page slice
-  __shared__ __align__(128) __nv_bfloat16 sk[2][kPageTokens * HD];
-  __shared__ __align__(128) __nv_bfloat16 sv[2][kPageTokens * HD];
-  __shared__ __align__(8) uint64_t bar[2];
+  constexpr uint32_t PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB K or V slice of one page
+  extern __shared__ __align__(128) uint8_t attn_smem_raw[];
+  AttnSmem& sm = *reinterpret_cast<AttnSmem*>(attn_smem_raw);
 
-  const int e = blockIdx.x, kh = blockIdx.y;
-  const ArEntryDesc ed = s.entries[e];
+  const AttnBlockDesc blk = s.attn_blocks[blockIdx.x];
+  const int kh = blockIdx.y;
+  const ArEntryDesc ed = s.entries[blk.entry];
   const int group = n_heads / n_kv;
-  const int nq = ed.q_len * group;  // query vectors in this CTA
-  const int ctx = ed.pos0 + ed.q_len;
-  const int n_pages = (ctx + kPageTokens - 1) / kPageTokens;
+  const int nq = blk.ntok * group;
+  const int kend = ed.pos0 + blk.tok0 + blk.ntok;  // causal context of the block
+  const int n_chunks = (kend + kAttnChunk - 1) / kAttnChunk;
   const int warp = warp_id(), lane = lane_id();
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
     fence_barrier_init();
+  }
+  // stage the (pre-scaled) query vectors
+  for (int t = threadIdx.x; t < nq * (HD / 2); t += blockDim.x) {
+    const int qi = t / (HD / 2), c2 = t % (HD / 2);
+    const int tok = blk.tok0 + qi / group, hq = kh * group + qi % group;
+    const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(
+        q + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD)[c2];
+    sm.q[qi][c2] = make_float2(__low2float(v) * scale, __high2float(v) * scale);
   }
   __syncthreads();
 
-  auto issue = [&](int p, int buf) {
-    const int page = s.page_table[e * s.max_pages + p];
-    const __nv_bfloat16* kp =
-        kv + ((((size_t)page * n_layers + layer) * 2 + 0) * n_kv + kh) * kPageTokens * HD;
-    const __nv_bfloat16* vp =
-        kv + ((((size_t)page * n_layers + layer) * 2 + 1) * n_kv + kh) * kPageTokens * HD;
-    mbar_expect_tx(&bar[buf], 2 * PAGE_BYTES);
-    bulk_load(sk[buf], kp, PAGE_BYTES, &bar[buf]);
-    bulk_load(sv[buf], vp, PAGE_BYTES, &bar[buf]);
+  auto issue = [&](int c, int buf) {
+    const int first = c * kAttnPagesPerChunk;
+    const int keys = min(kAttnChunk, kend - c * kAttnChunk);
+    const int np = (keys + kPageTokens - 1) / kPageTokens;
+    mbar_expect_tx(&sm.bar[buf], 2u * PAGE_BYTES * np);
+    for (int i = 0; i < np; ++i) {
+      const int page = s.page_table[blk.entry * s.max_pages + first + i];
+      const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
+      bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
+      bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
+                &sm.bar[buf]);
+    }
   };
+  if (threadIdx.x == 0) {
+    issue(0, 0);
+    if (n_chunks > 1) issue(1, 1);
+  }
 
-  // Per-warp state for up to kMaxQPerWarp query vectors (processed in waves).
-  constexpr int kMaxQPerWarp = 4;
-  const int n_waves = (nq + kAttnWarps * kMaxQPerWarp - 1) / (kAttnWarps * kMaxQPerWarp);
-  for (int wave = 0; wave < n_waves; ++wave) {
-    // the whole CTA sweeps the pages once per wave of query vectors; query
-    // vectors are dealt round-robin so small (decode) entries use all warps
-    const int q0 = wave * kAttnWarps * kMaxQPerWarp;
-    float m[kMaxQPerWarp], l[kMaxQPerWarp], acc[kMaxQPerWarp][4], qv[kMaxQPerWarp][4];
-    int qpos[kMaxQPerWarp];
+  constexpr int QW = kAttnQMax / kAttnWarps;  // query vectors per warp
+  float m[QW], l[QW], acc[QW][4];
 #pragma unroll
-    for (int j = 0; j < kMaxQPerWarp; ++j) {
-      m[j] = -INFINITY;
-      l[j] = 0.f;
-      qpos[j] = -1;
+  for (int j = 0; j < QW; ++j) {
+    m[j] = -INFINITY;
+    l[j] = 0.f;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) acc[j][t] = 0.f, qv[j][t] = 0.f;
-      const int qi = q0 + j * kAttnWarps + warp;
-      if (qi < nq) {
-        const int tok = qi / group, hq = kh * group + qi % group;
-        const __nv_bfloat16* qp = q + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD;
+    for (int t = 0; t < 4; ++t) acc[j][t] = 0.f;
+  }
+
+  for (int c = 0; c < n_chunks; ++c) {
+    const int buf = c & 1;
+    mbar_wait(&sm.bar[buf], (c >> 1) & 1);
+    const int kbase = c * kAttnChunk;
+    const __nv_bfloat162* K2 = reinterpret_cast<const __nv_bfloat162*>(sm.k[buf]);
+    const __nv_bfloat16* V = sm.v[buf];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) qv[j][t] = bf2f(qp[lane * 4 + t]) * scale;
-        qpos[j] = ed.pos0 + tok;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) issue(0, 0);
-    for (int p = 0; p < n_pages; ++p) {
-      const int buf = p & 1;
-      if (threadIdx.x == 0 && p + 1 < n_pages) issue(p + 1, buf ^ 1);
-      mbar_wait(&bar[buf], (p >> 1) & 1);
-      const int kbase = p * kPageTokens;
-      for (int jk = 0; jk < kPageTokens; ++jk) {
-        const int kpos = kbase + jk;
-        if (kpos >= ctx) break;
-        float kr[4], vr[4];
+    for (int j = 0; j < QW; ++j) {
+      const int qi = warp + j * kAttnWarps;
+      if (qi >= nq) break;  // warp-uniform
+      const int qpos = ed.pos0 + blk.tok0 + qi / group;
+      const int nk = min(kAttnChunk, qpos + 1 - kbase);  // causal keys of this chunk
+      if (nk <= 0) continue;
+      float sc[kAttnChunk / 32];
+      float cmax = -INFINITY;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          kr[t] = bf2f(sk[buf][jk * HD + lane * 4 + t]);
-          vr[t] = bf2f(sv[buf][jk * HD + lane * 4 + t]);
+      for (int i = 0; i < kAttnChunk / 32; ++i) {
+        const int key = lane + 32 * i;
+        float d = -INFINITY;
+        if (key < nk) {
+          const __nv_bfloat162* kr = K2 + key * (HD / 2);
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+          for (int cp = 0; cp < HD / 2; ++cp) {
+            const int x = (cp + lane) & (HD / 2 - 1);  // rotated: distinct banks per lane
+            const float2 kv2 = __bfloat1622float2(kr[x]);
+            const float2 qv = sm.q[qi][x];
+            a0 += qv.x * kv2.x;
+            a1 += qv.y * kv2.y;
+          }
+          d = a0 + a1;
         }
-#pragma unroll
-        for (int j = 0; j < kMaxQPerWarp; ++j) {
-          if (qpos[j] < 0 || kpos > qpos[j]) continue;  // warp-uniform
-          float dot = qv[j][0] * kr[0] + qv[j][1] * kr[1] + qv[j][2] * kr[2] + qv[j][3] * kr[3];
-          dot = warp_sum(dot);
-          const float mn = fmaxf(m[j], dot);
-          const float corr = __expf(m[j] - mn);
-          const float pj = __expf(dot - mn);
-          l[j] = l[j] * corr + pj;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) acc[j][t] = acc[j][t] * corr + pj * vr[t];
-          m[j] = mn;
-        }
+        sc[i] = d;
+        cmax = fmaxf(cmax, d);
       }
-      __syncthreads();  // everyone done with `buf` before it is refilled
-    }
+      cmax = warp_max(cmax);
+      const float mn = fmaxf(m[j], cmax);
+      const float corr = __expf(m[j] - mn);
+      float ps = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxQPerWarp; ++j) {
-      const int qi = q0 + j * kAttnWarps + warp;
-      if (qi >= nq) continue;
-      const int tok = qi / group, hq = kh * group + qi % group;
-      __nv_bfloat16* op = out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD;
-      const float inv = 1.f / l[j];
+      for (int i = 0; i < kAttnChunk / 32; ++i) {
+        const float pv = (lane + 32 * i < nk) ? __expf(sc[i] - mn) : 0.f;
+        sm.p[warp][lane + 32 * i] = pv;
+        ps += pv;
+      }
+      ps = warp_sum(ps);
+      l[j] = l[j] * corr + ps;
+      m[j] = mn;
+      __syncwarp();
+      float o0 = acc[j][0] * corr, o1 = acc[j][1] * corr, o2 = acc[j][2] * corr, o3 = acc[j][3] * corr;
+      for (int k = 0; k < nk; ++k) {
+        const float pk = sm.p[warp][k];
+        const uint2 raw = *reinterpret_cast<const uint2*>(V + k * HD + lane * 4);
+        const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+        const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+        o0 += pk * v01.x;
+        o1 += pk * v01.y;
+        o2 += pk * v23.x;
+        o3 += pk * v23.y;
+      }
+      acc[j][0] = o0, acc[j][1] = o1, acc[j][2] = o2, acc[j][3] = o3;
+      __syncwarp();
+    }
+    __syncthreads();  // every warp is done with `buf`
+    if (threadIdx.x == 0 && c + 2 < n_chunks) issue(c + 2, buf);
+  }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) op[lane * 4 + t] = f2bf(acc[j][t] * inv);
-    }
-    // phases of bar[] advance once per page per wave; re-init for next wave
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      mbar_init(&bar[0], 1);
-      mbar_init(&bar[1], 1);
-      fence_barrier_init();
-    }
-    __syncthreads();
+  for (int j = 0; j < QW; ++j) {
+    const int qi = warp + j * kAttnWarps;
+    if (qi >= nq) break;
+    const int tok = blk.tok0 + qi / group, hq = kh * group + qi % group;
+    const float inv = 1.f / l[j];
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + lane * 4);
+    op[0] = __floats2bfloat162_rn(acc[j][0] * inv, acc[j][1] * inv);
+    op[1] = __floats2bfloat162_rn(acc[j][2] * inv, acc[j][3] * inv);
   }
 }
 
@@ -349,12 +388,20 @@ cudaError_t launch_rope_kv(const ArStepDev& s, int n_rows, const float* qkv, int
   rope_kv_kernel<<<n_rows, 256, 0, st>>>(s, qkv, n_heads, n_kv, rope, layer, n_layers, q_out, kv);
   return cudaGetLastError();
 }
-cudaError_t launch_attention(const ArStepDev& s, int n_entries, const __nv_bfloat16* q,
+cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat16* q,
                              int n_heads, int n_kv, int layer, int n_layers,
                              const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st) {
-  dim3 grid(n_entries, n_kv);
-  attention_kernel<<<grid, kAttnWarps * 32, 0, st>>>(s, q, n_heads, n_kv, layer, n_layers, kv, out,
-                                                     rsqrtf((float)kHeadDim));
+  if (n_heads / n_kv > 8) return cudaErrorInvalidValue;
+  static bool configured = false;
+  const size_t smem = sizeof(AttnSmem);
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid(n_blocks, n_kv);
+  attention_kernel<<<grid, kAttnWarps * 32, smem, st>>>(s, q, n_heads, n_kv, layer, n_layers, kv, out,
+                                                        1.0f / sqrtf((float)kHeadDim));
   return cudaGetLastError();
 }
 cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,

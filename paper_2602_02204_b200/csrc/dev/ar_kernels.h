@@ -29,11 +29,21 @@ struct ArRowDesc {  // one token row of the step
   uint64_t cond_src; // talker prefill: device address of the upstream hidden row
 };
 
+constexpr int kAttnQTok = 4;  // query tokens per attention block (x group heads)
+
+struct AttnBlockDesc {  // one attention CTA row: tokens [tok0, tok0+ntok) of an entry
+  int32_t entry;
+  int32_t tok0;
+  int32_t ntok;
+  int32_t pad;
+};
+
 struct ArStepDev {
   const ArEntryDesc* entries;
   const ArRowDesc* rows;
   const int32_t* page_table;   // [n_entries][max_pages]
   const int32_t* dec_entries;  // [n_dec] entry index of each decode row
+  const AttnBlockDesc* attn_blocks;
   int32_t max_pages;
 };
 
@@ -47,7 +57,7 @@ cudaError_t launch_rmsnorm(const float* x, int rows, int d, float eps, __nv_bflo
 cudaError_t launch_rope_kv(const ArStepDev& s, int n_rows, const float* qkv, int n_heads, int n_kv,
                            const float2* rope, int layer, int n_layers, __nv_bfloat16* q_out,
                            __nv_bfloat16* kv, cudaStream_t st);
-cudaError_t launch_attention(const ArStepDev& s, int n_entries, const __nv_bfloat16* q,
+cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat16* q,
                              int n_heads, int n_kv, int layer, int n_layers,
                              const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st);
 cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,

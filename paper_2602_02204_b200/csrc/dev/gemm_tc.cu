@@ -38,42 +38,77 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 }
 __device__ __forceinline__ float silu(float x) { return x / (1.f + expf(-x)); }
 
+__device__ __forceinline__ void ld8(const float* p, float (&v)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+}
+__device__ __forceinline__ void st8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+__device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162 h[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  u.x = *reinterpret_cast<uint32_t*>(&h[0]);
+  u.y = *reinterpret_cast<uint32_t*>(&h[1]);
+  u.z = *reinterpret_cast<uint32_t*>(&h[2]);
+  u.w = *reinterpret_cast<uint32_t*>(&h[3]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
 // Applies the fused epilogue to `ncols` finished accumulator columns held in
-// smem as acc[c * 128 + row] (fp32), column c = token tok0 + c.  Thread `row`
-// owns output feature row `row` of the tile; SWIGLU pairs row f (gate) with
-// row f + 64 (up) of the same tile.
+// smem as acc[c * 128 + row] (fp32), column c = token tok0 + c. Each thread
+// owns 8 consecutive output features of one token, so every global access
+// is a 16-byte vector (bf16) or 2x16-byte (fp32); SWIGLU pairs gate row f
+// with up row f + 64 of the same tile.
 template <int EPI>
-__device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int row, int tok0,
-                                         int ncols, const float* acc) {
+__device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0, int ncols,
+                                         const float* acc) {
   __syncthreads();
+  const int t = threadIdx.x;
   if constexpr (EPI == EPI_SWIGLU) {
-    if (row < 64) {
-      const int f = n_tile * 64 + row;
-      __nv_bfloat16* out = static_cast<__nv_bfloat16*>(a.out);
-      for (int c = 0; c < ncols; ++c) {
-        const float g = acc[c * 128 + row], u = acc[c * 128 + row + 64];
-        out[(size_t)(tok0 + c) * a.ldo + f] = f2bf(silu(g) * u);
-      }
+    const int f0 = (t & 7) * 8;
+    for (int c = t >> 3; c < ncols; c += kThreads / 8) {
+      float g[8], u[8], o[8];
+      ld8(acc + c * 128 + f0, g);
+      ld8(acc + c * 128 + 64 + f0, u);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = silu(g[i]) * u[i];
+      st8_bf16(static_cast<__nv_bfloat16*>(a.out) + (size_t)(tok0 + c) * a.ldo + n_tile * 64 + f0, o);
     }
   } else {
-    const int n = n_tile * kBlockM + row;
-    if (n >= a.n_valid) return;
-    for (int c = 0; c < ncols; ++c) {
+    const int r0 = (t & 15) * 8;
+    const int n0 = n_tile * kBlockM + r0;
+    if (n0 >= a.n_valid) return;
+    for (int c = t >> 4; c < ncols; c += kThreads / 16) {
       const int tok = tok0 + c;
-      const float v = acc[c * 128 + row];
+      float v[8];
+      ld8(acc + c * 128 + r0, v);
       if constexpr (EPI == EPI_BF16) {
-        static_cast<__nv_bfloat16*>(a.out)[(size_t)tok * a.ldo + n] = f2bf(v);
+        st8_bf16(static_cast<__nv_bfloat16*>(a.out) + (size_t)tok * a.ldo + n0, v);
       } else if constexpr (EPI == EPI_F32) {
-        static_cast<float*>(a.out)[(size_t)tok * a.ldo + n] = v;
+        st8(static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0, v);
       } else if constexpr (EPI == EPI_RESID) {
-        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n;
-        *r = *r + v;
+        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
+        float x[8];
+        ld8(r, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] += v[i];
+        st8(r, x);
       } else if constexpr (EPI == EPI_GATED_RESID) {
-        const float g = a.gate[(size_t)(tok / a.rows_per_group) * a.ldg + a.gate_off + n];
-        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n;
-        *r = *r + g * v;
+        float g[8], x[8];
+        ld8(a.gate + (size_t)(tok / a.rows_per_group) * a.ldg + a.gate_off + n0, g);
+        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
+        ld8(r, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] += g[i] * v[i];
+        st8(r, x);
       } else if constexpr (EPI == EPI_GELU) {
-        static_cast<__nv_bfloat16*>(a.out)[(size_t)tok * a.ldo + n] = f2bf(gelu_tanh(v));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = gelu_tanh(v[i]);
+        st8_bf16(static_cast<__nv_bfloat16*>(a.out) + (size_t)tok * a.ldo + n0, v);
       }
     }
   }
@@ -173,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 16; ++j) red[(c * 16 + j) * 128 + row] = v[j];
   }
   if (a.splits == 1) {
-    epi_cols<EPI>(a, n_tile, row, m0, cols, red);
+    epi_cols<EPI>(a, n_tile, m0, cols, red);
   } else {
     // The split CTAs of this tile form one cluster (rank == split). Each
     // reduces a slice of token columns across all ranks, in rank order, so
@@ -191,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int z = 0; z < S; ++z) acc += dsmem_ld_f32(dsmem_map(red_s + off, z));
       fin[(c - c0) * 128 + row] = acc;
     }
-    if (c1 > c0) epi_cols<EPI>(a, n_tile, row, m0 + c0, c1 - c0, fin);
+    if (c1 > c0) epi_cols<EPI>(a, n_tile, m0 + c0, c1 - c0, fin);
     cluster_sync();  // keep our partial alive until every rank has read it
   }
 
@@ -263,6 +298,9 @@ int gemm_block_n(int M) {
 cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, const GemmEpilogue& e,
                      cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
+  // vectorised epilogue: 8-element aligned rows
+  if (e.ldo % 8 != 0 || (reinterpret_cast<uintptr_t>(e.out) & 15) != 0 || w.N % 8 != 0) return cudaErrorInvalidValue;
+  if (epi == EPI_GATED_RESID && (e.ldg % 4 != 0 || e.gate_off % 4 != 0)) return cudaErrorInvalidValue;
   if (M > x.rows_cap || w.K != x.K) return cudaErrorInvalidValue;
   GemmArgs a{};
   a.M = M;

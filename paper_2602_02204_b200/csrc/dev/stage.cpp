@@ -302,12 +302,16 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   const size_t off_rows = align16((size_t)ne * sizeof(ArEntryDesc));
   const size_t off_pt = off_rows + align16((size_t)n_rows * sizeof(ArRowDesc));
   const size_t off_dec = off_pt + align16((size_t)ne * st->max_pages * sizeof(int32_t));
-  const size_t total = off_dec + align16((size_t)ne * sizeof(int32_t));
+  const size_t off_blk = off_dec + align16((size_t)ne * sizeof(int32_t));
+  const size_t max_blocks = (size_t)n_rows + ne;  // >= sum ceil(span / kAttnQTok)
+  const size_t total = off_blk + align16(max_blocks * sizeof(AttnBlockDesc));
   staging_reserve(st->desc, total);
   auto* ents = reinterpret_cast<ArEntryDesc*>(st->desc.host);
   auto* rows = reinterpret_cast<ArRowDesc*>(st->desc.host + off_rows);
   auto* pt = reinterpret_cast<int32_t*>(st->desc.host + off_pt);
   auto* dec = reinterpret_cast<int32_t*>(st->desc.host + off_dec);
+  auto* blks = reinterpret_cast<AttnBlockDesc*>(st->desc.host + off_blk);
+  int n_blocks = 0;
   std::vector<int> dec_list;
   int r = 0, n_prefill_rows = 0;
   for (int e = 0; e < ne; ++e) {
@@ -332,6 +336,8 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
     }
     for (size_t k = 0; k < s.pages.size() && (int)k < st->max_pages; ++k)
       pt[(size_t)e * st->max_pages + k] = s.pages[k];
+    for (int t0 = 0; t0 < b->span[e]; t0 += kAttnQTok)
+      blks[n_blocks++] = AttnBlockDesc{e, t0, std::min(kAttnQTok, b->span[e] - t0), 0};
     for (int t = 0; t < b->span[e]; ++t, ++r) {
       ArRowDesc& rd = rows[r];
       rd.entry = e;
@@ -362,6 +368,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + off_rows);
   sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + off_pt);
   sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + off_dec);
+  sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + off_blk);
   sd.max_pages = st->max_pages;
 
   const auto& m = st->m;
@@ -384,7 +391,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       e.ldo = (H + 2 * KVH) * kHeadDim;
       OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_F32, e, s));
       OMNI_KERNEL(launch_rope_kv(sd, n_rows, st->qkv, H, KVH, st->rope, l, L, st->q, st->kv, s));
-      OMNI_KERNEL(launch_attention(sd, ne, st->q, H, KVH, l, L, st->kv, st->attn, s));
+      OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, s));
       e.out = st->x;
       e.ldo = d;
       OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID, e, s));
