@@ -261,6 +261,20 @@ void om_seq_free(om_seq* s) {
 }
 int om_seq_len(const om_seq* s) { return s->len; }
 
+/* Fused RMSNorm as the B200 kernels compute it (gemm_tc.cu EPI_RESID_NORM /
+ * GemmEpilogue::ss_in): the GEMM consumes bf16(x) un-normalised and its
+ * output row is scaled by inv = rsqrt(sum_tiles(sum_{i in tile} x_i^2)/d + eps),
+ * tiles of 128 features summed in tile order. */
+static float rms_inv_tiled(const float* x, int d) {
+  float ss = 0.f;
+  for (int t = 0; t < d; t += 128) {
+    float p = 0.f;
+    for (int i = t; i < t + 128 && i < d; ++i) p += x[i] * x[i];
+    ss += p;
+  }
+  return 1.f / sqrtf(ss / d + 1e-6f);
+}
+
 static void rmsnorm_bf16(const float* x, int d, float* y) {
   float ss = 0.f;
   for (int i = 0; i < d; ++i) ss += x[i] * x[i];
@@ -331,11 +345,13 @@ int om_ar_feed(const om_model* mo, om_seq* s, int n, const int* tokens, const in
   const int half = hd / 2, group = H / KVH;
   for (int l = 0; l < L; ++l) {
     const ArLayer* ly = &mo->layers[l];
-    for (int i = 0; i < n; ++i) rmsnorm_bf16(x + (size_t)i * d, d, xn + (size_t)i * d);
+    for (size_t i = 0; i < (size_t)n * d; ++i) xn[i] = bf16r(x[i]);
     gemm(xn, n, &ly->wqkv, qkv);
     for (int i = 0; i < n; ++i) {
       const int pos = s->len + i;
-      const float* row = qkv + (size_t)i * qkv_w;
+      float* row = qkv + (size_t)i * qkv_w;
+      const float inv = rms_inv_tiled(x + (size_t)i * d, d);
+      for (int c = 0; c < qkv_w; ++c) row[c] *= inv;
       for (int h = 0; h < H + 2 * KVH; ++h)
         for (int j = 0; j < half; ++j) {
           float a = row[h * hd + j], b = row[h * hd + j + half], o0 = a, o1 = b;
@@ -383,10 +399,16 @@ int om_ar_feed(const om_model* mo, om_seq* s, int n, const int* tokens, const in
       }
     gemm(at, n, &ly->wo, tmp);
     for (size_t i = 0; i < (size_t)n * d; ++i) x[i] += tmp[i];
-    for (int i = 0; i < n; ++i) rmsnorm_bf16(x + (size_t)i * d, d, xn + (size_t)i * d);
+    for (size_t i = 0; i < (size_t)n * d; ++i) xn[i] = bf16r(x[i]);
     gemm(xn, n, &ly->wg, g);
     gemm(xn, n, &ly->wu, u);
-    for (size_t i = 0; i < (size_t)n * ff; ++i) g[i] = bf16r(silu(g[i]) * u[i]);
+    for (int i = 0; i < n; ++i) {
+      const float inv = rms_inv_tiled(x + (size_t)i * d, d);
+      for (int c = 0; c < ff; ++c) {
+        const size_t k = (size_t)i * ff + c;
+        g[k] = bf16r(silu(g[k] * inv) * (u[k] * inv));
+      }
+    }
     gemm(g, n, &ly->wd, tmp);
     for (size_t i = 0; i < (size_t)n * d; ++i) x[i] += tmp[i];
   }

@@ -1,8 +1,9 @@
 // K2-K4: the non-GEMM kernels of one batched AR step (Thinker / Talker).
 //
-//   embed            token (+ talker conditioning) -> fp32 residual rows
-//   rmsnorm          fp32 residual -> bf16 GEMM input (no gain; folded away)
-//   rope_kv          fp32 QKV -> RoPE(q,k) -> q bf16 rows, k/v into paged KV
+//   embed            token (+ talker conditioning) -> fp32 residual rows,
+//                    bf16 copy + sums of squares for the fused RMSNorm
+//   (RMSNorm and RoPE + paged-KV append are fused into the GEMM epilogues,
+//    gemm_tc.cu EPI_RESID_NORM / EPI_ROPE_KV / GemmEpilogue::ss_in)
 //   attention        paged-KV causal attention for mixed decode / chunked-
 //                    prefill entries (GQA), pages staged by 1-D TMA bulk copies
 //   final_gather     final RMSNorm of DECODE rows -> hidden rows (bf16),
@@ -16,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include "ar_kernels.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace omni_dev {
@@ -25,39 +27,69 @@ namespace omni_dev {
 //   cond_j = E_t[tok] + (W_h h_j) (precomputed GEMM rows in `hproj`), stored
 //   to the sequence's conditioning table, x = cond_j.  Talker decode step m:
 //   x = E_c[prev] + cond_{m/4}.
+// Also emits the first layer's fused-RMSNorm inputs: xb = bf16(x) and the
+// per-128-feature sums of squares ss[row][tile] (same fixed 16-lane order as
+// the EPI_RESID_NORM GEMM epilogue).
 // ---------------------------------------------------------------------------
 __global__ void embed_kernel(const ArStepDev s, const __nv_bfloat16* __restrict__ emb,
                              const __nv_bfloat16* __restrict__ emb2, const float* __restrict__ hproj,
                              float* __restrict__ cond_table, int cond_rows, int d, int start_id,
-                             float* __restrict__ x) {
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                             float* __restrict__ ss_out, int ss_ld) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const ArRowDesc rd = s.rows[r];
   const ArEntryDesc ed = s.entries[rd.entry];
   const int tok = rd.token < 0 ? start_id : rd.token;
   float* xr = x + (size_t)r * d;
-  if (emb2 == nullptr) {  // thinker
-    const __nv_bfloat16* e = emb + (size_t)tok * d;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = bf2f(e[i]);
-    return;
-  }
-  float* cond = cond_table + ((size_t)ed.slot * cond_rows + rd.cond_row) * d;
-  if (!ed.is_decode) {  // talker prefill: build conditioning row j
-    const __nv_bfloat16* et = emb + (size_t)tok * d;
-    const float* hp = hproj + (size_t)r * d;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
-      const float c = bf2f(et[i]) + hp[i];
-      cond[i] = c;
-      xr[i] = c;
+  const int mode = emb2 == nullptr ? 0 : (ed.is_decode ? 2 : 1);
+  float* cond = mode ? cond_table + ((size_t)ed.slot * cond_rows + rd.cond_row) * d : nullptr;
+  const __nv_bfloat16* e = mode == 2 ? emb2 + (size_t)tok * d : emb + (size_t)tok * d;
+  for (int base = 0; base < d; base += blockDim.x * 8) {
+    const int i0 = base + threadIdx.x * 8;
+    const bool live = i0 < d;
+    float ss = 0.f;
+    if (live) {
+      float v[8];
+      const uint4 raw = *reinterpret_cast<const uint4*>(e + i0);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h2[k]);
+        v[2 * k] = f.x, v[2 * k + 1] = f.y;
+      }
+      if (mode == 1) {
+        const float* hp = hproj + (size_t)r * d + i0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += hp[k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cond[i0 + k] = v[k];
+      } else if (mode == 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += cond[i0 + k];
+      }
+      uint4 ob;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&ob);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o2[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      *reinterpret_cast<uint4*>(xb + (size_t)r * d + i0) = ob;
+      reinterpret_cast<float4*>(xr + i0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(xr + i0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss += v[k] * v[k];
     }
-  } else {
-    const __nv_bfloat16* ec = emb2 + (size_t)tok * d;
-    for (int i = threadIdx.x; i < d; i += blockDim.x) xr[i] = bf2f(ec[i]) + cond[i];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (live && (threadIdx.x & 15) == 0) ss_out[(size_t)r * ss_ld + i0 / 128] = ss;
   }
 }
 
 // Talker: gather the upstream FIX16 hidden rows (2-byte aligned inside the
 // packed connector payload) into an aligned bf16 GEMM input.
 __global__ void gather_cond_kernel(const ArStepDev s, int d, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const uint64_t src = s.rows[r].cond_src;
   __nv_bfloat16* o = out + (size_t)r * d;
@@ -70,9 +102,6 @@ __global__ void gather_cond_kernel(const ArStepDev s, int d, __nv_bfloat16* __re
   for (int i = threadIdx.x; i < d; i += blockDim.x) q[i] = p[i];
 }
 
-// ---------------------------------------------------------------------------
-// RMSNorm without gain: y = bf16(x / sqrt(mean(x^2) + eps)).  One CTA/row.
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -83,62 +112,6 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   const int nw = blockDim.x >> 5;
   for (int i = 0; i < nw; ++i) t += red[i];  // fixed order: deterministic
   return t;
-}
-
-__global__ void rmsnorm_kernel(const float* __restrict__ x, int d, float eps,
-                               __nv_bfloat16* __restrict__ y) {
-  __shared__ float red[32];
-  const float* xr = x + (size_t)blockIdx.x * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
-  const float tot = block_sum(ss, red);
-  const float inv = rsqrtf(tot / d + eps);
-  __nv_bfloat16* yr = y + (size_t)blockIdx.x * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) yr[i] = f2bf(xr[i] * inv);
-}
-
-// ---------------------------------------------------------------------------
-// RoPE (rotate-half, pairs (i, i+64) of a 128-dim head) on fp32 QKV, then
-// q -> bf16 rows, k/v -> bf16 paged KV at the row's position.
-// KV page layout: [page][layer][k|v][kv_head][16 tokens][head_dim].
-// ---------------------------------------------------------------------------
-__global__ void rope_kv_kernel(const ArStepDev s, const float* __restrict__ qkv, int n_heads,
-                               int n_kv, const float2* __restrict__ rope, int layer, int n_layers,
-                               __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kv) {
-  constexpr int HD = kHeadDim, HALF = kHeadDim / 2;
-  const int r = blockIdx.x;
-  const ArRowDesc rd = s.rows[r];
-  const ArEntryDesc ed = s.entries[rd.entry];
-  const int pos = rd.pos;
-  const int page = s.page_table[rd.entry * s.max_pages + pos / kPageTokens];
-  const int slot_tok = pos % kPageTokens;
-  const int width = (n_heads + 2 * n_kv) * HD;
-  const float* row = qkv + (size_t)r * width;
-  // heads: [0, n_heads) q, [n_heads, n_heads + n_kv) k, then v
-  for (int t = threadIdx.x; t < (n_heads + 2 * n_kv) * HALF; t += blockDim.x) {
-    const int h = t / HALF, i = t % HALF;
-    const float a = row[h * HD + i], b = row[h * HD + i + HALF];
-    float o0 = a, o1 = b;
-    if (h < n_heads + n_kv) {
-      const float2 cs = rope[(size_t)pos * HALF + i];  // (cos, sin)
-      o0 = a * cs.x - b * cs.y;
-      o1 = b * cs.x + a * cs.y;
-    }
-    if (h < n_heads) {
-      __nv_bfloat16* q = q_out + (size_t)r * n_heads * HD + h * HD;
-      q[i] = f2bf(o0);
-      q[i + HALF] = f2bf(o1);
-    } else {
-      const int is_v = h >= n_heads + n_kv;
-      const int kh = is_v ? h - n_heads - n_kv : h - n_heads;
-      __nv_bfloat16* dst =
-          kv + ((((size_t)page * n_layers + layer) * 2 + is_v) * n_kv + kh) * kPageTokens * HD +
-          (size_t)slot_tok * HD;
-      dst[i] = f2bf(o0);
-      dst[i + HALF] = f2bf(o1);
-    }
-  }
-  (void)ed;
 }
 
 // ---------------------------------------------------------------------------
@@ -173,6 +146,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   extern __shared__ __align__(128) uint8_t attn_smem_raw[];
   AttnSmem& sm = *reinterpret_cast<AttnSmem*>(attn_smem_raw);
 
+  pdl_wait();
+  pdl_trigger();
   const AttnBlockDesc blk = s.attn_blocks[blockIdx.x];
   const int kh = blockIdx.y;
   const ArEntryDesc ed = s.entries[blk.entry];
@@ -311,6 +286,8 @@ __global__ void final_gather_kernel(const ArStepDev s, const float* __restrict__
                                     __nv_bfloat16* __restrict__ hout, __nv_bfloat16* __restrict__ ring,
                                     int ring_rows) {
   __shared__ float red[32];
+  pdl_wait();
+  pdl_trigger();
   const int e = s.dec_entries[blockIdx.x];
   const ArEntryDesc ed = s.entries[e];
   const float* xr = x + (size_t)ed.row0 * d;  // decode entries have exactly one row
@@ -331,6 +308,8 @@ __global__ void final_gather_kernel(const ArStepDev s, const float* __restrict__
 // top-2 margin used by the teacher-forced parity rule.
 __global__ void argmax_kernel(const float* __restrict__ logits, int ld, int lo, int hi,
                               int* __restrict__ tok_out, float* __restrict__ margin_out) {
+  pdl_wait();
+  pdl_trigger();
   const float* row = logits + (size_t)blockIdx.x * ld;
   float b1 = -INFINITY, b2 = -INFINITY;
   int i1 = 0x7fffffff;
@@ -368,54 +347,35 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int ld, int lo, 
 // ---------------------------------------------------------------------------
 cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,
                          const __nv_bfloat16* emb2, const float* hproj, float* cond_table,
-                         int cond_rows, int d, int start_id, float* x, cudaStream_t st) {
-  embed_kernel<<<n_rows, 256, 0, st>>>(s, emb, emb2, hproj, cond_table, cond_rows, d, start_id, x);
-  return cudaGetLastError();
+                         int cond_rows, int d, int start_id, float* x, __nv_bfloat16* xb, float* ss,
+                         int ss_ld, cudaStream_t st) {
+  if (d % 128 != 0) return cudaErrorInvalidValue;
+  return launch_k(embed_kernel, dim3(n_rows), dim3(256), 0, st, 1, s, emb, emb2, hproj, cond_table,
+                  cond_rows, d, start_id, x, xb, ss, ss_ld);
 }
 cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloat16* out,
                                cudaStream_t st) {
-  gather_cond_kernel<<<n_rows, 256, 0, st>>>(s, d, out);
-  return cudaGetLastError();
-}
-cudaError_t launch_rmsnorm(const float* x, int rows, int d, float eps, __nv_bfloat16* y,
-                           cudaStream_t st) {
-  rmsnorm_kernel<<<rows, 256, 0, st>>>(x, d, eps, y);
-  return cudaGetLastError();
-}
-cudaError_t launch_rope_kv(const ArStepDev& s, int n_rows, const float* qkv, int n_heads, int n_kv,
-                           const float2* rope, int layer, int n_layers, __nv_bfloat16* q_out,
-                           __nv_bfloat16* kv, cudaStream_t st) {
-  rope_kv_kernel<<<n_rows, 256, 0, st>>>(s, qkv, n_heads, n_kv, rope, layer, n_layers, q_out, kv);
-  return cudaGetLastError();
+  return launch_k(gather_cond_kernel, dim3(n_rows), dim3(256), 0, st, 1, s, d, out);
 }
 cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat16* q,
                              int n_heads, int n_kv, int layer, int n_layers,
                              const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st) {
   if (n_heads / n_kv > 8) return cudaErrorInvalidValue;
-  static bool configured = false;
+  static std::atomic<uint64_t> configured{0};
   const size_t smem = sizeof(AttnSmem);
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  dim3 grid(n_blocks, n_kv);
-  attention_kernel<<<grid, kAttnWarps * 32, smem, st>>>(s, q, n_heads, n_kv, layer, n_layers, kv, out,
-                                                        1.0f / sqrtf((float)kHeadDim));
-  return cudaGetLastError();
+  if (cudaError_t e = smem_attr_once(attention_kernel, smem, configured); e != cudaSuccess) return e;
+  return launch_k(attention_kernel, dim3(n_blocks, n_kv), dim3(kAttnWarps * 32), smem, st, 1, s, q, n_heads,
+                  n_kv, layer, n_layers, kv, out, 1.0f / sqrtf((float)kHeadDim));
 }
 cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
                                 cudaStream_t st) {
-  if (n_dec == 0) return cudaSuccess;
-  final_gather_kernel<<<n_dec, 256, 0, st>>>(s, x, d, eps, hout, ring, ring_rows);
-  return cudaGetLastError();
+  return launch_k(final_gather_kernel, dim3(n_dec), dim3(256), 0, st, 1, s, x, d, eps, hout, ring,
+                  ring_rows);
 }
 cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
                           cudaStream_t st) {
-  if (n == 0) return cudaSuccess;
-  argmax_kernel<<<n, 32, 0, st>>>(logits, ld, lo, hi, tok, margin);
-  return cudaGetLastError();
+  return launch_k(argmax_kernel, dim3(n), dim3(32), 0, st, 1, logits, ld, lo, hi, tok, margin);
 }
 
 }  // namespace omni_dev

@@ -49,14 +49,10 @@ struct ArStepDev {
 
 cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,
                          const __nv_bfloat16* emb2, const float* hproj, float* cond_table,
-                         int cond_rows, int d, int start_id, float* x, cudaStream_t st);
+                         int cond_rows, int d, int start_id, float* x, __nv_bfloat16* xb, float* ss,
+                         int ss_ld, cudaStream_t st);
 cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloat16* out,
                                cudaStream_t st);
-cudaError_t launch_rmsnorm(const float* x, int rows, int d, float eps, __nv_bfloat16* y,
-                           cudaStream_t st);
-cudaError_t launch_rope_kv(const ArStepDev& s, int n_rows, const float* qkv, int n_heads, int n_kv,
-                           const float2* rope, int layer, int n_layers, __nv_bfloat16* q_out,
-                           __nv_bfloat16* kv, cudaStream_t st);
 cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat16* q,
                              int n_heads, int n_kv, int layer, int n_layers,
                              const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st);

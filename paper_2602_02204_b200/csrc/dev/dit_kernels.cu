@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "dit_kernels.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 #include "rng.h"
 
@@ -15,6 +16,8 @@ namespace omni_dev {
 // x0[row, ch] ~ N(0,1) keyed by (request, global token position, sample, ch).
 __global__ void dit_noise_kernel(const DitTokDesc* __restrict__ toks, int S, int C, uint64_t seed,
                                  float* __restrict__ x, int rows) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)rows * C) return;
   const int r = (int)(i / C), ch = (int)(i % C);
@@ -28,6 +31,8 @@ __global__ void dit_noise_kernel(const DitTokDesc* __restrict__ toks, int S, int
 __global__ void dit_cond_kernel(const DitTokDesc* __restrict__ toks, const __nv_bfloat16* __restrict__ tok_emb,
                                 const __nv_bfloat16* __restrict__ t_emb, int step, int d,
                                 __nv_bfloat16* __restrict__ cvec) {
+  pdl_wait();
+  pdl_trigger();
   const int p = blockIdx.x;
   const __nv_bfloat16* e = tok_emb + (size_t)toks[p].id * d;
   const __nv_bfloat16* te = t_emb + (size_t)step * d;
@@ -37,13 +42,29 @@ __global__ void dit_cond_kernel(const DitTokDesc* __restrict__ toks, const __nv_
   }
 }
 
+// dmod[p] = table[id_p]: the adaLN modulation rows are a function of
+// (conditioning id, Euler step) only, precomputed once per stage.
+__global__ void dit_mod_gather_kernel(const DitTokDesc* __restrict__ toks, const float* __restrict__ table,
+                                      int ld4, float4* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int p = blockIdx.x;
+  const float4* src = reinterpret_cast<const float4*>(table) + (size_t)toks[p].id * ld4;
+  float4* dst = out + (size_t)p * ld4;
+  for (int i = threadIdx.x; i < ld4; i += blockDim.x) dst[i] = src[i];
+}
+
 __global__ void dit_to_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ y) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i] = f2bf(x[i]);
 }
 
 __global__ void dit_add_pos_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ pos_emb,
                                    int S, int d, int rows) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.x;
   const __nv_bfloat16* pe = pos_emb + (size_t)(r % S) * d;
   for (int i = threadIdx.x; i < d; i += blockDim.x) h[(size_t)r * d + i] += bf2f(pe[i]);
@@ -65,6 +86,8 @@ __device__ __forceinline__ float block_sum2(float v, float* red) {
 __global__ void dit_ln_mod_kernel(const float* __restrict__ h, int d, const float* __restrict__ mod,
                                   int ld_mod, int shift_off, int scale_off, int S,
                                   __nv_bfloat16* __restrict__ a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const float* hr = h + (size_t)r * d;
@@ -89,6 +112,8 @@ __global__ void dit_ln_mod_kernel(const float* __restrict__ h, int d, const floa
 __global__ void __launch_bounds__(128)
     dit_attn_kernel(const __nv_bfloat16* __restrict__ qkv, int d, int n_heads,
                     __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int S = kDitSamples, HD = 128;
   __shared__ float sq[S][HD + 1], sk[S][HD + 1], sv[S][HD];
   __shared__ float sp[S][S + 1];
@@ -136,6 +161,8 @@ __global__ void __launch_bounds__(128)
 // x += dt * v; on the final step also quantise channel 0 to an int32 sample.
 __global__ void dit_euler_kernel(float* __restrict__ x, const float* __restrict__ v, int C, int rows,
                                  float dt, int last, int32_t* __restrict__ samples) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)rows * C) return;
   const float nx = x[i] + dt * v[i];
@@ -152,38 +179,37 @@ cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t 
                       cudaStream_t st) {
   const int rows = n_tok * S;
   const int64_t n = (int64_t)rows * C;
-  dit_noise_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(toks, S, C, seed, x, rows);
-  return cudaGetLastError();
+  return launch_k(dit_noise_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, toks, S, C, seed, x, rows);
 }
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st) {
-  dit_cond_kernel<<<n_tok, 256, 0, st>>>(toks, tok_emb, t_emb, step, d, cvec);
-  return cudaGetLastError();
+  return launch_k(dit_cond_kernel, dim3(n_tok), dim3(256), 0, st, 1, toks, tok_emb, t_emb, step, d, cvec);
+}
+cudaError_t dit_mod_gather(const DitTokDesc* toks, int n_tok, const float* table, int ld_mod, float* out,
+                           cudaStream_t st) {
+  if (ld_mod % 4 != 0) return cudaErrorInvalidValue;
+  return launch_k(dit_mod_gather_kernel, dim3(n_tok), dim3(256), 0, st, 1, toks, table, ld_mod / 4,
+                  reinterpret_cast<float4*>(out));
 }
 cudaError_t dit_to_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
-  dit_to_bf16_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, n, y);
-  return cudaGetLastError();
+  return launch_k(dit_to_bf16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, x, n, y);
 }
 cudaError_t dit_add_pos(float* h, const __nv_bfloat16* pos_emb, int S, int d, int rows, cudaStream_t st) {
-  dit_add_pos_kernel<<<rows, 256, 0, st>>>(h, pos_emb, S, d, rows);
-  return cudaGetLastError();
+  return launch_k(dit_add_pos_kernel, dim3(rows), dim3(256), 0, st, 1, h, pos_emb, S, d, rows);
 }
 cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod, int ld_mod, int shift_off,
                        int scale_off, int S, __nv_bfloat16* a, cudaStream_t st) {
-  dit_ln_mod_kernel<<<rows, 256, 0, st>>>(h, d, mod, ld_mod, shift_off, scale_off, S, a);
-  return cudaGetLastError();
+  return launch_k(dit_ln_mod_kernel, dim3(rows), dim3(256), 0, st, 1, h, d, mod, ld_mod, shift_off, scale_off, S, a);
 }
 cudaError_t dit_attn(const __nv_bfloat16* qkv, int n_tok, int d, int n_heads, __nv_bfloat16* out,
                      cudaStream_t st) {
   dim3 grid(n_tok, n_heads);
-  dit_attn_kernel<<<grid, 128, 0, st>>>(qkv, d, n_heads, out);
-  return cudaGetLastError();
+  return launch_k(dit_attn_kernel, dim3(grid), dim3(128), 0, st, 1, qkv, d, n_heads, out);
 }
 cudaError_t dit_euler(float* x, const float* v, int C, int rows, float dt, int last, int32_t* samples,
                       cudaStream_t st) {
   const int64_t n = (int64_t)rows * C;
-  dit_euler_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, v, C, rows, dt, last, samples);
-  return cudaGetLastError();
+  return launch_k(dit_euler_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, x, v, C, rows, dt, last, samples);
 }
 
 }  // namespace omni_dev

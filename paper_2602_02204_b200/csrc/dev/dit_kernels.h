@@ -23,6 +23,8 @@ cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t 
                       cudaStream_t st);
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st);
+cudaError_t dit_mod_gather(const DitTokDesc* toks, int n_tok, const float* table, int ld_mod, float* out,
+                           cudaStream_t st);
 cudaError_t dit_to_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st);
 cudaError_t dit_add_pos(float* h, const __nv_bfloat16* pos_emb, int S, int d, int rows, cudaStream_t st);
 cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod, int ld_mod, int shift_off,

@@ -16,6 +16,21 @@ enum GemmEpi : int {
   EPI_GATED_RESID = 3,  // R_f32[tok, n] += gate[tok/G, off+n] * acc   (DiT adaLN gate)
   EPI_SWIGLU = 4,       // act_bf16[tok, f] = silu(acc[gate f]) * acc[up f]  (tile-interleaved)
   EPI_GELU = 5,         // Y_bf16[tok, n] = gelu_tanh(acc)
+  EPI_RESID_NORM = 6,   // R_f32[tok, n] += acc; Xb_bf16[tok, n] = bf16(R); ss_out[tok, tile] = sum R^2
+  EPI_ROPE_KV = 7,      // one tile = one 128-dim head of QKV: RoPE(q,k), q -> q_out rows, k/v -> paged KV
+};
+
+// Fused RoPE + paged-KV append (EPI_ROPE_KV): the QKV GEMM tile n is head n
+// (q heads, then k heads, then v heads), so the rotate-half pairs (i, i+64)
+// live in one tile. `rows` are the step's ArRowDesc (ar_kernels.h).
+struct RopeKvArgs {
+  const void* rows = nullptr;
+  const int32_t* page_table = nullptr;
+  int max_pages = 0;
+  const float2* table = nullptr;  // [pos][64] (cos, sin)
+  __nv_bfloat16* q_out = nullptr;
+  __nv_bfloat16* kv = nullptr;
+  int n_heads = 0, n_kv = 0, layer = 0, n_layers = 0;
 };
 
 // A weight matrix W[N_pad, K] bf16 row-major resident in HBM, plus its TMA
@@ -44,6 +59,17 @@ struct GemmEpilogue {
   int ldo = 0;
   const float* gate = nullptr;
   int ldg = 0, gate_off = 0, rows_per_group = 1;
+  // Fused RMSNorm of the GEMM input X (un-normalised bf16 rows): every output
+  // column (token) is scaled by rsqrt(sum_{j<ss_n} ss_in[tok*ss_ld+j] / norm_d + eps),
+  // the per-128-feature partial sums of squares written by the producer
+  // (EPI_RESID_NORM / the embed kernel), summed in fixed j order.
+  const float* ss_in = nullptr;
+  int ss_ld = 0, ss_n = 0;
+  float norm_d = 0.f, norm_eps = 0.f;
+  // EPI_RESID_NORM outputs (ld of xb = ldo, of ss_out = ss_ld)
+  __nv_bfloat16* xb = nullptr;
+  float* ss_out = nullptr;
+  RopeKvArgs rope;
 };
 
 // Kernel-side argument block.
@@ -53,14 +79,21 @@ struct GemmArgs {
   int ldo;
   const float* gate;
   int ldg, gate_off, rows_per_group;
+  const float* ss_in;
+  int ss_ld, ss_n;
+  float norm_d, norm_eps;
+  __nv_bfloat16* xb;
+  float* ss_out;
+  RopeKvArgs rope;
 };
 
 int gemm_block_n(int M);
-int gemm_choose_splits(int N_pad, int K, int max_splits);
-// max_splits: 8 for decode-path (weight-streaming) matrices, 1 for the
-// compute-bound DiT matrices. The choice is frozen into the weight.
+int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas = 296);
+// max_splits / target_ctas: 8 / 296 for decode-path (weight-streaming)
+// matrices, 4 / 64 for the compute-bound DiT matrices (which run 2-3 token
+// tiles). The choice is frozen into the weight (batch invariance).
 bool gemm_make_weight(GemmWeight& w, const __nv_bfloat16* ptr, int N, int N_pad, int K,
-                      int max_splits);
+                      int max_splits, int target_ctas = 296);
 bool gemm_make_input(GemmInput& x, const __nv_bfloat16* ptr, int rows_cap, int K);
 cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi,
                      const GemmEpilogue& e, cudaStream_t st);

@@ -39,26 +39,27 @@ bool encode_2d(CUtensorMap& m, const void* ptr, uint64_t rows, uint64_t K, uint3
 
 }  // namespace
 
-int gemm_choose_splits(int N_pad, int K, int max_splits) {
-  // Fill two CTAs per SM (148 SMs) with at least two 64-wide K blocks per
-  // split; one cluster (<= 8 CTAs) per output tile. Depends on the weight
-  // shape only — never on the batch.
+int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas) {
+  // Fill `target_ctas` (decode weights: two CTAs per SM of 148 SMs, one
+  // m-tile; DiT weights: ~64 tiles x the typical 2-3 m-tiles) with at least
+  // two 64-wide K blocks per split; one cluster (<= 8 CTAs) per output tile.
+  // Depends on the weight shape only — never on the batch.
   const int tiles = N_pad / 128;
   const int kb = K / 64;
   int s = 1;
-  while (s * 2 <= max_splits && tiles * s * 2 <= 296 && (kb % (s * 2)) == 0 && kb / (s * 2) >= 2)
+  while (s * 2 <= max_splits && tiles * s * 2 <= target_ctas && (kb % (s * 2)) == 0 && kb / (s * 2) >= 2)
     s *= 2;
   return s;
 }
 
 bool gemm_make_weight(GemmWeight& w, const __nv_bfloat16* ptr, int N, int N_pad, int K,
-                      int max_splits) {
+                      int max_splits, int target_ctas) {
   if (N_pad % 128 != 0 || K % 64 != 0 || N > N_pad) return false;
   w.ptr = ptr;
   w.N = N;
   w.N_pad = N_pad;
   w.K = K;
-  w.splits = gemm_choose_splits(N_pad, K, max_splits < 1 ? 1 : (max_splits > 8 ? 8 : max_splits));
+  w.splits = gemm_choose_splits(N_pad, K, max_splits < 1 ? 1 : (max_splits > 8 ? 8 : max_splits), target_ctas);
   return encode_2d(w.tmap, ptr, N_pad, K, 128);
 }
 

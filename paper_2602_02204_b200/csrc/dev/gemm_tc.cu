@@ -21,7 +21,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "ar_kernels.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace omni_dev {
@@ -58,14 +60,31 @@ __device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float (&v)[8]) 
   *reinterpret_cast<uint4*>(p) = u;
 }
 
+// Per-token input-RMS scale of the fused RMSNorm (GemmEpilogue::ss_in):
+// inv[c] = rsqrt(sum_j ss_in[tok0 + c][j] / d + eps), j in fixed order.
+__device__ __forceinline__ void input_scales(const GemmArgs& a, int tok0, int ncols, float* inv) {
+  for (int c = threadIdx.x; c < ncols; c += kThreads) {
+    float s = 0.f;
+    if (a.ss_in) {
+      const float* p = a.ss_in + (size_t)(tok0 + c) * a.ss_ld;
+      for (int j = 0; j < a.ss_n; ++j) s += p[j];
+      inv[c] = rsqrtf(s / a.norm_d + a.norm_eps);
+    } else {
+      inv[c] = 1.f;
+    }
+  }
+}
+
 // Applies the fused epilogue to `ncols` finished accumulator columns held in
 // smem as acc[c * 128 + row] (fp32), column c = token tok0 + c. Each thread
 // owns 8 consecutive output features of one token, so every global access
 // is a 16-byte vector (bf16) or 2x16-byte (fp32); SWIGLU pairs gate row f
-// with up row f + 64 of the same tile.
+// with up row f + 64 of the same tile, ROPE_KV rotates feature f with f + 64.
 template <int EPI>
 __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0, int ncols,
-                                         const float* acc) {
+                                         const float* acc, float* inv) {
+  __syncthreads();
+  input_scales(a, tok0, ncols, inv);
   __syncthreads();
   const int t = threadIdx.x;
   if constexpr (EPI == EPI_SWIGLU) {
@@ -74,9 +93,79 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
       float g[8], u[8], o[8];
       ld8(acc + c * 128 + f0, g);
       ld8(acc + c * 128 + 64 + f0, u);
+      const float sc = inv[c];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = silu(g[i]) * u[i];
+      for (int i = 0; i < 8; ++i) o[i] = silu(g[i] * sc) * (u[i] * sc);
       st8_bf16(static_cast<__nv_bfloat16*>(a.out) + (size_t)(tok0 + c) * a.ldo + n_tile * 64 + f0, o);
+    }
+  } else if constexpr (EPI == EPI_ROPE_KV) {
+    const RopeKvArgs& rp = a.rope;
+    const ArRowDesc* rows = static_cast<const ArRowDesc*>(rp.rows);
+    const int f0 = (t & 7) * 8;
+    const int head = n_tile;
+    for (int c = t >> 3; c < ncols; c += kThreads / 8) {
+      const int tok = tok0 + c;
+      float lo[8], hi[8];
+      ld8(acc + c * 128 + f0, lo);
+      ld8(acc + c * 128 + 64 + f0, hi);
+      const float sc = inv[c];
+      const ArRowDesc rd = rows[tok];
+      float o0[8], o1[8];
+      if (head < rp.n_heads + rp.n_kv) {
+        const float4* cs4 = reinterpret_cast<const float4*>(rp.table + (size_t)rd.pos * 64 + f0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 w = cs4[i];  // (cos, sin) of pairs 2i, 2i+1
+          const float a0 = lo[2 * i] * sc, b0 = hi[2 * i] * sc;
+          const float a1 = lo[2 * i + 1] * sc, b1 = hi[2 * i + 1] * sc;
+          o0[2 * i] = a0 * w.x - b0 * w.y;
+          o1[2 * i] = b0 * w.x + a0 * w.y;
+          o0[2 * i + 1] = a1 * w.z - b1 * w.w;
+          o1[2 * i + 1] = b1 * w.z + a1 * w.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o0[i] = lo[i] * sc, o1[i] = hi[i] * sc;
+      }
+      __nv_bfloat16* dst;
+      if (head < rp.n_heads) {
+        dst = rp.q_out + (size_t)tok * rp.n_heads * 128 + head * 128;
+      } else {
+        const int is_v = head >= rp.n_heads + rp.n_kv;
+        const int kh = head - rp.n_heads - (is_v ? rp.n_kv : 0);
+        const int page = rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens];
+        dst = rp.kv +
+              ((((size_t)page * rp.n_layers + rp.layer) * 2 + is_v) * rp.n_kv + kh) * kPageTokens * 128 +
+              (size_t)(rd.pos % kPageTokens) * 128;
+      }
+      st8_bf16(dst + f0, o0);
+      st8_bf16(dst + 64 + f0, o1);
+    }
+  } else if constexpr (EPI == EPI_RESID_NORM) {
+    // warp-uniform trip count so the 16-lane sum-of-squares shuffle is safe
+    const int r0 = (t & 15) * 8;
+    const int n0 = n_tile * kBlockM + r0;
+    for (int cb = 0; cb < ncols; cb += kThreads / 16) {
+      const int c = cb + (t >> 4);
+      const bool live = c < ncols;
+      float ss = 0.f;
+      if (live) {
+        const int tok = tok0 + c;
+        float v[8], x[8];
+        ld8(acc + c * 128 + r0, v);
+        float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
+        ld8(r, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          x[i] += v[i];
+          ss += x[i] * x[i];
+        }
+        st8(r, x);
+        st8_bf16(a.xb + (size_t)tok * a.ldo + n0, x);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (live && (t & 15) == 0) a.ss_out[(size_t)(tok0 + c) * a.ss_ld + n_tile] = ss;
     }
   } else {
     const int r0 = (t & 15) * 8;
@@ -86,6 +175,9 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
       const int tok = tok0 + c;
       float v[8];
       ld8(acc + c * 128 + r0, v);
+      const float sc = inv[c];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] *= sc;
       if constexpr (EPI == EPI_BF16) {
         st8_bf16(static_cast<__nv_bfloat16*>(a.out) + (size_t)tok * a.ldo + n0, v);
       } else if constexpr (EPI == EPI_F32) {
@@ -117,7 +209,7 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                   GemmArgs a) {
+                   const GemmArgs a) {
   constexpr uint32_t kABytes = kBlockM * kBlockK * 2;
   constexpr uint32_t kBBytes = BN * kBlockK * 2;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
@@ -134,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  float* inv_s = reinterpret_cast<float*>(done + 2);  // [BN] input-RMS scales
 
   const int warp = warp_id(), lane = lane_id();
   const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
@@ -155,12 +248,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
 
   if (warp == 0) {
     if (elect_one()) {
       const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
       const uint64_t pol_x = policy_evict_last();   // activations: shared by all n-tiles
-      for (int i = 0; i < kb_per; ++i) {
+      // Weights never depend on the previous kernel: fill the ring with W
+      // tiles BEFORE waiting on the predecessor (PDL), then add the X tiles.
+      const int pre = kb_per < STAGES ? kb_per : STAGES;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], kABytes + kBBytes);
+        tma_load_2d(sA + i * kABytes, &tmW, &full[i], (kb0 + i) * kBlockK, n_tile * kBlockM, pol_w);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(sB + i * kBBytes, &tmX, &full[i], (kb0 + i) * kBlockK, m_tile * BN, pol_x);
+      for (int i = pre; i < kb_per; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
@@ -190,6 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   __syncwarp();
+  pdl_wait();  // epilogue reads / writes activations of the predecessor
 
   // ---- epilogue: TMEM -> smem (fp32, column-major) -> [cluster split-K
   // reduction over DSMEM in fixed rank order] -> fused op -------------------
@@ -208,11 +313,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 16; ++j) red[(c * 16 + j) * 128 + row] = v[j];
   }
   if (a.splits == 1) {
-    epi_cols<EPI>(a, n_tile, m0, cols, red);
+    epi_cols<EPI>(a, n_tile, m0, cols, red, inv_s);
   } else {
     // The split CTAs of this tile form one cluster (rank == split). Each
     // reduces a slice of token columns across all ranks, in rank order, so
-    // the sum order never depends on the batch.
+    // the sum order never depends on the batch. All S remote 16-byte loads
+    // of an element group are issued before the ordered sum.
     cluster_sync();
     const int S = a.splits;
     const int per = (cols + S - 1) / S;
@@ -220,13 +326,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c1 = min(cols, c0 + per);
     float* fin = red + BN * 128;
     const uint32_t red_s = smem_addr(red);
-    for (int c = c0; c < c1; ++c) {
-      const uint32_t off = static_cast<uint32_t>((c * 128 + row) * 4);
-      float acc = 0.f;
-      for (int z = 0; z < S; ++z) acc += dsmem_ld_f32(dsmem_map(red_s + off, z));
-      fin[(c - c0) * 128 + row] = acc;
+    const int n4 = (c1 > c0 ? c1 - c0 : 0) * 32;  // float4 groups in the slice
+    for (int q = threadIdx.x; q < n4; q += kThreads) {
+      const int c = c0 + q / 32, r4 = (q % 32) * 4;
+      const uint32_t off = static_cast<uint32_t>((c * 128 + r4) * 4);
+      float4 v[8];
+#pragma unroll
+      for (int z = 0; z < 8; ++z)
+        if (z < S) v[z] = dsmem_ld_f32x4(dsmem_map(red_s + off, z));
+      float4 acc = v[0];
+#pragma unroll
+      for (int z = 1; z < 8; ++z)
+        if (z < S) acc.x += v[z].x, acc.y += v[z].y, acc.z += v[z].z, acc.w += v[z].w;
+      *reinterpret_cast<float4*>(fin + (c - c0) * 128 + r4) = acc;
     }
-    if (c1 > c0) epi_cols<EPI>(a, n_tile, m0 + c0, c1 - c0, fin);
+    if (c1 > c0) epi_cols<EPI>(a, n_tile, m0 + c0, c1 - c0, fin, inv_s);
     cluster_sync();  // keep our partial alive until every rank has read it
   }
 
@@ -247,7 +361,8 @@ constexpr size_t epi_smem_for() {
 template <int BN>
 constexpr size_t smem_for() {
   constexpr size_t pipe = stages_for<BN>() * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
-  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256;
+  // + barriers / tmem slot (256 B) + per-column input-RMS scales (4 B x BN)
+  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256 + 4 * BN;
 }
 
 template <int BN, int EPI>
@@ -255,25 +370,10 @@ cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a
                       cudaStream_t st) {
   auto kern = gemm_tc_kernel<BN, stages_for<BN>(), EPI>;
   constexpr size_t smem = smem_for<BN>();
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(w.N_pad / kBlockM, (a.M + BN - 1) / BN, a.splits);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = a.splits;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, w.tmap, x.tmap_for(BN), a);
+  static std::atomic<uint64_t> configured{0};  // per instantiation, per device
+  if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
+  return launch_k(kern, dim3(w.N_pad / kBlockM, (a.M + BN - 1) / BN, a.splits), dim3(kThreads), smem, st,
+                  a.splits, w.tmap, x.tmap_for(BN), a);
 }
 
 template <int EPI>
@@ -314,6 +414,20 @@ cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, co
   a.ldg = e.ldg;
   a.gate_off = e.gate_off;
   a.rows_per_group = e.rows_per_group > 0 ? e.rows_per_group : 1;
+  a.ss_in = e.ss_in;
+  a.ss_ld = e.ss_ld;
+  a.ss_n = e.ss_n;
+  a.norm_d = e.norm_d;
+  a.norm_eps = e.norm_eps;
+  a.xb = e.xb;
+  a.ss_out = e.ss_out;
+  a.rope = e.rope;
+  if (epi == EPI_RESID_NORM && (e.xb == nullptr || e.ss_out == nullptr || w.N != w.N_pad))
+    return cudaErrorInvalidValue;
+  if (epi == EPI_ROPE_KV && (e.rope.rows == nullptr || e.rope.kv == nullptr || e.rope.q_out == nullptr ||
+                             w.K % 64 != 0 || w.N != (e.rope.n_heads + 2 * e.rope.n_kv) * 128))
+    return cudaErrorInvalidValue;
+  if (e.ss_in && (e.ss_n <= 0 || e.norm_d <= 0.f)) return cudaErrorInvalidValue;
   if (w.splits > 8 || (a.K / kBlockK) % w.splits != 0) return cudaErrorInvalidValue;
   switch (epi) {
     case EPI_BF16: return launch_epi<EPI_BF16>(w, x, a, st);
@@ -322,6 +436,8 @@ cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, co
     case EPI_GATED_RESID: return launch_epi<EPI_GATED_RESID>(w, x, a, st);
     case EPI_SWIGLU: return launch_epi<EPI_SWIGLU>(w, x, a, st);
     case EPI_GELU: return launch_epi<EPI_GELU>(w, x, a, st);
+    case EPI_RESID_NORM: return launch_epi<EPI_RESID_NORM>(w, x, a, st);
+    case EPI_ROPE_KV: return launch_epi<EPI_ROPE_KV>(w, x, a, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "launch.cuh"
 #include "pack_kernels.h"
 #include "ptx.cuh"
 
@@ -48,6 +49,8 @@ __device__ __forceinline__ uint32_t u16_at(const PackChunkDesc& c, const __nv_bf
 __global__ void pack_hidden_kernel(const PackChunkDesc* __restrict__ chunks,
                                    const __nv_bfloat16* __restrict__ ring, int d, int ring_rows,
                                    uint8_t* __restrict__ dst_base) {
+  pdl_wait();
+  pdl_trigger();
   const PackChunkDesc c = chunks[blockIdx.y];
   const int64_t rows = c.end - c.begin;
   const int64_t total_u16 = 5 + rows * (d + 1);
@@ -106,8 +109,7 @@ cudaError_t launch_pack_hidden(const PackChunkDesc* chunks_dev, int n_chunks, in
   const int threads = 256;
   const int bx = (int)((words + threads - 1) / threads);
   dim3 grid(bx < 1 ? 1 : bx, n_chunks);
-  pack_hidden_kernel<<<grid, threads, 0, st>>>(chunks_dev, ring, d, ring_rows, dst_base);
-  return cudaGetLastError();
+  return launch_k(pack_hidden_kernel, grid, dim3(threads), 0, st, 1, chunks_dev, ring, d, ring_rows, dst_base);
 }
 
 }  // namespace omni_dev

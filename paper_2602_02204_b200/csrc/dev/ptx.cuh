@@ -168,6 +168,23 @@ __device__ __forceinline__ float dsmem_ld_f32(uint32_t cluster_saddr) {
   return v;
 }
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Every kernel of a stage step is launched with programmatic stream
+// serialization: it may start while its predecessor is still running, and
+// must call pdl_wait() before touching anything the predecessor produces (or
+// reads). pdl_trigger() lets the successor start its own prologue early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ float4 dsmem_ld_f32x4(uint32_t cluster_saddr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(cluster_saddr)
+               : "memory");
+  return v;
+}
+
 // ---- misc -----------------------------------------------------------------
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;

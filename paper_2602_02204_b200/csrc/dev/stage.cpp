@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -57,9 +58,9 @@ DevTensor make_swiglu(omni_stage* st, const std::string& name, int64_t ff, int64
   return t;
 }
 
-GemmWeight gemm_of(const DevTensor& t, int max_splits) {
+GemmWeight gemm_of(const DevTensor& t, int max_splits, int target_ctas = 296) {
   GemmWeight g;
-  OMNI_REQUIRE(gemm_make_weight(g, t.p, (int)t.rows, (int)t.rows_pad, (int)t.cols, max_splits),
+  OMNI_REQUIRE(gemm_make_weight(g, t.p, (int)t.rows, (int)t.rows_pad, (int)t.cols, max_splits, target_ctas),
                OMNI_E_BADARG, "weight tensor map encode failed");
   return g;
 }
@@ -70,8 +71,9 @@ GemmInput input_of(const __nv_bfloat16* p, int rows_cap, int K) {
   return x;
 }
 
-void staging_reserve(Staging& s, size_t bytes) {
-  if (bytes <= s.cap) return;
+// Returns true when the buffers were (re)allocated.
+bool staging_reserve(Staging& s, size_t bytes) {
+  if (bytes <= s.cap) return false;
   if (s.in_use) OMNI_CUDA(cudaEventSynchronize(s.in_use));
   if (s.host) cudaFreeHost(s.host);
   if (s.dev) cudaFree(s.dev);
@@ -80,6 +82,12 @@ void staging_reserve(Staging& s, size_t bytes) {
   OMNI_CUDA(cudaMalloc(&s.dev, cap));
   s.cap = cap;
   if (!s.in_use) OMNI_CUDA(cudaEventCreateWithFlags(&s.in_use, cudaEventDisableTiming));
+  return true;
+}
+
+void drop_graphs(omni_stage* st) {
+  for (auto& kv : st->graphs) cudaGraphExecDestroy(kv.second.exec);
+  st->graphs.clear();
 }
 
 void require_device() {
@@ -141,7 +149,7 @@ void build_ar(omni_stage* st) {
   const int R = st->rows_cap = std::max(16, st->lim.max_batch_tokens);
   st->x = dev_alloc<float>(st, (size_t)R * d);
   st->xn = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
-  st->qkv = dev_alloc<float>(st, (size_t)R * qkv_rows);
+  st->ss = dev_alloc<float>(st, (size_t)R * (d / 128));
   st->q = dev_alloc<__nv_bfloat16>(st, (size_t)R * H * kHeadDim);
   st->attn = dev_alloc<__nv_bfloat16>(st, (size_t)R * H * kHeadDim);
   st->act = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
@@ -199,7 +207,7 @@ void build_dit(omni_stage* st) {
   st->w_out = make_weight(st, "w_out", C, round_up(C, 128), d, 5, s_d);
   st->w_mod = make_weight(st, "w_mod", (int64_t)L * 6 * d, (int64_t)L * 6 * d, d, 6, 0.5f * s_d);
   st->g_in = gemm_of(st->w_in, 1);
-  st->g_out = gemm_of(st->w_out, 1);
+  st->g_out = gemm_of(st->w_out, 4, 64);
   st->g_mod = gemm_of(st->w_mod, 1);
   st->dlayers.resize(L);
   for (int l = 0; l < L; ++l) {
@@ -210,10 +218,10 @@ void build_dit(omni_stage* st) {
     ly.wo = make_weight(st, p + "wo", d, d, d, b + 2, s_d);
     ly.w1 = make_weight(st, p + "w1", ff, ff, d, b + 3, s_d);
     ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
-    ly.gqkv = gemm_of(ly.wqkv, 1);
-    ly.go = gemm_of(ly.wo, 1);
-    ly.g1 = gemm_of(ly.w1, 1);
-    ly.g2 = gemm_of(ly.w2, 1);
+    ly.gqkv = gemm_of(ly.wqkv, 4, 64);
+    ly.go = gemm_of(ly.wo, 4, 64);
+    ly.g1 = gemm_of(ly.w1, 4, 64);
+    ly.g2 = gemm_of(ly.w2, 4, 64);
   }
   const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
   const int R = st->drows_cap = T * kDitSamples;
@@ -233,6 +241,27 @@ void build_dit(omni_stage* st) {
   st->din_o = input_of(st->dout, R, d);
   st->din_u = input_of(st->du, R, ff);
   st->din_c = input_of(st->dcvec, T, d);
+  // adaLN modulation table: mod[t][id] = W_mod . silu(tok_emb[id] + t_emb[t])
+  // for every (Euler step, conditioning id) — the per-token GEMM of the
+  // reference-shaped model depends on nothing else, so it is evaluated once
+  // here with the same kernel (batch invariance => identical rows).
+  OMNI_REQUIRE(m.vocab <= T, OMNI_E_BADARG, "DiT vocab exceeds dit_max_tokens");
+  const int ld_mod = L * 6 * d;
+  st->mod_table = dev_alloc<float>(st, (size_t)m.dit_steps * m.vocab * ld_mod);
+  {
+    std::vector<DitTokDesc> ids(m.vocab);
+    for (int i = 0; i < m.vocab; ++i) ids[i] = DitTokDesc{0, 0, i};
+    DitTokDesc* ids_dev = dev_alloc<DitTokDesc>(st, m.vocab);
+    OMNI_CUDA(cudaMemcpyAsync(ids_dev, ids.data(), ids.size() * sizeof(DitTokDesc), cudaMemcpyHostToDevice,
+                              st->stream));
+    for (int t = 0; t < m.dit_steps; ++t) {
+      OMNI_KERNEL(dit_cond(ids_dev, m.vocab, st->tok_emb.p, st->t_emb.p, t, d, st->dcvec, st->stream));
+      GemmEpilogue e;
+      e.out = st->mod_table + (size_t)t * m.vocab * ld_mod;
+      e.ldo = ld_mod;
+      OMNI_KERNEL(gemm_run(st->g_mod, st->din_c, m.vocab, EPI_F32, e, st->stream));
+    }
+  }
   OMNI_CUDA(cudaMallocHost(&st->h_samples, (size_t)R * sizeof(int32_t)));
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
 }
@@ -241,6 +270,7 @@ void destroy_stage(omni_stage* st) {
   if (!st) return;
   cudaSetDevice(st->dev);
   if (st->stream) cudaStreamSynchronize(st->stream);
+  drop_graphs(st);
   for (void* p : st->allocs) cudaFree(p);
   for (Staging* s : {&st->desc, &st->pack}) {
     if (s->host) cudaFreeHost(s->host);
@@ -282,6 +312,55 @@ void ensure_pages(omni_stage* st, SeqSlot& s, int upto) {
 
 size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
+// OMNI_GRAPHS=0 launches every step eagerly (A/B measurements).
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("OMNI_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Runs the kernel sequence `body` on the stage stream through a CUDA graph
+// cached under `key` (the launch geometry of the step: every pointer the
+// kernels see is fixed per stage, every per-step value lives in the device
+// descriptor blob copied before the launch). The first occurrence of a key
+// is captured (PDL launch attributes become programmatic graph edges) and
+// instantiated; later steps replay it with one cudaGraphLaunch.
+template <typename F>
+void run_graph(omni_stage* st, uint64_t key, F&& body) {
+  cudaStream_t s = st->stream;
+  if (!graphs_enabled()) {
+    body();
+    return;
+  }
+  auto it = st->graphs.find(key);
+  if (it == st->graphs.end()) {
+    if (st->graphs.size() >= 4096) drop_graphs(st);
+    const uint64_t l0 = counters().launches;
+    OMNI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+    cudaGraph_t g = nullptr;
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      counters().launches = l0;
+      throw;
+    }
+    OMNI_CUDA(cudaStreamEndCapture(s, &g));
+    StepGraph sg;
+    sg.nodes = (int)(counters().launches - l0);
+    counters().launches = l0;  // counted per replay below
+    const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
+    cudaGraphDestroy(g);
+    OMNI_CUDA(e);
+    it = st->graphs.emplace(key, sg).first;
+  }
+  OMNI_CUDA(cudaGraphLaunch(it->second.exec, s));
+  counters().launches += it->second.nodes;
+}
+
 void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* margin_out) {
   ensure_idle(st);
   const int ne = b->n_entries;
@@ -298,14 +377,17 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
                "batch of " + std::to_string(n_rows) + " tokens exceeds max_batch_tokens");
   if (talker) OMNI_REQUIRE(b->cond_row != nullptr, OMNI_E_BADARG, "talker step needs cond_row");
 
-  // descriptor blob: entries | rows | page table | decode entry list
-  const size_t off_rows = align16((size_t)ne * sizeof(ArEntryDesc));
-  const size_t off_pt = off_rows + align16((size_t)n_rows * sizeof(ArRowDesc));
-  const size_t off_dec = off_pt + align16((size_t)ne * st->max_pages * sizeof(int32_t));
-  const size_t off_blk = off_dec + align16((size_t)ne * sizeof(int32_t));
-  const size_t max_blocks = (size_t)n_rows + ne;  // >= sum ceil(span / kAttnQTok)
-  const size_t total = off_blk + align16(max_blocks * sizeof(AttnBlockDesc));
-  staging_reserve(st->desc, total);
+  OMNI_REQUIRE(ne <= st->lim.max_resident, OMNI_E_BADARG, "more entries than max_resident_requests");
+  // descriptor blob at FIXED offsets (capacity-sized regions, so the device
+  // pointers baked into a captured step graph never change):
+  //   entries | decode entry list | attention blocks | rows | page table
+  const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
+  const size_t off_dec = align16(cap_e * sizeof(ArEntryDesc));
+  const size_t off_blk = off_dec + align16(cap_e * sizeof(int32_t));
+  const size_t off_rows = off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
+  const size_t off_pt = off_rows + align16(cap_r * sizeof(ArRowDesc));
+  const size_t total = off_pt + align16((size_t)ne * st->max_pages * sizeof(int32_t));
+  if (staging_reserve(st->desc, off_pt + cap_e * st->max_pages * sizeof(int32_t))) drop_graphs(st);
   auto* ents = reinterpret_cast<ArEntryDesc*>(st->desc.host);
   auto* rows = reinterpret_cast<ArRowDesc*>(st->desc.host + off_rows);
   auto* pt = reinterpret_cast<int32_t*>(st->desc.host + off_pt);
@@ -374,44 +456,69 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   const auto& m = st->m;
   const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   if (n_rows > 0) {
-    if (talker && n_prefill_rows > 0) {
-      OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
-      GemmEpilogue e;
-      e.out = st->hproj;
-      e.ldo = d;
-      OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
-    }
-    OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
-                           st->cond_table, st->cond_rows, d, st->start_id, st->x, s));
-    for (int l = 0; l < L; ++l) {
-      const auto& ly = st->layers[l];
-      OMNI_KERNEL(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
-      GemmEpilogue e;
-      e.out = st->qkv;
-      e.ldo = (H + 2 * KVH) * kHeadDim;
-      OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_F32, e, s));
-      OMNI_KERNEL(launch_rope_kv(sd, n_rows, st->qkv, H, KVH, st->rope, l, L, st->q, st->kv, s));
-      OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, s));
-      e.out = st->x;
-      e.ldo = d;
-      OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID, e, s));
-      OMNI_KERNEL(launch_rmsnorm(st->x, n_rows, d, kNormEps, st->xn, s));
-      e.out = st->act;
-      e.ldo = m.d_ff;
-      OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
-      e.out = st->x;
-      e.ldo = d;
-      OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID, e, s));
-    }
+    const uint64_t key = ((uint64_t)n_rows << 40) | ((uint64_t)n_blocks << 20) | ((uint64_t)n_dec << 1) |
+                         (talker && n_prefill_rows > 0 ? 1u : 0u);
+    run_graph(st, key, [&] {
+      if (talker && n_prefill_rows > 0) {
+        OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
+        GemmEpilogue e;
+        e.out = st->hproj;
+        e.ldo = d;
+        OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
+      }
+      // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
+      // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
+      const int ss_ld = d / 128;
+      OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
+                             st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld, s));
+      GemmEpilogue norm_in;  // fused RMSNorm of the GEMM input
+      norm_in.ss_in = st->ss;
+      norm_in.ss_ld = ss_ld;
+      norm_in.ss_n = ss_ld;
+      norm_in.norm_d = (float)d;
+      norm_in.norm_eps = kNormEps;
+      for (int l = 0; l < L; ++l) {
+        const auto& ly = st->layers[l];
+        GemmEpilogue e = norm_in;  // QKV: norm scale -> RoPE -> q rows / paged KV
+        e.out = st->q;
+        e.ldo = H * kHeadDim;
+        e.rope.rows = sd.rows;
+        e.rope.page_table = sd.page_table;
+        e.rope.max_pages = sd.max_pages;
+        e.rope.table = st->rope;
+        e.rope.q_out = st->q;
+        e.rope.kv = st->kv;
+        e.rope.n_heads = H;
+        e.rope.n_kv = KVH;
+        e.rope.layer = l;
+        e.rope.n_layers = L;
+        OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
+        OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, s));
+        GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
+        r.out = st->x;
+        r.ldo = d;
+        r.xb = st->xn;
+        r.ss_out = st->ss;
+        r.ss_ld = ss_ld;
+        OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, r, s));
+        e = norm_in;
+        e.out = st->act;
+        e.ldo = m.d_ff;
+        OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
+        OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, r, s));
+      }
+      if (n_dec > 0) {
+        OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
+                                      talker ? nullptr : st->ring, st->ring_rows, s));
+        GemmEpilogue e;
+        e.out = st->logits;
+        e.ldo = st->vocab_pad;
+        OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
+        OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
+                                st->d_tok, st->d_margin, s));
+      }
+    });
     if (n_dec > 0) {
-      OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
-                                    talker ? nullptr : st->ring, st->ring_rows, s));
-      GemmEpilogue e;
-      e.out = st->logits;
-      e.ldo = st->vocab_pad;
-      OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
-      OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
-                              st->d_tok, st->d_margin, s));
       OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       counters().d2h_bytes += n_dec * (sizeof(int32_t) + sizeof(float));
       OMNI_CUDA(cudaMemcpyAsync(st->h_margin, st->d_margin, n_dec * sizeof(float),
@@ -438,11 +545,9 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
   cudaStream_t s = st->stream;
   OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, s));
   for (int t = 0; t < T; ++t) {
-    OMNI_KERNEL(dit_cond(toks_dev, n_tok, st->tok_emb.p, st->t_emb.p, t, d, st->dcvec, s));
+    OMNI_KERNEL(dit_mod_gather(toks_dev, n_tok, st->mod_table + (size_t)t * m.vocab * ld_mod, ld_mod,
+                               st->dmod, s));
     GemmEpilogue e;
-    e.out = st->dmod;
-    e.ldo = ld_mod;
-    OMNI_KERNEL(gemm_run(st->g_mod, st->din_c, n_tok, EPI_F32, e, s));
     OMNI_KERNEL(dit_to_bf16(st->dx, (int64_t)rows * C, st->dxin, s));
     e.out = st->dh;
     e.ldo = d;
@@ -491,7 +596,8 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
     n_tok += b->n_tokens[j];
   }
   const size_t bytes = align16((size_t)n_tok * sizeof(DitTokDesc));
-  staging_reserve(st->desc, bytes);
+  if (staging_reserve(st->desc, std::max(bytes, align16((size_t)st->tok_cap * sizeof(DitTokDesc)))))
+    drop_graphs(st);
   auto* toks = reinterpret_cast<DitTokDesc*>(st->desc.host);
   int64_t k = 0;
   for (int j = 0; j < b->n_jobs; ++j)
@@ -511,7 +617,7 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
     const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
     for (int64_t t0 = 0; t0 < n_tok; t0 += st->tok_cap) {
       const int nt = (int)std::min<int64_t>(st->tok_cap, n_tok - t0);
-      dit_chunk(st, toks_dev + t0, nt, st->dsamples);
+      run_graph(st, (uint64_t)nt << 20 | (uint64_t)t0, [&] { dit_chunk(st, toks_dev + t0, nt, st->dsamples); });
       const int64_t nsamp = (int64_t)nt * kDitSamples;
       OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));

@@ -36,6 +36,12 @@ struct SeqSlot {
   std::vector<int> pages;
 };
 
+// An instantiated CUDA graph of one step's kernel sequence.
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  int nodes = 0;  // kernels per replay (launch accounting)
+};
+
 // Pinned host staging + device mirror for per-step descriptors.
 struct Staging {
   uint8_t* host = nullptr;
@@ -65,7 +71,7 @@ struct omni_stage {
   int rows_cap = 0, max_pages = 0, ring_rows = 64, cond_rows = 64;
   float* x = nullptr;
   __nv_bfloat16* xn = nullptr;
-  float* qkv = nullptr;
+  float* ss = nullptr;  // [rows][d/128] per-tile sums of squares (fused RMSNorm)
   __nv_bfloat16* q = nullptr;
   __nv_bfloat16* attn = nullptr;
   __nv_bfloat16* act = nullptr;
@@ -89,6 +95,7 @@ struct omni_stage {
   std::vector<omni_dev::DitLayer> dlayers;
   int tok_cap = 0, drows_cap = 0;
   float *dx = nullptr, *dh = nullptr, *dv = nullptr, *dmod = nullptr;
+  float* mod_table = nullptr;  // [T][vocab][L*6*d] adaLN modulation rows
   __nv_bfloat16 *dxin = nullptr, *da = nullptr, *dqkv = nullptr, *dout = nullptr, *du = nullptr,
                 *dcvec = nullptr;
   int32_t* dsamples = nullptr;
@@ -108,4 +115,5 @@ struct omni_stage {
   int32_t* user_samples = nullptr;
   int64_t pending_samples = 0;
   float last_step_us = 0.f;
+  std::unordered_map<uint64_t, omni_dev::StepGraph> graphs;  // step graphs by launch geometry
 };

@@ -27,6 +27,9 @@ def ar_probe(kind: int, batches, prompt: int = 64, steps: int = 12):
     m = D.model_default(kind)
     st = D.Stage(m, D.StageLimits(256, 64, 512, 0, 512), seed=7)
     wbytes = THINKER_BYTES if kind == D.THINKER else TALKER_BYTES
+    cond = D.mem_alloc(2 * m.cond_dim * 256) if kind == D.TALKER else 0
+    if cond:
+        D.mem_set(cond, 0, 2 * m.cond_dim * 256)
     out = []
     for B in batches:
         ids = list(range(1000 * (B + 1), 1000 * (B + 1) + B))
@@ -34,7 +37,7 @@ def ar_probe(kind: int, batches, prompt: int = 64, steps: int = 12):
         for i in range(0, B, 4):
             grp = ids[i:i + 4]
             toks = [(7 * j + 3) % 250 + 1 for j in range(prompt)] * len(grp)
-            cs = [0] * len(toks) if kind == D.TALKER else None
+            cs = [cond + 2 * m.cond_dim * (j % 256) for j in range(len(toks))] if kind == D.TALKER else None
             cr = [j for _ in grp for j in range(prompt)] if kind == D.TALKER else None
             st.ar_step(grp, [D.PREFILL] * len(grp), [prompt] * len(grp), [0] * len(grp), [-1] * len(grp),
                        toks, cs, cr)
