@@ -104,22 +104,34 @@ def dist_setup(n_gpus: int):
     return 1, 0, local, None
 
 
-def max_over_ranks(x: float, dist) -> float:
+def _reduce(x: float, dist, op: str) -> float:
+    """All-reduce one scalar over the ranks (nccl on the GPU box, gloo on CPU)."""
     if dist is None:
         return x
     import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def max_over_ranks(x: float, dist) -> float:
+    return _reduce(x, dist, "max")
 
 
 def sum_over_ranks(x: float, dist) -> float:
-    if dist is None:
-        return x
-    import torch
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t)
-    return float(t.item())
+    return _reduce(x, dist, "sum")
+
+
+def aggregate(completed: float, dev_ms: float, wall_s: float, dist) -> dict:
+    """Whole-job numbers of a weak-scaling run: every rank ran its own full
+    workload replica; value = all requests completed / the SLOWEST rank's
+    device time (max over ranks), e2e likewise on the host clock."""
+    t_max_ms = max_over_ranks(dev_ms, dist)
+    wall_max = max_over_ranks(wall_s, dist)
+    done = sum_over_ranks(completed, dist)
+    return {"completed": done, "t_max_ms": t_max_ms, "wall_max_s": wall_max,
+            "value": done / (t_max_ms / 1e3), "e2e": done / wall_max}
 
 
 def gemm_roofline(pk: dict) -> dict:
@@ -149,10 +161,16 @@ def gemm_roofline(pk: dict) -> dict:
         D.mem_free(p)
     t_ms = statistics.median(times)
     algo = N * K * 2 + M * K * 2 + M * (N // 2) * 2
+    # DRAM traffic per launch of this kernel from the committed `ncu --set full`
+    # capture (tools/ncu_gemm.py 16 -> profiles/ncu_traffic.json)
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("gemm_gateup_m16", {}).get("dram_bytes_per_launch")
     gbs = algo / (t_ms * 1e-3) / 1e9
     return {"kernel": "gemm_tc_kernel<BN=16,EPI_SWIGLU> gate-up N=16384 K=2048 M=16", "bound": "hbm",
             "achieved": round(gbs, 1), "peak": pk["hbm"], "unit": "GB/s", "frac": round(gbs / pk["hbm"], 4),
-            "traffic": None, "algorithmic_bytes": algo, "us_per_launch": round(t_ms * 1e3, 2),
+            "traffic": traffic, "algorithmic_bytes": algo, "us_per_launch": round(t_ms * 1e3, 2),
             "peak_source": pk["source"]}
 
 
@@ -254,13 +272,10 @@ def main() -> None:
     l1, h1, d1 = C.c_uint64(), C.c_uint64(), C.c_uint64()
     lib.omni_dev_counters(C.byref(l1), C.byref(h1), C.byref(d1))
     dev_ms = e0.elapsed_time(e1)
-    t_max_ms = max_over_ranks(dev_ms, dist)
-    wall_max = max_over_ranks(wall, dist)
-    done = sum(r["completed"] for r in results)
-    done_all = sum_over_ranks(done, dist)
+    agg = aggregate(sum(r["completed"] for r in results), dev_ms, wall, dist)
+    t_max_ms, wall_max, done_all, value = agg["t_max_ms"], agg["wall_max_s"], agg["completed"], agg["value"]
     # serving metric as the reference defines it: completed / makespan (first admit -> last done)
     rps_makespan = statistics.mean(r["requests_per_s"] for r in results)
-    value = done_all / (t_max_ms / 1e3)
     mean_jct = statistics.mean(r["mean_jct_us"] for r in results)
     p99_jct = statistics.mean(r["p99_jct_us"] for r in results)
     if rank != 0:

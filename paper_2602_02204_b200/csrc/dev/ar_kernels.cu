@@ -35,7 +35,9 @@ __global__ void embed_kernel(const ArStepDev s, const __nv_bfloat16* __restrict_
                              const __nv_bfloat16* __restrict__ emb2, const float* __restrict__ hproj,
                              float* __restrict__ cond_table, int cond_rows, int d, int start_id,
                              float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
-                             float* __restrict__ ss_out, int ss_ld) {
+                             float* __restrict__ ss_out, int ss_ld, const void* pf_ptr,
+                             uint64_t pf_bytes) {
+  prefetch_l2_share(pf_ptr, pf_bytes, blockIdx.x, gridDim.x, threadIdx.x, blockDim.x);
   pdl_wait();
   pdl_trigger();
   const int r = blockIdx.x;
@@ -140,12 +142,16 @@ struct AttnSmem {
 __global__ void __launch_bounds__(kAttnWarps * 32)
     attention_kernel(const ArStepDev s, const __nv_bfloat16* __restrict__ q, int n_heads, int n_kv,
                      int layer, int n_layers, const __nv_bfloat16* __restrict__ kv,
-                     __nv_bfloat16* __restrict__ out, float scale) {
+                     __nv_bfloat16* __restrict__ out, float scale, const void* pf_ptr,
+                     uint64_t pf_bytes) {
   constexpr int HD = kHeadDim;
   constexpr uint32_t PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB K or V slice of one page
   extern __shared__ __align__(128) uint8_t attn_smem_raw[];
   AttnSmem& sm = *reinterpret_cast<AttnSmem*>(attn_smem_raw);
 
+  // static weights of a later GEMM (OMNI_PF_MB, default off)
+  prefetch_l2_share(pf_ptr, pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y,
+                    threadIdx.x, blockDim.x);
   pdl_wait();
   pdl_trigger();
   const AttnBlockDesc blk = s.attn_blocks[blockIdx.x];
@@ -348,10 +354,10 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int ld, int lo, 
 cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,
                          const __nv_bfloat16* emb2, const float* hproj, float* cond_table,
                          int cond_rows, int d, int start_id, float* x, __nv_bfloat16* xb, float* ss,
-                         int ss_ld, cudaStream_t st) {
+                         int ss_ld, const void* pf_ptr, uint64_t pf_bytes, cudaStream_t st) {
   if (d % 128 != 0) return cudaErrorInvalidValue;
   return launch_k(embed_kernel, dim3(n_rows), dim3(256), 0, st, 1, s, emb, emb2, hproj, cond_table,
-                  cond_rows, d, start_id, x, xb, ss, ss_ld);
+                  cond_rows, d, start_id, x, xb, ss, ss_ld, pf_ptr, pf_bytes & ~uint64_t(15));
 }
 cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloat16* out,
                                cudaStream_t st) {
@@ -359,13 +365,15 @@ cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloa
 }
 cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat16* q,
                              int n_heads, int n_kv, int layer, int n_layers,
-                             const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st) {
+                             const __nv_bfloat16* kv, __nv_bfloat16* out, const void* pf_ptr,
+                             uint64_t pf_bytes, cudaStream_t st) {
   if (n_heads / n_kv > 8) return cudaErrorInvalidValue;
   static std::atomic<uint64_t> configured{0};
   const size_t smem = sizeof(AttnSmem);
   if (cudaError_t e = smem_attr_once(attention_kernel, smem, configured); e != cudaSuccess) return e;
   return launch_k(attention_kernel, dim3(n_blocks, n_kv), dim3(kAttnWarps * 32), smem, st, 1, s, q, n_heads,
-                  n_kv, layer, n_layers, kv, out, 1.0f / sqrtf((float)kHeadDim));
+                  n_kv, layer, n_layers, kv, out, 1.0f / sqrtf((float)kHeadDim), pf_ptr,
+                  pf_bytes & ~uint64_t(15));
 }
 cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,

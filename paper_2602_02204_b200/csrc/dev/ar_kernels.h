@@ -50,12 +50,13 @@ struct ArStepDev {
 cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,
                          const __nv_bfloat16* emb2, const float* hproj, float* cond_table,
                          int cond_rows, int d, int start_id, float* x, __nv_bfloat16* xb, float* ss,
-                         int ss_ld, cudaStream_t st);
+                         int ss_ld, const void* pf_ptr, uint64_t pf_bytes, cudaStream_t st);
 cudaError_t launch_gather_cond(const ArStepDev& s, int n_rows, int d, __nv_bfloat16* out,
                                cudaStream_t st);
 cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat16* q,
                              int n_heads, int n_kv, int layer, int n_layers,
-                             const __nv_bfloat16* kv, __nv_bfloat16* out, cudaStream_t st);
+                             const __nv_bfloat16* kv, __nv_bfloat16* out, const void* pf_ptr,
+                             uint64_t pf_bytes, cudaStream_t st);
 cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
                                 cudaStream_t st);

@@ -15,7 +15,7 @@ namespace omni_dev {
 
 // x0[row, ch] ~ N(0,1) keyed by (request, global token position, sample, ch).
 __global__ void dit_noise_kernel(const DitTokDesc* __restrict__ toks, int S, int C, uint64_t seed,
-                                 float* __restrict__ x, int rows) {
+                                 float* __restrict__ x, __nv_bfloat16* __restrict__ xb, int rows) {
   pdl_wait();
   pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -23,8 +23,10 @@ __global__ void dit_noise_kernel(const DitTokDesc* __restrict__ toks, int S, int
   const int r = (int)(i / C), ch = (int)(i % C);
   const DitTokDesc t = toks[r / S];
   const int s = r % S;
-  x[i] = static_cast<float>(irwin4(noise_hash(seed, t.rid, (uint32_t)t.pos, (uint32_t)s, (uint32_t)ch))) *
-         kNoiseMult;
+  const float v =
+      static_cast<float>(irwin4(noise_hash(seed, t.rid, (uint32_t)t.pos, (uint32_t)s, (uint32_t)ch))) * kNoiseMult;
+  x[i] = v;
+  xb[i] = f2bf(v);  // the next input projection's bf16 operand
 }
 
 // cvec[p] = bf16(silu(tok_emb[id_p] + t_emb[step]))
@@ -81,30 +83,53 @@ __device__ __forceinline__ float block_sum2(float v, float* red) {
   return t;
 }
 
-// a = bf16(LN(h) * (1 + scale) + shift); mod == nullptr -> plain LN.
+// a = bf16(LN(h) * (1 + scale) + shift); mod_base == nullptr -> plain LN.
 // LN without affine params, eps 1e-6, two-pass (mean, then centred variance).
-__global__ void dit_ln_mod_kernel(const float* __restrict__ h, int d, const float* __restrict__ mod,
-                                  int ld_mod, int shift_off, int scale_off, int S,
-                                  __nv_bfloat16* __restrict__ a) {
+// One warp per row (the row stays in registers: d/32 floats per lane, float4
+// loads), 8 rows per CTA. The modulation row of token p is the adaLN table
+// row of its conditioning id: mod_base + id_p * ld_mod.
+template <int PER>  // d / 128 float4 groups per lane
+__global__ void __launch_bounds__(256)
+    dit_ln_mod_kernel(const float* __restrict__ h, int rows, const float* __restrict__ mod_base,
+                      const DitTokDesc* __restrict__ toks, int ld_mod, int shift_off, int scale_off, int S,
+                      __nv_bfloat16* __restrict__ a) {
   pdl_wait();
   pdl_trigger();
-  __shared__ float red[32];
-  const int r = blockIdx.x;
-  const float* hr = h + (size_t)r * d;
-  float s = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) s += hr[i];
-  const float mean = block_sum2(s, red) / d;
-  float v = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float t = hr[i] - mean;
-    v += t * t;
+  constexpr int d = PER * 128;
+  const int r = blockIdx.x * 8 + warp_id(), lane = lane_id();
+  if (r >= rows) return;
+  const float4* hr = reinterpret_cast<const float4*>(h + (size_t)r * d);
+  float4 x[PER];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    x[k] = hr[lane + 32 * k];
+    sum += (x[k].x + x[k].y) + (x[k].z + x[k].w);
   }
-  const float inv = rsqrtf(block_sum2(v, red) / d + 1e-6f);
-  const float* mr = mod ? mod + (size_t)(r / S) * ld_mod : nullptr;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float y = (hr[i] - mean) * inv;
-    if (mr) y = y * (1.f + mr[scale_off + i]) + mr[shift_off + i];
-    a[(size_t)r * d + i] = f2bf(y);
+  const float mean = warp_sum(sum) / d;
+  float var = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const float a0 = x[k].x - mean, a1 = x[k].y - mean, a2 = x[k].z - mean, a3 = x[k].w - mean;
+    var += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+  }
+  const float inv = rsqrtf(warp_sum(var) / d + 1e-6f);
+  const float* mr = mod_base ? mod_base + (size_t)toks[r / S].id * ld_mod : nullptr;
+  uint2* out = reinterpret_cast<uint2*>(a + (size_t)r * d);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = 4 * (lane + 32 * k);
+    float y[4] = {(x[k].x - mean) * inv, (x[k].y - mean) * inv, (x[k].z - mean) * inv, (x[k].w - mean) * inv};
+    if (mr) {
+      const float4 sc = *reinterpret_cast<const float4*>(mr + scale_off + i);
+      const float4 sh = *reinterpret_cast<const float4*>(mr + shift_off + i);
+      y[0] = y[0] * (1.f + sc.x) + sh.x;
+      y[1] = y[1] * (1.f + sc.y) + sh.y;
+      y[2] = y[2] * (1.f + sc.z) + sh.z;
+      y[3] = y[3] * (1.f + sc.w) + sh.w;
+    }
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(y[0], y[1]), hi = __floats2bfloat162_rn(y[2], y[3]);
+    out[lane + 32 * k] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
   }
 }
 
@@ -159,14 +184,16 @@ __global__ void __launch_bounds__(128)
 }
 
 // x += dt * v; on the final step also quantise channel 0 to an int32 sample.
-__global__ void dit_euler_kernel(float* __restrict__ x, const float* __restrict__ v, int C, int rows,
-                                 float dt, int last, int32_t* __restrict__ samples) {
+__global__ void dit_euler_kernel(float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                                 const float* __restrict__ v, int C, int rows, float dt, int last,
+                                 int32_t* __restrict__ samples) {
   pdl_wait();
   pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)rows * C) return;
   const float nx = x[i] + dt * v[i];
   x[i] = nx;
+  xb[i] = f2bf(nx);  // the next step's input-projection operand (fused to_bf16)
   if (last && (i % C) == 0) {
     float q = rintf(kSampleScale * nx);
     q = fminf(fmaxf(q, -64.f), 63.f);
@@ -176,10 +203,10 @@ __global__ void dit_euler_kernel(float* __restrict__ x, const float* __restrict_
 
 // ---------------------------------------------------------------------------
 cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t seed, float* x,
-                      cudaStream_t st) {
+                      __nv_bfloat16* xb, cudaStream_t st) {
   const int rows = n_tok * S;
   const int64_t n = (int64_t)rows * C;
-  return launch_k(dit_noise_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, toks, S, C, seed, x, rows);
+  return launch_k(dit_noise_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, toks, S, C, seed, x, xb, rows);
 }
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st) {
@@ -197,19 +224,26 @@ cudaError_t dit_to_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_
 cudaError_t dit_add_pos(float* h, const __nv_bfloat16* pos_emb, int S, int d, int rows, cudaStream_t st) {
   return launch_k(dit_add_pos_kernel, dim3(rows), dim3(256), 0, st, 1, h, pos_emb, S, d, rows);
 }
-cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod, int ld_mod, int shift_off,
-                       int scale_off, int S, __nv_bfloat16* a, cudaStream_t st) {
-  return launch_k(dit_ln_mod_kernel, dim3(rows), dim3(256), 0, st, 1, h, d, mod, ld_mod, shift_off, scale_off, S, a);
+cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod_base, const DitTokDesc* toks,
+                       int ld_mod, int shift_off, int scale_off, int S, __nv_bfloat16* a, cudaStream_t st) {
+  const dim3 grid((rows + 7) / 8);
+  switch (d) {
+    case 256: return launch_k(dit_ln_mod_kernel<2>, grid, dim3(256), 0, st, 1, h, rows, mod_base, toks, ld_mod, shift_off, scale_off, S, a);
+    case 512: return launch_k(dit_ln_mod_kernel<4>, grid, dim3(256), 0, st, 1, h, rows, mod_base, toks, ld_mod, shift_off, scale_off, S, a);
+    case 1024: return launch_k(dit_ln_mod_kernel<8>, grid, dim3(256), 0, st, 1, h, rows, mod_base, toks, ld_mod, shift_off, scale_off, S, a);
+    case 2048: return launch_k(dit_ln_mod_kernel<16>, grid, dim3(256), 0, st, 1, h, rows, mod_base, toks, ld_mod, shift_off, scale_off, S, a);
+  }
+  return cudaErrorInvalidValue;
 }
 cudaError_t dit_attn(const __nv_bfloat16* qkv, int n_tok, int d, int n_heads, __nv_bfloat16* out,
                      cudaStream_t st) {
   dim3 grid(n_tok, n_heads);
   return launch_k(dit_attn_kernel, dim3(grid), dim3(128), 0, st, 1, qkv, d, n_heads, out);
 }
-cudaError_t dit_euler(float* x, const float* v, int C, int rows, float dt, int last, int32_t* samples,
-                      cudaStream_t st) {
+cudaError_t dit_euler(float* x, __nv_bfloat16* xb, const float* v, int C, int rows, float dt, int last,
+                      int32_t* samples, cudaStream_t st) {
   const int64_t n = (int64_t)rows * C;
-  return launch_k(dit_euler_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, x, v, C, rows, dt, last, samples);
+  return launch_k(dit_euler_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, x, xb, v, C, rows, dt, last, samples);
 }
 
 }  // namespace omni_dev

@@ -40,6 +40,7 @@ struct GemmWeight {
   const __nv_bfloat16* ptr = nullptr;
   int N = 0, N_pad = 0, K = 0;
   int splits = 1;
+  bool fill_sms = false;  // compute-bound (DiT): pick the token tile to fill 148 SMs
   CUtensorMap tmap;
 };
 
@@ -59,6 +60,10 @@ struct GemmEpilogue {
   int ldo = 0;
   const float* gate = nullptr;
   int ldg = 0, gate_off = 0, rows_per_group = 1;
+  // EPI_GATED_RESID: gate row of group g = gate_index ? gate_index[g * gate_index_stride] : g
+  // (DiT: the adaLN table row of the token's conditioning id)
+  const int32_t* gate_index = nullptr;
+  int gate_index_stride = 1;
   // Fused RMSNorm of the GEMM input X (un-normalised bf16 rows): every output
   // column (token) is scaled by rsqrt(sum_{j<ss_n} ss_in[tok*ss_ld+j] / norm_d + eps),
   // the per-128-feature partial sums of squares written by the producer
@@ -70,6 +75,12 @@ struct GemmEpilogue {
   __nv_bfloat16* xb = nullptr;
   float* ss_out = nullptr;
   RopeKvArgs rope;
+  // L2 prefetch of a later kernel's weights (see ptx.cuh prefetch_l2_share)
+  const void* pf_ptr = nullptr;
+  uint64_t pf_bytes = 0;
+  // EPI_F32 only: out[tok, n] = acc + row_bias[tok % bias_period, n] (bf16 rows of width N)
+  const __nv_bfloat16* row_bias = nullptr;
+  int bias_period = 1;
 };
 
 // Kernel-side argument block.
@@ -79,21 +90,28 @@ struct GemmArgs {
   int ldo;
   const float* gate;
   int ldg, gate_off, rows_per_group;
+  const int32_t* gate_index;
+  int gate_index_stride;
   const float* ss_in;
   int ss_ld, ss_n;
   float norm_d, norm_eps;
   __nv_bfloat16* xb;
   float* ss_out;
   RopeKvArgs rope;
+  const void* pf_ptr;
+  uint64_t pf_bytes;
+  const __nv_bfloat16* row_bias;
+  int bias_period;
 };
 
 int gemm_block_n(int M);
-int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas = 296);
-// max_splits / target_ctas: 8 / 296 for decode-path (weight-streaming)
-// matrices, 4 / 64 for the compute-bound DiT matrices (which run 2-3 token
-// tiles). The choice is frozen into the weight (batch invariance).
+int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas = 192);
+// max_splits / target_ctas: 8 / 192 for decode-path (weight-streaming)
+// matrices (measured in-chain optimum: qkv 24x8, wo 16x8, down 16x8,
+// gate-up 128x1 CTAs), 1 for the compute-bound DiT matrices. The choice is
+// frozen into the weight (batch invariance).
 bool gemm_make_weight(GemmWeight& w, const __nv_bfloat16* ptr, int N, int N_pad, int K,
-                      int max_splits, int target_ctas = 296);
+                      int max_splits, int target_ctas = 192);
 bool gemm_make_input(GemmInput& x, const __nv_bfloat16* ptr, int rows_cap, int K);
 cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi,
                      const GemmEpilogue& e, cudaStream_t st);

@@ -40,9 +40,9 @@ bool encode_2d(CUtensorMap& m, const void* ptr, uint64_t rows, uint64_t K, uint3
 }  // namespace
 
 int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas) {
-  // Fill `target_ctas` (decode weights: two CTAs per SM of 148 SMs, one
-  // m-tile; DiT weights: ~64 tiles x the typical 2-3 m-tiles) with at least
-  // two 64-wide K blocks per split; one cluster (<= 8 CTAs) per output tile.
+  // Fill up to `target_ctas` CTAs (decode weights: 192 — the in-chain optimum
+  // measured by tools/gemm_sweep.py) with at least two 64-wide K blocks per
+  // split; one cluster (<= 8 CTAs) per output tile.
   // Depends on the weight shape only — never on the batch.
   const int tiles = N_pad / 128;
   const int kb = K / 64;

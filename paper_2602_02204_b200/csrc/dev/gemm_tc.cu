@@ -62,8 +62,9 @@ __device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float (&v)[8]) 
 
 // Per-token input-RMS scale of the fused RMSNorm (GemmEpilogue::ss_in):
 // inv[c] = rsqrt(sum_j ss_in[tok0 + c][j] / d + eps), j in fixed order.
-__device__ __forceinline__ void input_scales(const GemmArgs& a, int tok0, int ncols, float* inv) {
-  for (int c = threadIdx.x; c < ncols; c += kThreads) {
+__device__ __forceinline__ void input_scales(const GemmArgs& a, int tok0, int ncols, float* inv,
+                                             int tid, int nthreads) {
+  for (int c = tid; c < ncols; c += nthreads) {
     float s = 0.f;
     if (a.ss_in) {
       const float* p = a.ss_in + (size_t)(tok0 + c) * a.ss_ld;
@@ -82,9 +83,7 @@ __device__ __forceinline__ void input_scales(const GemmArgs& a, int tok0, int nc
 // with up row f + 64 of the same tile, ROPE_KV rotates feature f with f + 64.
 template <int EPI>
 __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0, int ncols,
-                                         const float* acc, float* inv) {
-  __syncthreads();
-  input_scales(a, tok0, ncols, inv);
+                                         const float* acc, const float* inv) {
   __syncthreads();
   const int t = threadIdx.x;
   if constexpr (EPI == EPI_SWIGLU) {
@@ -181,6 +180,15 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
       if constexpr (EPI == EPI_BF16) {
         st8_bf16(static_cast<__nv_bfloat16*>(a.out) + (size_t)tok * a.ldo + n0, v);
       } else if constexpr (EPI == EPI_F32) {
+        if (a.row_bias) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(a.row_bias + (size_t)(tok % a.bias_period) * a.N + n0);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(b2[i]);
+            v[2 * i] += f.x, v[2 * i + 1] += f.y;
+          }
+        }
         st8(static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0, v);
       } else if constexpr (EPI == EPI_RESID) {
         float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
@@ -191,7 +199,9 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
         st8(r, x);
       } else if constexpr (EPI == EPI_GATED_RESID) {
         float g[8], x[8];
-        ld8(a.gate + (size_t)(tok / a.rows_per_group) * a.ldg + a.gate_off + n0, g);
+        const int grp = tok / a.rows_per_group;
+        const int grow = a.gate_index ? a.gate_index[(size_t)grp * a.gate_index_stride] : grp;
+        ld8(a.gate + (size_t)grow * a.ldg + a.gate_off + n0, g);
         float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
         ld8(r, x);
 #pragma unroll
@@ -273,7 +283,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sA + s * kABytes, &tmW, &full[s], kx, n_tile * kBlockM, pol_w);
         tma_load_2d(sB + s * kBBytes, &tmX, &full[s], kx, m_tile * BN, pol_x);
       }
+      // own stream fully issued: pull this CTA's share of the successor's
+      // weights into L2 so the kernel boundary does not idle HBM
+      const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+      prefetch_l2_share(a.pf_ptr, a.pf_bytes, cta, gridDim.x * gridDim.y * gridDim.z);
     }
+  } else if (warp >= 2) {
+    // idle warps: input-RMS scales of this token tile, overlapped with the mainloop
+    pdl_wait();
+    const int m0 = m_tile * BN;
+    input_scales(a, m0, min(BN, a.M - m0), inv_s, threadIdx.x - 64, kThreads - 64);
   } else if (warp == 1) {
     if (elect_one()) {
       for (int i = 0; i < kb_per; ++i) {
@@ -313,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 16; ++j) red[(c * 16 + j) * 128 + row] = v[j];
   }
   if (a.splits == 1) {
-    epi_cols<EPI>(a, n_tile, m0, cols, red, inv_s);
+    epi_cols<EPI>(a, n_tile, m0, cols, red, inv_s);  // epi_cols syncs before reading inv_s
   } else {
     // The split CTAs of this tile form one cluster (rank == split). Each
     // reduces a slice of token columns across all ranks, in rank order, so
@@ -340,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (z < S) acc.x += v[z].x, acc.y += v[z].y, acc.z += v[z].z, acc.w += v[z].w;
       *reinterpret_cast<float4*>(fin + (c - c0) * 128 + r4) = acc;
     }
-    if (c1 > c0) epi_cols<EPI>(a, n_tile, m0 + c0, c1 - c0, fin, inv_s);
+    if (c1 > c0) epi_cols<EPI>(a, n_tile, m0 + c0, c1 - c0, fin, inv_s + c0);
     cluster_sync();  // keep our partial alive until every rank has read it
   }
 
@@ -351,8 +370,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN>
 constexpr int stages_for() {
-  // two CTAs per SM for the skinny decode tiles, deep rings for the wide ones
-  return BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 8 : BN <= 128 ? 6 : 4;
+  // Decode tiles: <= ~112 KB (two CTAs per SM; a decode grid has <= 192
+  // CTAs, so every SM keeps a slot for the NEXT kernel's CTA to start (PDL)
+  // and prefetch its weights while this one drains). Measured (in-chain,
+  // tools/gemm_sweep.py): 6 stages beat 4 on the 67 MB gate-up weight.
+  // Wide tiles (prefill / DiT): deep rings, one CTA per SM.
+  return BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 6 : 4;
 }
 template <int BN>
 constexpr size_t epi_smem_for() {
@@ -379,7 +402,14 @@ cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a
 template <int EPI>
 cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                        cudaStream_t st) {
-  const int bn = gemm_block_n(a.M);
+  int bn = gemm_block_n(a.M);
+  if (w.fill_sms && bn > 64) {
+    // compute-bound weights (DiT): the widest token tile that still puts
+    // >= one CTA on every SM; the per-element result does not depend on BN
+    const int tiles = w.N_pad / kBlockM;
+    bn = 256;
+    while (bn > 64 && tiles * ((a.M + bn - 1) / bn) * a.splits < 148) bn /= 2;
+  }
   switch (bn) {
     case 16: return launch_bn<16, EPI>(w, x, a, st);
     case 32: return launch_bn<32, EPI>(w, x, a, st);
@@ -414,6 +444,8 @@ cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, co
   a.ldg = e.ldg;
   a.gate_off = e.gate_off;
   a.rows_per_group = e.rows_per_group > 0 ? e.rows_per_group : 1;
+  a.gate_index = e.gate_index;
+  a.gate_index_stride = e.gate_index_stride;
   a.ss_in = e.ss_in;
   a.ss_ld = e.ss_ld;
   a.ss_n = e.ss_n;
@@ -422,6 +454,11 @@ cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, co
   a.xb = e.xb;
   a.ss_out = e.ss_out;
   a.rope = e.rope;
+  a.row_bias = e.row_bias;
+  a.bias_period = e.bias_period > 0 ? e.bias_period : 1;
+  if (e.row_bias && (epi != EPI_F32 || w.N != w.N_pad)) return cudaErrorInvalidValue;
+  a.pf_ptr = e.pf_ptr;
+  a.pf_bytes = e.pf_bytes & ~uint64_t(15);
   if (epi == EPI_RESID_NORM && (e.xb == nullptr || e.ss_out == nullptr || w.N != w.N_pad))
     return cudaErrorInvalidValue;
   if (epi == EPI_ROPE_KV && (e.rope.rows == nullptr || e.rope.kv == nullptr || e.rope.q_out == nullptr ||

@@ -76,6 +76,29 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// L2 prefetch of a global range (bytes multiple of 16, 16-B aligned).
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// This CTA's share of a successor-weight range, prefetched into L2 in 64 KB
+// pieces spread over the calling threads (tid / nthreads): the weights a
+// later kernel of the step will stream are static, so they can be pulled
+// into the 126 MB L2 while the current kernel's own streaming drains
+// (cross-kernel pipelining of the step's weight stream).
+__device__ __forceinline__ void prefetch_l2_share(const void* base, uint64_t bytes, uint32_t part,
+                                                  uint32_t parts, uint32_t tid = 0,
+                                                  uint32_t nthreads = 1) {
+  if (base == nullptr || bytes == 0) return;
+  const uint64_t per = ((bytes + parts - 1) / parts + 15) & ~uint64_t(15);
+  uint64_t lo = (uint64_t)part * per, hi = lo + per;
+  if (hi > bytes) hi = bytes;
+  const char* p = static_cast<const char*>(base);
+  for (uint64_t o = lo + (uint64_t)tid * 65536; o < hi; o += (uint64_t)nthreads * 65536) {
+    const uint64_t n = hi - o < 65536 ? hi - o : 65536;
+    prefetch_l2(p + o, (uint32_t)(n & ~uint64_t(15)));
+  }
+}
+
 // ---- tcgen05 --------------------------------------------------------------
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {

@@ -9,6 +9,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <tuple>
 
 #include "common.h"
 #include "kernels.h"
@@ -58,7 +59,7 @@ DevTensor make_swiglu(omni_stage* st, const std::string& name, int64_t ff, int64
   return t;
 }
 
-GemmWeight gemm_of(const DevTensor& t, int max_splits, int target_ctas = 296) {
+GemmWeight gemm_of(const DevTensor& t, int max_splits, int target_ctas = 192) {
   GemmWeight g;
   OMNI_REQUIRE(gemm_make_weight(g, t.p, (int)t.rows, (int)t.rows_pad, (int)t.cols, max_splits, target_ctas),
                OMNI_E_BADARG, "weight tensor map encode failed");
@@ -207,7 +208,9 @@ void build_dit(omni_stage* st) {
   st->w_out = make_weight(st, "w_out", C, round_up(C, 128), d, 5, s_d);
   st->w_mod = make_weight(st, "w_mod", (int64_t)L * 6 * d, (int64_t)L * 6 * d, d, 6, 0.5f * s_d);
   st->g_in = gemm_of(st->w_in, 1);
-  st->g_out = gemm_of(st->w_out, 4, 64);
+  st->g_in.fill_sms = true;
+  st->g_out = gemm_of(st->w_out, 1);
+  st->g_out.fill_sms = true;
   st->g_mod = gemm_of(st->w_mod, 1);
   st->dlayers.resize(L);
   for (int l = 0; l < L; ++l) {
@@ -218,10 +221,14 @@ void build_dit(omni_stage* st) {
     ly.wo = make_weight(st, p + "wo", d, d, d, b + 2, s_d);
     ly.w1 = make_weight(st, p + "w1", ff, ff, d, b + 3, s_d);
     ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
-    ly.gqkv = gemm_of(ly.wqkv, 4, 64);
-    ly.go = gemm_of(ly.wo, 4, 64);
-    ly.g1 = gemm_of(ly.w1, 4, 64);
-    ly.g2 = gemm_of(ly.w2, 4, 64);
+    ly.gqkv = gemm_of(ly.wqkv, 1);
+    ly.gqkv.fill_sms = true;
+    ly.go = gemm_of(ly.wo, 1);
+    ly.go.fill_sms = true;
+    ly.g1 = gemm_of(ly.w1, 1);
+    ly.g1.fill_sms = true;
+    ly.g2 = gemm_of(ly.w2, 1);
+    ly.g2.fill_sms = true;
   }
   const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
   const int R = st->drows_cap = T * kDitSamples;
@@ -233,19 +240,18 @@ void build_dit(omni_stage* st) {
   st->dout = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
   st->du = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
   st->dv = dev_alloc<float>(st, (size_t)R * C);
-  st->dcvec = dev_alloc<__nv_bfloat16>(st, (size_t)T * d);
-  st->dmod = dev_alloc<float>(st, (size_t)T * L * 6 * d);
+  const int cvec_rows = std::max(T, m.vocab);  // per-step rows / adaLN table rows
+  st->dcvec = dev_alloc<__nv_bfloat16>(st, (size_t)cvec_rows * d);
   st->dsamples = dev_alloc<int32_t>(st, R);
   st->din_x = input_of(st->dxin, R, C);
   st->din_a = input_of(st->da, R, d);
   st->din_o = input_of(st->dout, R, d);
   st->din_u = input_of(st->du, R, ff);
-  st->din_c = input_of(st->dcvec, T, d);
+  st->din_c = input_of(st->dcvec, cvec_rows, d);
   // adaLN modulation table: mod[t][id] = W_mod . silu(tok_emb[id] + t_emb[t])
   // for every (Euler step, conditioning id) — the per-token GEMM of the
   // reference-shaped model depends on nothing else, so it is evaluated once
   // here with the same kernel (batch invariance => identical rows).
-  OMNI_REQUIRE(m.vocab <= T, OMNI_E_BADARG, "DiT vocab exceeds dit_max_tokens");
   const int ld_mod = L * 6 * d;
   st->mod_table = dev_alloc<float>(st, (size_t)m.dit_steps * m.vocab * ld_mod);
   {
@@ -469,8 +475,23 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
       // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
       const int ss_ld = d / 128;
+      // Cross-kernel weight pipelining: every kernel prefetches (into L2) a
+      // slice of a LATER GEMM's weights, so HBM keeps streaming through the
+      // kernel boundaries (epilogues, attention, launch gaps).
+      static const uint64_t kPf = [] {  // OMNI_PF_MB: prefetch window, default off (measured slower)
+        const char* e = std::getenv("OMNI_PF_MB");
+        return (uint64_t)(e ? std::atoi(e) : 0) << 20;
+      }();
+      auto wbytes = [](const GemmWeight& g) { return (uint64_t)g.N_pad * g.K * 2; };
+      auto part = [&](const GemmWeight& g, uint64_t off) -> std::pair<const void*, uint64_t> {
+        const uint64_t n = wbytes(g);
+        if (off >= n || kPf == 0) return {nullptr, 0};
+        return {reinterpret_cast<const char*>(g.ptr) + off, std::min(kPf, n - off)};
+      };
+      const auto pf0 = part(st->layers[0].gqkv, 0);
       OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
-                             st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld, s));
+                             st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld,
+                             pf0.first, pf0.second, s));
       GemmEpilogue norm_in;  // fused RMSNorm of the GEMM input
       norm_in.ss_in = st->ss;
       norm_in.ss_ld = ss_ld;
@@ -492,19 +513,25 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
         e.rope.n_kv = KVH;
         e.rope.layer = l;
         e.rope.n_layers = L;
+        std::tie(e.pf_ptr, e.pf_bytes) = part(ly.go, 0);
         OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
-        OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, s));
+        const auto pfa = part(ly.ggu, 0);
+        OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, pfa.first,
+                                     pfa.second, s));
         GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
         r.out = st->x;
         r.ldo = d;
         r.xb = st->xn;
         r.ss_out = st->ss;
         r.ss_ld = ss_ld;
+        std::tie(r.pf_ptr, r.pf_bytes) = part(ly.ggu, kPf);
         OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, r, s));
         e = norm_in;
         e.out = st->act;
         e.ldo = m.d_ff;
+        std::tie(e.pf_ptr, e.pf_bytes) = part(ly.gd, 0);
         OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
+        std::tie(r.pf_ptr, r.pf_bytes) = l + 1 < L ? part(st->layers[l + 1].gqkv, 0) : part(st->glm, 0);
         OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, r, s));
       }
       if (n_dec > 0) {
@@ -543,20 +570,22 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
   const int rows = n_tok * S;
   const int ld_mod = L * 6 * d;
   cudaStream_t s = st->stream;
-  OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, s));
+  OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, st->dxin, s));
   for (int t = 0; t < T; ++t) {
-    OMNI_KERNEL(dit_mod_gather(toks_dev, n_tok, st->mod_table + (size_t)t * m.vocab * ld_mod, ld_mod,
-                               st->dmod, s));
+    // adaLN rows of this Euler step: table[t][id] (no per-step gather)
+    const float* mod_t = st->mod_table + (size_t)t * m.vocab * ld_mod;
+    const int32_t* tok_ids = &toks_dev[0].id;
+    constexpr int kIdStride = sizeof(DitTokDesc) / sizeof(int32_t);
     GemmEpilogue e;
-    OMNI_KERNEL(dit_to_bf16(st->dx, (int64_t)rows * C, st->dxin, s));
     e.out = st->dh;
     e.ldo = d;
+    e.row_bias = st->pos_emb.p;  // h = W_in x + pos_emb[sample] (fused)
+    e.bias_period = S;
     OMNI_KERNEL(gemm_run(st->g_in, st->din_x, rows, EPI_F32, e, s));
-    OMNI_KERNEL(dit_add_pos(st->dh, st->pos_emb.p, S, d, rows, s));
     for (int l = 0; l < L; ++l) {
       const auto& ly = st->dlayers[l];
       const int base = l * 6 * d;
-      OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 0, base + d, S, st->da, s));
+      OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, mod_t, toks_dev, ld_mod, base + 0, base + d, S, st->da, s));
       e = GemmEpilogue{};
       e.out = st->dqkv;
       e.ldo = 3 * d;
@@ -565,12 +594,14 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
       e = GemmEpilogue{};
       e.out = st->dh;
       e.ldo = d;
-      e.gate = st->dmod;
+      e.gate = mod_t;
       e.ldg = ld_mod;
       e.gate_off = base + 2 * d;
       e.rows_per_group = S;
+      e.gate_index = tok_ids;
+      e.gate_index_stride = kIdStride;
       OMNI_KERNEL(gemm_run(ly.go, st->din_o, rows, EPI_GATED_RESID, e, s));
-      OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, st->dmod, ld_mod, base + 3 * d, base + 4 * d, S, st->da, s));
+      OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, mod_t, toks_dev, ld_mod, base + 3 * d, base + 4 * d, S, st->da, s));
       GemmEpilogue e1;
       e1.out = st->du;
       e1.ldo = m.d_ff;
@@ -578,12 +609,12 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
       e.gate_off = base + 5 * d;
       OMNI_KERNEL(gemm_run(ly.g2, st->din_u, rows, EPI_GATED_RESID, e, s));
     }
-    OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, nullptr, 0, 0, 0, S, st->da, s));
+    OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, nullptr, toks_dev, 0, 0, 0, S, st->da, s));
     GemmEpilogue eo;
     eo.out = st->dv;
     eo.ldo = C;
     OMNI_KERNEL(gemm_run(st->g_out, st->din_a, rows, EPI_F32, eo, s));
-    OMNI_KERNEL(dit_euler(st->dx, st->dv, C, rows, 1.f / T, t == T - 1, samples_dev, s));
+    OMNI_KERNEL(dit_euler(st->dx, st->dxin, st->dv, C, rows, 1.f / T, t == T - 1, samples_dev, s));
   }
 }
 
@@ -742,7 +773,17 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;
     if (st->lim.dit_max_tokens <= 0) st->lim.dit_max_tokens = 512;
     OMNI_CUDA(cudaSetDevice(dev));
-    OMNI_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+    // Stream priority by stage kind when stages share a GPU: the Talker's
+    // per-token decode chain is the pipeline's critical path (4 codec tokens
+    // per text token), then the Thinker; the DiT (compute-bound,
+    // chunk-batched) soaks up the SMs the AR chains leave idle.
+    int lo = 0, hi = 0;
+    OMNI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // hi = numerically lowest = most urgent
+    const int prio = model->kind == OMNI_MODEL_TALKER ? hi
+                     : model->kind == OMNI_MODEL_THINKER ? (hi + lo) / 2
+                                                         : lo;
+    OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking,
+                                           std::getenv("OMNI_PRIO") && std::getenv("OMNI_PRIO")[0] == '0' ? lo : prio));
     OMNI_CUDA(cudaEventCreate(&st->ev_start));
     OMNI_CUDA(cudaEventCreate(&st->ev_done));
     OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_link, cudaEventDisableTiming));

@@ -94,7 +94,7 @@ struct omni_stage {
   omni_dev::GemmWeight g_in, g_out, g_mod;
   std::vector<omni_dev::DitLayer> dlayers;
   int tok_cap = 0, drows_cap = 0;
-  float *dx = nullptr, *dh = nullptr, *dv = nullptr, *dmod = nullptr;
+  float *dx = nullptr, *dh = nullptr, *dv = nullptr;
   float* mod_table = nullptr;  // [T][vocab][L*6*d] adaLN modulation rows
   __nv_bfloat16 *dxin = nullptr, *da = nullptr, *dqkv = nullptr, *dout = nullptr, *du = nullptr,
                 *dcvec = nullptr;

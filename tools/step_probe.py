@@ -86,6 +86,10 @@ def dit_probe(ntoks):
 
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
-    ar_probe(D.THINKER, [1, 4, 16] if quick else [1, 2, 4, 8, 16, 32, 64])
-    ar_probe(D.TALKER, [1, 16] if quick else [1, 4, 16, 32, 64])
-    dit_probe([8, 64] if quick else [8, 32, 64, 128, 256, 512])
+    if "--dit-only" not in sys.argv:
+        ar_probe(D.THINKER, [1, 4, 16] if quick else [1, 2, 4, 8, 16, 32, 64])
+        ar_probe(D.TALKER, [1, 16] if quick else [1, 4, 16, 32, 64])
+    if "--dit64" in sys.argv:
+        dit_probe([64])
+    elif "--ar-only" not in sys.argv:
+        dit_probe([8, 64] if quick else [8, 32, 64, 128, 256, 512])
