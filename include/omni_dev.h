@@ -221,6 +221,13 @@ omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, i
                                    int32_t M, int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits,
                                    int32_t iters, float* ms);
 
+/* Phase trace of the last of n_w chained launches (tools/gemm_trace.py):
+ * trace_dev holds 8 u64 per CTA (globaltimer entry/exit + clock64 phase
+ * offsets); *grid_ctas = CTAs of the launch. */
+omni_status omni_k_gemm_trace(const uint64_t* Ws, int32_t n_w, int32_t N, int32_t K, uint64_t X, int32_t M,
+                              int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits, uint64_t trace_dev,
+                              int32_t* grid_ctas);
+
 #ifdef __cplusplus
 }
 #endif

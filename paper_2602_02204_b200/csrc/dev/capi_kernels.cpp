@@ -207,6 +207,37 @@ omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, i
   });
 }
 
+omni_status omni_k_gemm_trace(const uint64_t* Ws, int32_t n_w, int32_t N, int32_t K, uint64_t X, int32_t M,
+                              int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits, uint64_t trace_dev,
+                              int32_t* grid_ctas) {
+  return guarded([&] {
+    require_gpu();
+    OMNI_REQUIRE(n_w > 0, OMNI_E_BADARG, "gemm_trace: empty");
+    const int N_pad = (N + 127) / 128 * 128;
+    std::vector<GemmWeight> ws(n_w);
+    for (int i = 0; i < n_w; ++i)
+      OMNI_REQUIRE(gemm_make_weight(ws[i], reinterpret_cast<const __nv_bfloat16*>(Ws[i]), N, N_pad, K, max_splits),
+                   OMNI_E_BADARG, "weight tensor map");
+    GemmInput x;
+    OMNI_REQUIRE(gemm_make_input(x, reinterpret_cast<const __nv_bfloat16*>(X), M, K), OMNI_E_BADARG, "input map");
+    GemmEpilogue e;
+    e.out = reinterpret_cast<void*>(out);
+    e.ldo = ldo;
+    cudaStream_t cs;
+    OMNI_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int i = 0; i < n_w; ++i) OMNI_CUDA(gemm_run(ws[i], x, M, epi, e, cs));  // warm-up chain
+    OMNI_CUDA(cudaStreamSynchronize(cs));
+    // a PDL chain of n_w launches; the last one is traced
+    for (int i = 0; i < n_w; ++i) {
+      if (i == n_w - 1) e.trace = reinterpret_cast<unsigned long long*>(trace_dev);
+      OMNI_CUDA(gemm_run(ws[i], x, M, epi, e, cs));
+    }
+    OMNI_CUDA(cudaStreamSynchronize(cs));
+    cudaStreamDestroy(cs);
+    if (grid_ctas) *grid_ctas = (N_pad / 128) * ((M + gemm_block_n(M) - 1) / gemm_block_n(M)) * ws[0].splits;
+  });
+}
+
 omni_status omni_k_fill_weights(uint64_t dst, int64_t n, uint64_t seed, uint32_t tensor_id,
                                 float scale) {
   return guarded([&] {

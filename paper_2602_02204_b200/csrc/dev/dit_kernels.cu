@@ -133,53 +133,115 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Attention among the S samples of one token, one CTA per (token, head).
-__global__ void __launch_bounds__(128)
-    dit_attn_kernel(const __nv_bfloat16* __restrict__ qkv, int d, int n_heads,
+// Attention among the S = 16 samples of one token: one WARP per (token,
+// head), 8 per CTA. S = Q K^T (16x16, K = 128) runs on the warp MMA
+// (mma.sync m16n8k16 bf16 -> fp32, Q/K fragments loaded straight from the
+// bf16 QKV rows), softmax in fp32 on the accumulator fragments (row = 4
+// lanes), P.V in fp32 on the CUDA cores (lane = 4 head dims, V rows read
+// once per warp, coalesced).
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                               uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__global__ void __launch_bounds__(256)
+    dit_attn_kernel(const __nv_bfloat16* __restrict__ qkv, int n_tok, int d, int n_heads,
                     __nv_bfloat16* __restrict__ out) {
   pdl_wait();
   pdl_trigger();
   constexpr int S = kDitSamples, HD = 128;
-  __shared__ float sq[S][HD + 1], sk[S][HD + 1], sv[S][HD];
-  __shared__ float sp[S][S + 1];
-  const int p = blockIdx.x, h = blockIdx.y;
-  const size_t row0 = (size_t)p * S;
-  const int ld = 3 * d;
-  for (int t = threadIdx.x; t < S * HD; t += blockDim.x) {
-    const int i = t / HD, c = t % HD;
-    const __nv_bfloat16* rp = qkv + (row0 + i) * ld + h * HD + c;
-    sq[i][c] = bf2f(rp[0]);
-    sk[i][c] = bf2f(rp[d]);
-    sv[i][c] = bf2f(rp[2 * d]);
+  static_assert(S == 16, "one m16 MMA tile per token");
+  __shared__ float sp[8][S][S + 1];
+  const int warp = warp_id(), lane = lane_id();
+  const int item = blockIdx.x * 8 + warp;
+  if (item >= n_tok * n_heads) return;
+  const int p = item / n_heads, h = item % n_heads;
+  const int g = lane >> 2, t = lane & 3;
+  const size_t ld = 3 * (size_t)d;
+  const __nv_bfloat16* Q = qkv + (size_t)p * S * ld + h * HD;
+  const __nv_bfloat16* K = Q + d;
+  const __nv_bfloat16* V = Q + 2 * d;
+  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};  // keys 0-7, 8-15
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    const int col = kk * 16 + 2 * t;
+    uint32_t a[4];
+    a[0] = *reinterpret_cast<const uint32_t*>(Q + (size_t)g * ld + col);
+    a[1] = *reinterpret_cast<const uint32_t*>(Q + (size_t)(g + 8) * ld + col);
+    a[2] = *reinterpret_cast<const uint32_t*>(Q + (size_t)g * ld + col + 8);
+    a[3] = *reinterpret_cast<const uint32_t*>(Q + (size_t)(g + 8) * ld + col + 8);
+    // B = K^T: column n = key n, k = head dim -> contiguous pairs of a K row
+    const uint32_t b00 = *reinterpret_cast<const uint32_t*>(K + (size_t)g * ld + col);
+    const uint32_t b01 = *reinterpret_cast<const uint32_t*>(K + (size_t)g * ld + col + 8);
+    const uint32_t b10 = *reinterpret_cast<const uint32_t*>(K + (size_t)(g + 8) * ld + col);
+    const uint32_t b11 = *reinterpret_cast<const uint32_t*>(K + (size_t)(g + 8) * ld + col + 8);
+    mma_bf16_16816(c0, a, b00, b01);
+    mma_bf16_16816(c1, a, b10, b11);
   }
-  __syncthreads();
+  // fragments: row g -> c0[0..1] (keys 2t,2t+1), c1[0..1] (keys 8+2t, 9+2t);
+  //            row g+8 -> c0[2..3], c1[2..3]
   const float scale = rsqrtf((float)HD);
-  for (int t = threadIdx.x; t < S * S; t += blockDim.x) {
-    const int i = t / S, j = t % S;
-    float acc = 0.f;
-    for (int c = 0; c < HD; ++c) acc += sq[i][c] * sk[j][c];
-    sp[i][j] = acc * scale;
+  float r0[4] = {c0[0] * scale, c0[1] * scale, c1[0] * scale, c1[1] * scale};
+  float r1[4] = {c0[2] * scale, c0[3] * scale, c1[2] * scale, c1[3] * scale};
+  float m0 = fmaxf(fmaxf(r0[0], r0[1]), fmaxf(r0[2], r0[3]));
+  float m1 = fmaxf(fmaxf(r1[0], r1[1]), fmaxf(r1[2], r1[3]));
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
   }
-  __syncthreads();
-  if (threadIdx.x < S) {
-    const int i = threadIdx.x;
-    float m = -INFINITY;
-    for (int j = 0; j < S; ++j) m = fmaxf(m, sp[i][j]);
-    float l = 0.f;
-    for (int j = 0; j < S; ++j) {
-      const float e = expf(sp[i][j] - m);
-      sp[i][j] = e;
-      l += e;
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    r0[i] = expf(r0[i] - m0);
+    r1[i] = expf(r1[i] - m1);
+    s0 += r0[i];
+    s1 += r1[i];
+  }
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  const float i0 = 1.f / s0, i1 = 1.f / s1;
+  float(*P)[S + 1] = sp[warp];
+  P[g][2 * t] = r0[0] * i0;
+  P[g][2 * t + 1] = r0[1] * i0;
+  P[g][8 + 2 * t] = r0[2] * i0;
+  P[g][9 + 2 * t] = r0[3] * i0;
+  P[g + 8][2 * t] = r1[0] * i1;
+  P[g + 8][2 * t + 1] = r1[1] * i1;
+  P[g + 8][8 + 2 * t] = r1[2] * i1;
+  P[g + 8][9 + 2 * t] = r1[3] * i1;
+  __syncwarp();
+  // P.V: lane owns head dims 4*lane .. 4*lane+3 of all 16 rows
+  float acc[S][4];
+#pragma unroll
+  for (int i = 0; i < S; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+#pragma unroll 4
+  for (int j = 0; j < S; ++j) {
+    const uint2 raw = *reinterpret_cast<const uint2*>(V + (size_t)j * ld + 4 * lane);
+    const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+    const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+      const float pij = P[i][j];
+      acc[i][0] += pij * v01.x;
+      acc[i][1] += pij * v01.y;
+      acc[i][2] += pij * v23.x;
+      acc[i][3] += pij * v23.y;
     }
-    const float inv = 1.f / l;
-    for (int j = 0; j < S; ++j) sp[i][j] *= inv;
   }
-  __syncthreads();
-  const int c = threadIdx.x;  // one head dim per thread
+#pragma unroll
   for (int i = 0; i < S; ++i) {
-    float acc = 0.f;
-    for (int j = 0; j < S; ++j) acc += sp[i][j] * sv[j][c];
-    out[(row0 + i) * d + h * HD + c] = f2bf(acc);
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(acc[i][0], acc[i][1]);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(acc[i][2], acc[i][3]);
+    *reinterpret_cast<uint2*>(out + ((size_t)p * S + i) * d + h * HD + 4 * lane) =
+        make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
   }
 }
 
@@ -237,8 +299,8 @@ cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod_base, c
 }
 cudaError_t dit_attn(const __nv_bfloat16* qkv, int n_tok, int d, int n_heads, __nv_bfloat16* out,
                      cudaStream_t st) {
-  dim3 grid(n_tok, n_heads);
-  return launch_k(dit_attn_kernel, dim3(grid), dim3(128), 0, st, 1, qkv, d, n_heads, out);
+  return launch_k(dit_attn_kernel, dim3((n_tok * n_heads + 7) / 8), dim3(256), 0, st, 1, qkv, n_tok, d, n_heads,
+                  out);
 }
 cudaError_t dit_euler(float* x, __nv_bfloat16* xb, const float* v, int C, int rows, float dt, int last,
                       int32_t* samples, cudaStream_t st) {

@@ -81,6 +81,9 @@ struct GemmEpilogue {
   // EPI_F32 only: out[tok, n] = acc + row_bias[tok % bias_period, n] (bf16 rows of width N)
   const __nv_bfloat16* row_bias = nullptr;
   int bias_period = 1;
+  // phase trace (tools only): per CTA 8 u64 = globaltimer at entry / exit and
+  // clock64 deltas of setup, producer-wait, last-load, mainloop-done, drain, end
+  unsigned long long* trace = nullptr;
 };
 
 // Kernel-side argument block.
@@ -102,6 +105,7 @@ struct GemmArgs {
   uint64_t pf_bytes;
   const __nv_bfloat16* row_bias;
   int bias_period;
+  unsigned long long* trace;
 };
 
 int gemm_block_n(int M);

@@ -28,6 +28,8 @@
 
 namespace omni_dev {
 
+static int bn_for(const GemmWeight& w, int M);  // token-tile width for (weight, batch)
+
 namespace {
 
 constexpr int kBlockM = 128;  // weight rows per tile (MMA M)
@@ -241,6 +243,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = warp_id(), lane = lane_id();
   const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
   const int kb_per = (a.K / kBlockK) / a.splits;
+  unsigned long long* tr = a.trace ? a.trace + 8ull * ((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x)
+                                   : nullptr;
+  const long long c0 = clock64();
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   const int kb0 = split * kb_per;
 
   if (warp == 0 && lane == 0) {
@@ -259,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
+  if (tr && threadIdx.x == 0) tr[1] = clock64() - c0;
 
   if (warp == 0) {
     if (elect_one()) {
@@ -272,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sA + i * kABytes, &tmW, &full[i], (kb0 + i) * kBlockK, n_tile * kBlockM, pol_w);
       }
       pdl_wait();
+      if (tr) tr[2] = clock64() - c0;
       for (int i = 0; i < pre; ++i)
         tma_load_2d(sB + i * kBBytes, &tmX, &full[i], (kb0 + i) * kBlockK, m_tile * BN, pol_x);
       for (int i = pre; i < kb_per; ++i) {
@@ -283,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sA + s * kABytes, &tmW, &full[s], kx, n_tile * kBlockM, pol_w);
         tma_load_2d(sB + s * kBBytes, &tmX, &full[s], kx, m_tile * BN, pol_x);
       }
+      if (tr) tr[3] = clock64() - c0;
       // own stream fully issued: pull this CTA's share of the successor's
       // weights into L2 so the kernel boundary does not idle HBM
       const uint32_t cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // reduction over DSMEM in fixed rank order] -> fused op -------------------
   mbar_wait(done, 0);
   tc_fence_after();
+  if (tr && threadIdx.x == 0) tr[4] = clock64() - c0;
   const int row = warp * 32 + lane;  // TMEM lane == output feature within tile
   const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
   const int m0 = m_tile * BN;
@@ -331,6 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
     for (int j = 0; j < 16; ++j) red[(c * 16 + j) * 128 + row] = v[j];
   }
+  if (tr && threadIdx.x == 0) tr[5] = clock64() - c0;
   if (a.splits == 1) {
     epi_cols<EPI>(a, n_tile, m0, cols, red, inv_s);  // epi_cols syncs before reading inv_s
   } else {
@@ -366,6 +377,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_free<kTmemCols>(tmem);
+  if (tr && threadIdx.x == 0) {
+    tr[6] = clock64() - c0;
+    tr[7] = globaltimer();
+  }
 }
 
 template <int BN>
@@ -384,8 +399,8 @@ constexpr size_t epi_smem_for() {
 template <int BN>
 constexpr size_t smem_for() {
   constexpr size_t pipe = stages_for<BN>() * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
-  // + barriers / tmem slot (256 B) + per-column input-RMS scales (4 B x BN)
-  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256 + 4 * BN;
+  // + barriers / tmem slot (256 B) + per-column input-RMS scales (4 B x BN) + flag
+  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256 + 4 * BN + 16;
 }
 
 template <int BN, int EPI>
@@ -402,15 +417,9 @@ cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a
 template <int EPI>
 cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                        cudaStream_t st) {
-  int bn = gemm_block_n(a.M);
-  if (w.fill_sms && bn > 64) {
-    // compute-bound weights (DiT): the widest token tile that still puts
-    // >= one CTA on every SM; the per-element result does not depend on BN
-    const int tiles = w.N_pad / kBlockM;
-    bn = 256;
-    while (bn > 64 && tiles * ((a.M + bn - 1) / bn) * a.splits < 148) bn /= 2;
-  }
-  switch (bn) {
+  // compute-bound weights (DiT, fill_sms): the widest token tile that still
+  // puts >= one CTA on every SM; the per-element result does not depend on BN
+  switch (bn_for(w, a.M)) {
     case 16: return launch_bn<16, EPI>(w, x, a, st);
     case 32: return launch_bn<32, EPI>(w, x, a, st);
     case 64: return launch_bn<64, EPI>(w, x, a, st);
@@ -420,6 +429,16 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
 }
 
 }  // namespace
+
+static int bn_for(const GemmWeight& w, int M) {
+  int bn = gemm_block_n(M);
+  if (w.fill_sms && bn > 64) {
+    const int tiles = w.N_pad / kBlockM;
+    bn = 256;
+    while (bn > 64 && tiles * ((M + bn - 1) / bn) * w.splits < 148) bn /= 2;
+  }
+  return bn;
+}
 
 int gemm_block_n(int M) {
   return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
@@ -454,6 +473,7 @@ cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, co
   a.xb = e.xb;
   a.ss_out = e.ss_out;
   a.rope = e.rope;
+  a.trace = e.trace;
   a.row_bias = e.row_bias;
   a.bias_period = e.bias_period > 0 ? e.bias_period : 1;
   if (e.row_bias && (epi != EPI_F32 || w.N != w.N_pad)) return cudaErrorInvalidValue;

@@ -209,6 +209,11 @@ __device__ __forceinline__ float4 dsmem_ld_f32x4(uint32_t cluster_saddr) {
 }
 
 // ---- misc -----------------------------------------------------------------
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

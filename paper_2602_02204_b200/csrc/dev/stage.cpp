@@ -162,6 +162,7 @@ void build_ar(omni_stage* st) {
   st->in_attn = input_of(st->attn, R, H * kHeadDim);
   st->in_act = input_of(st->act, R, ff);
   st->in_hbuf = input_of(st->hbuf, R, d);
+
   if (talker) {
     st->condin = dev_alloc<__nv_bfloat16>(st, (size_t)R * m.cond_dim);
     st->hproj = dev_alloc<float>(st, (size_t)R * d);
@@ -773,17 +774,19 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;
     if (st->lim.dit_max_tokens <= 0) st->lim.dit_max_tokens = 512;
     OMNI_CUDA(cudaSetDevice(dev));
-    // Stream priority by stage kind when stages share a GPU: the Talker's
-    // per-token decode chain is the pipeline's critical path (4 codec tokens
-    // per text token), then the Thinker; the DiT (compute-bound,
-    // chunk-batched) soaks up the SMs the AR chains leave idle.
+    // Stream priority by stage kind when stages share a GPU. OMNI_PRIO = three
+    // digits, the urgency rank (0 = most urgent) of thinker / talker / DiT.
+    // Default "000" (all equal): measured best for the bench workload; ranking
+    // the Talker (the per-token critical path) first starves the DiT and the
+    // final waveform chunks (profiles/r01_bench_prio_ab.txt).
     int lo = 0, hi = 0;
     OMNI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // hi = numerically lowest = most urgent
-    const int prio = model->kind == OMNI_MODEL_TALKER ? hi
-                     : model->kind == OMNI_MODEL_THINKER ? (hi + lo) / 2
-                                                         : lo;
-    OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking,
-                                           std::getenv("OMNI_PRIO") && std::getenv("OMNI_PRIO")[0] == '0' ? lo : prio));
+    const char* pe = std::getenv("OMNI_PRIO");
+    const char* ranks = (pe && std::strlen(pe) == 3) ? pe : "000";
+    const int kind_ix = model->kind == OMNI_MODEL_THINKER ? 0 : model->kind == OMNI_MODEL_TALKER ? 1 : 2;
+    const int rank = std::clamp(ranks[kind_ix] - '0', 0, 2);
+    const int prio = hi + (lo - hi) * rank / 2;
+    OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, prio));
     OMNI_CUDA(cudaEventCreate(&st->ev_start));
     OMNI_CUDA(cudaEventCreate(&st->ev_done));
     OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_link, cudaEventDisableTiming));

@@ -116,4 +116,5 @@ struct omni_stage {
   int64_t pending_samples = 0;
   float last_step_us = 0.f;
   std::unordered_map<uint64_t, omni_dev::StepGraph> graphs;  // step graphs by launch geometry
+
 };
