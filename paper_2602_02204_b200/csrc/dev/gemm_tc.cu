@@ -18,6 +18,7 @@
 // (ar_engine.hpp:308-337, reference_pipeline.hpp:96-154) for the dense
 // projections; reused by the DiT (diffusion_engine.hpp:28-43 replacement).
 #include <cuda.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -433,9 +434,22 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
 static int bn_for(const GemmWeight& w, int M) {
   int bn = gemm_block_n(M);
   if (w.fill_sms && bn > 64) {
+    static const int forced = [] {  // OMNI_DIT_BN: experiments only
+      const char* e = std::getenv("OMNI_DIT_BN");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (forced == 64 || forced == 128 || forced == 256) return forced;
+    // wave-quantised cost model: waves x (BN + 32), the 32 standing for the
+    // per-tile prologue/epilogue; ties go to the wider tile (fewer re-reads)
     const int tiles = w.N_pad / kBlockM;
-    bn = 256;
-    while (bn > 64 && tiles * ((M + bn - 1) / bn) * w.splits < 148) bn /= 2;
+    int best = 256;
+    long best_cost = -1;
+    for (int cand = 256; cand >= 64; cand /= 2) {
+      const long ctas = (long)tiles * ((M + cand - 1) / cand) * w.splits;
+      const long cost = ((ctas + 147) / 148) * (cand + 32);
+      if (best_cost < 0 || cost < best_cost) best = cand, best_cost = cost;
+    }
+    bn = best;
   }
   return bn;
 }

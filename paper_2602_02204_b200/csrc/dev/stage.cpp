@@ -224,11 +224,15 @@ void build_dit(omni_stage* st) {
     ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
     ly.gqkv = gemm_of(ly.wqkv, 1);
     ly.gqkv.fill_sms = true;
-    ly.go = gemm_of(ly.wo, 1);
+    static const int dit_split = [] {  // OMNI_DIT_SPLIT: split-K cap of the N=d DiT GEMMs (experiments)
+      const char* e = std::getenv("OMNI_DIT_SPLIT");
+      return e ? std::atoi(e) : 1;
+    }();
+    ly.go = gemm_of(ly.wo, dit_split, 64);
     ly.go.fill_sms = true;
     ly.g1 = gemm_of(ly.w1, 1);
     ly.g1.fill_sms = true;
-    ly.g2 = gemm_of(ly.w2, 1);
+    ly.g2 = gemm_of(ly.w2, dit_split, 64);
     ly.g2.fill_sms = true;
   }
   const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
@@ -476,10 +480,13 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
       // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
       const int ss_ld = d / 128;
-      // Cross-kernel weight pipelining: every kernel prefetches (into L2) a
-      // slice of a LATER GEMM's weights, so HBM keeps streaming through the
-      // kernel boundaries (epilogues, attention, launch gaps).
-      static const uint64_t kPf = [] {  // OMNI_PF_MB: prefetch window, default off (measured slower)
+      // Cross-kernel weight pipelining (OMNI_PF_MB, default off): each decode
+      // GEMM (>= 128 CTAs, so the prefetch is spread over every SM's memory
+      // pipe) pulls the first OMNI_PF_MB of the NEXT GEMM's weights into L2
+      // after issuing its own stream. Small-grid kernels (embed, attention)
+      // never prefetch: a few SMs cannot pull MBs fast (measured: 4 attention
+      // CTAs prefetching 32 MB took 43 us).
+      static const uint64_t kPf = [] {
         const char* e = std::getenv("OMNI_PF_MB");
         return (uint64_t)(e ? std::atoi(e) : 0) << 20;
       }();
@@ -489,10 +496,9 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
         if (off >= n || kPf == 0) return {nullptr, 0};
         return {reinterpret_cast<const char*>(g.ptr) + off, std::min(kPf, n - off)};
       };
-      const auto pf0 = part(st->layers[0].gqkv, 0);
       OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
                              st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld,
-                             pf0.first, pf0.second, s));
+                             nullptr, 0, s));
       GemmEpilogue norm_in;  // fused RMSNorm of the GEMM input
       norm_in.ss_in = st->ss;
       norm_in.ss_ld = ss_ld;
@@ -516,16 +522,14 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
         e.rope.n_layers = L;
         std::tie(e.pf_ptr, e.pf_bytes) = part(ly.go, 0);
         OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
-        const auto pfa = part(ly.ggu, 0);
-        OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, pfa.first,
-                                     pfa.second, s));
+        OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
         GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
         r.out = st->x;
         r.ldo = d;
         r.xb = st->xn;
         r.ss_out = st->ss;
         r.ss_ld = ss_ld;
-        std::tie(r.pf_ptr, r.pf_bytes) = part(ly.ggu, kPf);
+        std::tie(r.pf_ptr, r.pf_bytes) = part(ly.ggu, 0);
         OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, r, s));
         e = norm_in;
         e.out = st->act;
