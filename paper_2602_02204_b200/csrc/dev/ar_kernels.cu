@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   // static weights of a later GEMM (OMNI_PF_MB, default off)
   prefetch_l2_share(pf_ptr, pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y,
                     threadIdx.x, blockDim.x);
-  pdl_wait();
-  pdl_trigger();
+  // The step descriptors come from the H2D copy that completed before the
+  // step's first kernel started, so they are readable before pdl_wait.
   const AttnBlockDesc blk = s.attn_blocks[blockIdx.x];
   const int kh = blockIdx.y;
   const ArEntryDesc ed = s.entries[blk.entry];
@@ -168,6 +168,34 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     mbar_init(&sm.bar[1], 1);
     fence_barrier_init();
   }
+  // KV pages holding only positions < pos0 were written by EARLIER steps:
+  // they stream in before waiting on this step's QKV GEMM (PDL); only the
+  // page(s) receiving this step's K/V rows are loaded after the wait.
+  auto issue = [&](int c, int buf, int part) {  // part 0: history pages (+ expect_tx), 1: the rest
+    const int first = c * kAttnPagesPerChunk;
+    const int keys = min(kAttnChunk, kend - c * kAttnChunk);
+    const int np = (keys + kPageTokens - 1) / kPageTokens;
+    if (part == 0) mbar_expect_tx(&sm.bar[buf], 2u * PAGE_BYTES * np);
+    for (int i = 0; i < np; ++i) {
+      const bool history = (first + i + 1) * kPageTokens <= ed.pos0;
+      if (history != (part == 0)) continue;
+      const int page = s.page_table[blk.entry * s.max_pages + first + i];
+      const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
+      bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
+      bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
+                &sm.bar[buf]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    issue(0, 0, 0);
+    if (n_chunks > 1) issue(1, 1, 0);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    issue(0, 0, 1);
+    if (n_chunks > 1) issue(1, 1, 1);
+  }
   // stage the (pre-scaled) query vectors
   for (int t = threadIdx.x; t < nq * (HD / 2); t += blockDim.x) {
     const int qi = t / (HD / 2), c2 = t % (HD / 2);
@@ -177,24 +205,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     sm.q[qi][c2] = make_float2(__low2float(v) * scale, __high2float(v) * scale);
   }
   __syncthreads();
-
-  auto issue = [&](int c, int buf) {
-    const int first = c * kAttnPagesPerChunk;
-    const int keys = min(kAttnChunk, kend - c * kAttnChunk);
-    const int np = (keys + kPageTokens - 1) / kPageTokens;
-    mbar_expect_tx(&sm.bar[buf], 2u * PAGE_BYTES * np);
-    for (int i = 0; i < np; ++i) {
-      const int page = s.page_table[blk.entry * s.max_pages + first + i];
-      const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
-      bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
-      bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
-                &sm.bar[buf]);
-    }
-  };
-  if (threadIdx.x == 0) {
-    issue(0, 0);
-    if (n_chunks > 1) issue(1, 1);
-  }
 
   constexpr int QW = kAttnQMax / kAttnWarps;  // query vectors per warp
   float m[QW], l[QW], acc[QW][4];
@@ -270,7 +280,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       __syncwarp();
     }
     __syncthreads();  // every warp is done with `buf`
-    if (threadIdx.x == 0 && c + 2 < n_chunks) issue(c + 2, buf);
+    if (threadIdx.x == 0 && c + 2 < n_chunks) {
+      issue(c + 2, buf, 0);
+      issue(c + 2, buf, 1);
+    }
   }
 #pragma unroll
   for (int j = 0; j < QW; ++j) {

@@ -397,18 +397,18 @@ template <int BN>
 constexpr size_t epi_smem_for() {
   return (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
 }
-template <int BN>
+template <int BN, int STAGES = stages_for<BN>()>
 constexpr size_t smem_for() {
-  constexpr size_t pipe = stages_for<BN>() * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
+  constexpr size_t pipe = STAGES * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
   // + barriers / tmem slot (256 B) + per-column input-RMS scales (4 B x BN) + flag
   return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256 + 4 * BN + 16;
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int STAGES = stages_for<BN>()>
 cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                       cudaStream_t st) {
-  auto kern = gemm_tc_kernel<BN, stages_for<BN>(), EPI>;
-  constexpr size_t smem = smem_for<BN>();
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI>;
+  constexpr size_t smem = smem_for<BN, STAGES>();
   static std::atomic<uint64_t> configured{0};  // per instantiation, per device
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
   return launch_k(kern, dim3(w.N_pad / kBlockM, (a.M + BN - 1) / BN, a.splits), dim3(kThreads), smem, st,
@@ -420,6 +420,18 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
                        cudaStream_t st) {
   // compute-bound weights (DiT, fill_sms): the widest token tile that still
   // puts >= one CTA on every SM; the per-element result does not depend on BN
+  static const bool dit2 = [] {  // OMNI_DIT_2CTA=1: shallow rings, 2 CTAs/SM for DiT tiles (experiment)
+    const char* e = std::getenv("OMNI_DIT_2CTA");
+    return e && e[0] == '1';
+  }();
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_GATED_RESID || EPI == EPI_F32) {
+    if (dit2 && w.fill_sms) {
+      switch (bn_for(w, a.M)) {
+        case 64: return launch_bn<64, EPI, 4>(w, x, a, st);
+        default: return launch_bn<128, EPI, 3>(w, x, a, st);  // ~98 KB: 2 CTAs per SM
+      }
+    }
+  }
   switch (bn_for(w, a.M)) {
     case 16: return launch_bn<16, EPI>(w, x, a, st);
     case 32: return launch_bn<32, EPI>(w, x, a, st);

@@ -224,15 +224,19 @@ void build_dit(omni_stage* st) {
     ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
     ly.gqkv = gemm_of(ly.wqkv, 1);
     ly.gqkv.fill_sms = true;
-    static const int dit_split = [] {  // OMNI_DIT_SPLIT: split-K cap of the N=d DiT GEMMs (experiments)
+    static const int dit_split = [] {  // OMNI_DIT_SPLIT: split-K cap of the O projection (experiments)
       const char* e = std::getenv("OMNI_DIT_SPLIT");
+      return e ? std::atoi(e) : 1;
+    }();
+    static const int dit_split2 = [] {  // OMNI_DIT_SPLIT_W2: split-K cap of the MLP-down (K = 4d)
+      const char* e = std::getenv("OMNI_DIT_SPLIT_W2");
       return e ? std::atoi(e) : 1;
     }();
     ly.go = gemm_of(ly.wo, dit_split, 64);
     ly.go.fill_sms = true;
     ly.g1 = gemm_of(ly.w1, 1);
     ly.g1.fill_sms = true;
-    ly.g2 = gemm_of(ly.w2, dit_split, 64);
+    ly.g2 = gemm_of(ly.w2, dit_split2, 64);
     ly.g2.fill_sms = true;
   }
   const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
