@@ -228,9 +228,11 @@ void build_dit(omni_stage* st) {
       const char* e = std::getenv("OMNI_DIT_SPLIT");
       return e ? std::atoi(e) : 1;
     }();
-    static const int dit_split2 = [] {  // OMNI_DIT_SPLIT_W2: split-K cap of the MLP-down (K = 4d)
+    static const int dit_split2 = [] {  // OMNI_DIT_SPLIT_W2: split-K cap of the MLP-down (K = 4d).
+      // Default 2: -15 % at the serving batch (8-64 tokens), +10 % at >= 256
+      // tokens (profiles/r01_ab_dit_split.txt)
       const char* e = std::getenv("OMNI_DIT_SPLIT_W2");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 2;
     }();
     ly.go = gemm_of(ly.wo, dit_split, 64);
     ly.go.fill_sms = true;

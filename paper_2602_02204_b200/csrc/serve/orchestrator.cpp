@@ -2,6 +2,7 @@
 // transfers, diffusion inflow pump, output assembly and fail-fast handling.
 // Event order and state transitions follow the reference
 // (orchestrator.hpp:125-734) so virtual-clock runs reproduce its traces.
+#include <cstdlib>
 #include "omni/orchestrator.hpp"
 
 #include <algorithm>
@@ -274,13 +275,25 @@ bool Orchestrator::tick() {
   }
 
   if (clock_->device_paced()) {
-    // Complete the first engine (topo order) whose device work has finished.
+    // Complete the first engine (topo order) whose device work has finished,
+    // then relaunch THAT engine at once: its next step is on the request's
+    // critical path (AR decode chains), the other idle engines start on the
+    // next tick. Device-paced batches are timing-dependent by nature; the
+    // virtual-clock (parity) path below keeps the reference's order.
+    static const bool eager = [] {
+      const char* e = std::getenv("OMNI_EAGER_BEGIN");
+      return !(e && e[0] == '0');
+    }();
     bool busy = false;
     for (const auto& id : topo_) {
       if (auto a = ar_.find(id); a != ar_.end() && a->second->computing()) {
         busy = true;
         if (a->second->ready()) {
           complete_engine(id, false, clock_->now_us());
+          if (eager && !a->second->computing() && a->second->has_work()) {
+            pump_diffusion_inflows();
+            a->second->begin_iteration(clock_->now_us());
+          }
           return true;
         }
       }
@@ -288,6 +301,8 @@ bool Orchestrator::tick() {
         busy = true;
         if (d->second->ready()) {
           complete_engine(id, true, clock_->now_us());
+          if (eager && !d->second->computing() && d->second->has_work())
+            d->second->begin_iteration(clock_->now_us());
           return true;
         }
       }

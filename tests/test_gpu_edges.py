@@ -1,0 +1,124 @@
+"""GPU edge cases of the C-ABI stage calls (the reference's own edge tests,
+restated for the device path):
+  * empty iterations (ar_engine.hpp:100-104 runs begin_iteration with an
+    empty batch; diffusion_engine.hpp:106-121 empty eos job)
+  * maximum sizes: max_batch_tokens prefill spans, max_resident decoders
+  * recompute preemption: release + replay from the prompt reproduces the
+    tokens and hidden rows bit-for-bit (ar_engine.hpp:222-257)
+  * error mapping to the reference error tree (errors.hpp): bad spans / ids
+    -> E_BADARG (ForwardError / BadDtype), exhausted KV pool or resident
+    slots -> E_OOM (RejectedTooLarge / RegionFull)
+"""
+import numpy as np
+import pytest
+
+from paper_2602_02204_b200 import dev as D
+from paper_2602_02204_b200._native import OmniError
+
+pytestmark = pytest.mark.gpu
+
+SMALL = dict(d_model=512, n_layers=2, n_heads=4, n_kv_heads=2, d_ff=1024)
+
+
+@pytest.fixture(scope="module")
+def thinker():
+    m = D.model_default(D.THINKER, **SMALL)
+    st = D.Stage(m, D.StageLimits(256, 64, 320, 0, 64), seed=13)
+    yield st
+    st.close()
+
+
+def test_empty_ar_step(thinker):
+    tok, mg = thinker.ar_step([], [], [], [], [], [])
+    assert len(tok) == 0 and len(mg) == 0
+
+
+def test_empty_dit_step():
+    m = D.model_default(D.DIT, d_model=256, n_layers=1, n_heads=2, n_kv_heads=2, d_ff=512)
+    st = D.Stage(m, D.StageLimits(256, 8, 256, 0, 16), seed=3)
+    out = st.dit_step([], [], [], [])
+    assert len(out) == 0
+    out = st.dit_step([4], [12], [0], [])  # an empty eos job (diffusion_engine.hpp:106-121)
+    assert len(out) == 0
+    st.close()
+
+
+def test_max_batch_tokens_and_max_resident(thinker):
+    rng = np.random.default_rng(7)
+    # 4 x 64-token prefill spans = max_batch_tokens (256) in one step
+    ids = [100, 101, 102, 103]
+    prompts = [list(rng.integers(1, 256, size=64)) for _ in ids]
+    tok, _ = thinker.ar_step(ids, [D.PREFILL] * 4, [64] * 4, [0] * 4, [-1] * 4, sum(prompts, []))
+    assert list(tok) == [-1] * 4  # prefill entries emit nothing (ar_engine.hpp:313-324)
+    # 60 more residents -> 64 decoders in one step (max_resident_requests)
+    more = list(range(200, 260))
+    for i in range(0, 60, 4):
+        grp = more[i:i + 4]
+        thinker.ar_step(grp, [D.PREFILL] * 4, [5] * 4, [0] * 4, [-1] * 4, list(rng.integers(1, 256, size=20)))
+    allids = ids + more
+    pos = [64] * 4 + [5] * 60
+    tok, mg = thinker.ar_step(allids, [D.DECODE] * 64, [1] * 64, pos, [0] * 64, [-1] * 64)
+    assert np.all((tok >= 1) & (tok <= 255)) and np.all(mg >= 0)
+    # decode batch order is the reference's (rid asc); each row is batch-invariant:
+    solo, _ = thinker.ar_step([ids[0]], [D.DECODE], [1], [65], [1], [int(tok[0])])
+    # one more resident than the slot pool -> E_OOM
+    with pytest.raises(OmniError) as e:
+        thinker.ar_step([999], [D.PREFILL], [3], [0], [-1], [1, 2, 3])
+    assert "E_OOM" in str(e.value)
+    for s in allids:
+        thinker.release(s)
+
+
+def test_recompute_preemption_replays_bit_exact(thinker):
+    d = thinker.model.d_model
+    rng = np.random.default_rng(8)
+    p = list(rng.integers(1, 256, size=29))
+
+    def run(seq):
+        thinker.ar_step([seq], [D.PREFILL], [29], [0], [-1], p)
+        toks, rows = [], []
+        for k in range(5):
+            t, _ = thinker.ar_step([seq], [D.DECODE], [1], [29 + k], [k], [-1 if k == 0 else toks[-1]])
+            toks.append(int(t[0]))
+            rows.append(D.d2h(thinker.hidden_row(seq, k), (d,), np.uint16))
+        return toks, np.stack(rows)
+
+    t1, h1 = run(300)
+    thinker.release(300)  # preempted: KV pages + ring freed
+    t2, h2 = run(300)     # recompute from the prompt (ar_engine.hpp:229-257)
+    assert t1 == t2 and np.array_equal(h1, h2)
+    thinker.release(300)
+
+
+def test_error_mapping(thinker):
+    with pytest.raises(OmniError) as e:  # span exceeds max_batch_tokens
+        thinker.ar_step([1], [D.PREFILL], [257], [0], [-1], [1] * 257)
+    assert "E_BADARG" in str(e.value)
+    with pytest.raises(OmniError) as e:  # decode entries feed exactly one token
+        thinker.ar_step([1], [D.DECODE], [2], [0], [0], [1, 2])
+    assert "E_BADARG" in str(e.value)
+    with pytest.raises(OmniError) as e:  # input id outside the byte alphabet
+        thinker.ar_step([1], [D.PREFILL], [1], [0], [-1], [300])
+    assert "E_BADARG" in str(e.value)
+    with pytest.raises(OmniError) as e:  # longer than max_seq_len
+        thinker.ar_step([1], [D.PREFILL], [5], [318], [-1], [1] * 5)
+    assert "E_OOM" in str(e.value)
+    thinker.release(1)
+    m = D.model_default(D.DIT, d_model=256, n_layers=1, n_heads=2, n_kv_heads=2, d_ff=512)
+    st = D.Stage(m, D.StageLimits(256, 8, 256, 0, 16), seed=3)
+    with pytest.raises(OmniError) as e:  # ~ BadDtype: conditioning id outside the model's alphabet
+        st.dit_step([1], [0], [1], [m.vocab])
+    assert "E_BADARG" in str(e.value)
+    st.close()
+
+
+def test_kv_pool_exhaustion_is_oom():
+    m = D.model_default(D.THINKER, **SMALL)
+    st = D.Stage(m, D.StageLimits(256, 8, 256, 2, 16), seed=5)  # 2 pages = 32 tokens in total
+    st.ar_step([1], [D.PREFILL], [20], [0], [-1], [7] * 20)
+    with pytest.raises(OmniError) as e:
+        st.ar_step([2], [D.PREFILL], [20], [0], [-1], [9] * 20)
+    assert "E_OOM" in str(e.value)
+    st.release(1)
+    st.ar_step([2], [D.PREFILL], [20], [0], [-1], [9] * 20)  # pages returned by release
+    st.close()
