@@ -294,12 +294,18 @@ def main() -> None:
     }
     stage = {
         "thinker": {"steps": last["steps_thinker"], "device_ms": round(last["dev_ms_thinker"], 1),
+                    "host_us_per_step": round(1e3 * last["host_ms_thinker"] / max(1, last["steps_thinker"]), 1),
+                    "gap_us": round(last["gap_us_thinker"], 1),
                     "us_per_step": round(1e3 * last["dev_ms_thinker"] / max(1, last["steps_thinker"]), 1),
                     "weight_GBps": round(ar_bytes["thinker"] * last["steps_thinker"] / max(1e-9, last["dev_ms_thinker"] * 1e-3) / 1e9, 1)},
         "talker": {"steps": last["steps_talker"], "device_ms": round(last["dev_ms_talker"], 1),
+                   "host_us_per_step": round(1e3 * last["host_ms_talker"] / max(1, last["steps_talker"]), 1),
+                   "gap_us": round(last["gap_us_talker"], 1),
                    "us_per_step": round(1e3 * last["dev_ms_talker"] / max(1, last["steps_talker"]), 1),
                    "weight_GBps": round(ar_bytes["talker"] * last["steps_talker"] / max(1e-9, last["dev_ms_talker"] * 1e-3) / 1e9, 1)},
         "code2wav": {"steps": last["steps_dit"], "device_ms": round(last["dev_ms_dit"], 1),
+                     "host_us_per_step": round(1e3 * last["host_ms_dit"] / max(1, last["steps_dit"]), 1),
+                     "gap_us": round(last["gap_us_dit"], 1),
                      "us_per_step": round(1e3 * last["dev_ms_dit"] / max(1, last["steps_dit"]), 1)},
     }
     out = {

@@ -59,6 +59,10 @@ typedef struct omni_bench_result {
   uint64_t output_digest; /* FNV-1a over every request's (text, codec, waveform) */
   uint64_t preemptions;
   double wall_s;
+  /* host cost of driving each stage: ms spent inside the step launches, and
+     the mean gap (us) from collecting a step's results to launching the next */
+  double host_ms_thinker, host_ms_talker, host_ms_dit;
+  double gap_us_thinker, gap_us_talker, gap_us_dit;
 } omni_bench_result;
 
 /* Runs one full workload through a fresh Orchestrator on the pipeline. */

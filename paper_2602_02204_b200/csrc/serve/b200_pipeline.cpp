@@ -14,6 +14,7 @@
 #include "omni/b200_pipeline.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <unordered_map>
 
 #include "omni/errors.hpp"
@@ -78,6 +79,34 @@ class Arena {
   std::unordered_map<uint64_t, std::vector<std::pair<uint64_t, uint64_t>>> owned_;
 };
 
+// Host-side cost of driving a stage: wall time inside launch() (descriptor
+// build + C-ABI step call) and the gap from "previous step's results
+// collected" to "next step launched" (control-plane latency on the chain).
+struct HostTimer {
+  using clk = std::chrono::steady_clock;
+  double host_ms = 0, gap_ms = 0;
+  uint64_t gaps = 0;
+  clk::time_point t_ready{};
+  bool have_ready = false;
+  struct Scope {
+    HostTimer& h;
+    clk::time_point t0;
+    explicit Scope(HostTimer& x) : h(x), t0(clk::now()) {
+      if (h.have_ready) {
+        h.gap_ms += std::chrono::duration<double, std::milli>(t0 - h.t_ready).count();
+        ++h.gaps;
+        h.have_ready = false;
+      }
+    }
+    ~Scope() { h.host_ms += std::chrono::duration<double, std::milli>(clk::now() - t0).count(); }
+  };
+  void ready() {
+    t_ready = clk::now();
+    have_ready = true;
+  }
+  void reset() { host_ms = gap_ms = 0, gaps = 0, have_ready = false; }
+};
+
 struct ArStage {
   std::string name;
   int kind = OMNI_MODEL_THINKER;
@@ -95,6 +124,7 @@ struct ArStage {
   bool in_flight = false;
   double dev_ms = 0;
   uint64_t steps = 0;
+  HostTimer ht;
   // deferred packs of the current iteration
   struct Pack {
     uint64_t rid;
@@ -109,6 +139,7 @@ struct ArStage {
   }
 
   void launch(std::vector<BatchSlot>& slots) {
+    HostTimer::Scope hs(ht);
     const size_t n = slots.size();
     seq_id.resize(n);
     phase.resize(n);
@@ -179,6 +210,7 @@ struct ArStage {
 
   void collect(std::vector<BatchSlot>& slots, std::vector<int32_t>& out) {
     dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    ht.ready();
     in_flight = false;
     float us = 0;
     omni_stage_last_step_us(st, &us);
@@ -239,10 +271,12 @@ struct DitStage {
   std::vector<int32_t> off, ntok, tokens, samples;
   double dev_ms = 0;
   uint64_t steps = 0;
+  HostTimer ht;
   ~DitStage() {
     if (st) omni_stage_destroy(st);
   }
   void launch(const std::vector<DiffusionJob>& jobs) {
+    HostTimer::Scope hs(ht);
     rid.clear();
     off.clear();
     ntok.clear();
@@ -273,6 +307,7 @@ struct DitStage {
   }
   std::vector<Payload> collect() {
     dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    ht.ready();
     float us = 0;
     omni_stage_last_step_us(st, &us);
     dev_ms += us / 1e3;
@@ -402,6 +437,12 @@ std::map<std::string, double> B200Pipeline::device_ms() const {
   for (const auto& [n, s] : impl_->dit) m[n] = s->dev_ms;
   return m;
 }
+std::map<std::string, std::pair<double, double>> B200Pipeline::host_ms() const {
+  std::map<std::string, std::pair<double, double>> m;
+  for (const auto& [n, s] : impl_->ar) m[n] = {s->ht.host_ms, s->ht.gaps ? s->ht.gap_ms / s->ht.gaps : 0.0};
+  for (const auto& [n, s] : impl_->dit) m[n] = {s->ht.host_ms, s->ht.gaps ? s->ht.gap_ms / s->ht.gaps : 0.0};
+  return m;
+}
 std::map<std::string, uint64_t> B200Pipeline::step_counts() const {
   std::map<std::string, uint64_t> m;
   for (const auto& [n, s] : impl_->ar) m[n] = s->steps;
@@ -417,8 +458,8 @@ uint64_t B200Pipeline::weight_bytes() const {
   return t;
 }
 void B200Pipeline::reset_counters() {
-  for (auto& [_, s] : impl_->ar) s->dev_ms = 0, s->steps = 0;
-  for (auto& [_, s] : impl_->dit) s->dev_ms = 0, s->steps = 0;
+  for (auto& [_, s] : impl_->ar) s->dev_ms = 0, s->steps = 0, s->ht.reset();
+  for (auto& [_, s] : impl_->dit) s->dev_ms = 0, s->steps = 0, s->ht.reset();
 }
 
 void B200Pipeline::register_into(FunctionRegistry& reg) {

@@ -213,6 +213,14 @@ omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* s, omni
     r->steps_thinker = get(st, "thinker_forward") + get(st, "ar_forward");
     r->steps_talker = get(st, "talker_forward");
     r->steps_dit = get(st, "denoise") + get(st, "dit_image");
+    const auto hm = p->dev->host_ms();
+    auto hget = [&](const char* k) { auto it = hm.find(k); return it == hm.end() ? std::pair<double, double>{0, 0} : it->second; };
+    r->host_ms_thinker = hget("thinker_forward").first + hget("ar_forward").first;
+    r->host_ms_talker = hget("talker_forward").first;
+    r->host_ms_dit = hget("denoise").first + hget("dit_image").first;
+    r->gap_us_thinker = 1e3 * std::max(hget("thinker_forward").second, hget("ar_forward").second);
+    r->gap_us_talker = 1e3 * hget("talker_forward").second;
+    r->gap_us_dit = 1e3 * std::max(hget("denoise").second, hget("dit_image").second);
     p->csv = rep.csv;
     p->trace = std::move(tracer.out);
   });

@@ -47,6 +47,8 @@ class B200Pipeline {
   // Device milliseconds spent in steps, per stage kind (diagnostics).
   std::map<std::string, double> device_ms() const;
   std::map<std::string, uint64_t> step_counts() const;
+  // per stage: (host ms inside launches, mean ms from result collection to next launch)
+  std::map<std::string, std::pair<double, double>> host_ms() const;
   uint64_t weight_bytes() const;
   void reset_counters();
 

@@ -27,7 +27,9 @@ class BenchResult(C.Structure):
                 ("wave_samples", C.c_uint64), ("dev_ms_thinker", C.c_double), ("dev_ms_talker", C.c_double),
                 ("dev_ms_dit", C.c_double), ("steps_thinker", C.c_uint64), ("steps_talker", C.c_uint64),
                 ("steps_dit", C.c_uint64), ("output_digest", C.c_uint64), ("preemptions", C.c_uint64),
-                ("wall_s", C.c_double)]
+                ("wall_s", C.c_double),
+                ("host_ms_thinker", C.c_double), ("host_ms_talker", C.c_double), ("host_ms_dit", C.c_double),
+                ("gap_us_thinker", C.c_double), ("gap_us_talker", C.c_double), ("gap_us_dit", C.c_double)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
