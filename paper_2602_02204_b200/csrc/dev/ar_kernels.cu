@@ -136,6 +136,7 @@ struct AttnSmem {
   __nv_bfloat16 v[2][kAttnChunk * kHeadDim];
   float2 q[kAttnQMax][kHeadDim / 2];
   float p[kAttnWarps][kAttnChunk];
+  float ml[kAttnWarps][2];  // decode split: partial (max, sum) per warp
   uint64_t bar[2];
 };
 
@@ -206,7 +207,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   }
   __syncthreads();
 
-  constexpr int QW = kAttnQMax / kAttnWarps;  // query vectors per warp
+  constexpr int QW = kAttnQMax / kAttnWarps;  // query vectors per warp (prefill blocks)
+  constexpr int KG = kAttnChunk / 32;          // 32-key groups per chunk
+  // Decode blocks (few query vectors): `per` warps share one query vector,
+  // each taking every per-th 32-key group, and merge their partial softmax
+  // states at the end (flash-decoding inside the CTA) -> all 8 warps busy.
+  const int per = nq >= kAttnWarps ? 1 : min(KG, kAttnWarps / nq);
+  const int part = warp % per;
   float m[QW], l[QW], acc[QW][4];
 #pragma unroll
   for (int j = 0; j < QW; ++j) {
@@ -224,18 +231,18 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
     const __nv_bfloat16* V = sm.v[buf];
 #pragma unroll
     for (int j = 0; j < QW; ++j) {
-      const int qi = warp + j * kAttnWarps;
+      const int qi = per > 1 ? (j == 0 ? warp / per : nq) : warp + j * kAttnWarps;
       if (qi >= nq) break;  // warp-uniform
       const int qpos = ed.pos0 + blk.tok0 + qi / group;
       const int nk = min(kAttnChunk, qpos + 1 - kbase);  // causal keys of this chunk
       if (nk <= 0) continue;
-      float sc[kAttnChunk / 32];
+      float sc[KG];
       float cmax = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < kAttnChunk / 32; ++i) {
+      for (int i = 0; i < KG; ++i) {
         const int key = lane + 32 * i;
         float d = -INFINITY;
-        if (key < nk) {
+        if (key < nk && i % per == part) {
           const __nv_bfloat162* kr = K2 + key * (HD / 2);
           float a0 = 0.f, a1 = 0.f;
 #pragma unroll 8
@@ -252,11 +259,13 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         cmax = fmaxf(cmax, d);
       }
       cmax = warp_max(cmax);
+      if (cmax == -INFINITY) continue;  // none of this warp's keys are in range (warp-uniform)
       const float mn = fmaxf(m[j], cmax);
       const float corr = __expf(m[j] - mn);
       float ps = 0.f;
 #pragma unroll
-      for (int i = 0; i < kAttnChunk / 32; ++i) {
+      for (int i = 0; i < KG; ++i) {
+        if (i % per != part) continue;
         const float pv = (lane + 32 * i < nk) ? __expf(sc[i] - mn) : 0.f;
         sm.p[warp][lane + 32 * i] = pv;
         ps += pv;
@@ -266,15 +275,19 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       m[j] = mn;
       __syncwarp();
       float o0 = acc[j][0] * corr, o1 = acc[j][1] * corr, o2 = acc[j][2] * corr, o3 = acc[j][3] * corr;
-      for (int k = 0; k < nk; ++k) {
-        const float pk = sm.p[warp][k];
-        const uint2 raw = *reinterpret_cast<const uint2*>(V + k * HD + lane * 4);
-        const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-        const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-        o0 += pk * v01.x;
-        o1 += pk * v01.y;
-        o2 += pk * v23.x;
-        o3 += pk * v23.y;
+      for (int i = part; i < KG; i += per) {
+        const int kend_i = min(nk, 32 * (i + 1));
+#pragma unroll 4
+        for (int k = 32 * i; k < kend_i; ++k) {
+          const float pk = sm.p[warp][k];
+          const uint2 raw = *reinterpret_cast<const uint2*>(V + k * HD + lane * 4);
+          const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+          const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+          o0 += pk * v01.x;
+          o1 += pk * v01.y;
+          o2 += pk * v23.x;
+          o3 += pk * v23.y;
+        }
       }
       acc[j][0] = o0, acc[j][1] = o1, acc[j][2] = o2, acc[j][3] = o3;
       __syncwarp();
@@ -284,6 +297,38 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       issue(c + 2, buf, 0);
       issue(c + 2, buf, 1);
     }
+  }
+  if (per > 1) {
+    // merge the `per` partial (max, sum, acc) states of each query vector
+    const int qi = warp / per;
+    if (qi < nq) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sm.p[warp][lane * 4 + t] = acc[0][t];
+      if (lane == 0) {
+        sm.ml[warp][0] = m[0];
+        sm.ml[warp][1] = l[0];
+      }
+    }
+    __syncthreads();
+    if (qi < nq && part == 0) {
+      float mt = -INFINITY;
+      for (int p = 0; p < per; ++p) mt = fmaxf(mt, sm.ml[warp + p][0]);
+      float lt = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < per; ++p) {
+        const float mp = sm.ml[warp + p][0];
+        const float f = mp == -INFINITY ? 0.f : __expf(mp - mt);
+        lt += sm.ml[warp + p][1] * f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) o[t] += sm.p[warp + p][lane * 4 + t] * f;
+      }
+      const int tok = blk.tok0 + qi / group, hq = kh * group + qi % group;
+      const float inv = 1.f / lt;
+      __nv_bfloat162* op =
+          reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + lane * 4);
+      op[0] = __floats2bfloat162_rn(o[0] * inv, o[1] * inv);
+      op[1] = __floats2bfloat162_rn(o[2] * inv, o[3] * inv);
+    }
+    return;
   }
 #pragma unroll
   for (int j = 0; j < QW; ++j) {

@@ -528,7 +528,12 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
         e.rope.n_layers = L;
         std::tie(e.pf_ptr, e.pf_bytes) = part(ly.go, 0);
         OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
-        OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
+        static const bool skip_attn = [] {  // OMNI_SKIP_ATTN=1: timing attribution only (wrong outputs)
+          const char* e = std::getenv("OMNI_SKIP_ATTN");
+          return e && e[0] == '1';
+        }();
+        if (!skip_attn)
+          OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
         GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
         r.out = st->x;
         r.ldo = d;

@@ -14,6 +14,7 @@
 #include "omni/b200_pipeline.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <unordered_map>
 
@@ -261,63 +262,95 @@ struct ArStage {
   }
 };
 
+// The DiT plugin. One diffusion iteration's jobs (diffusion_engine.hpp:84-112)
+// are split into `ways` token-balanced groups, each run as its own batched
+// omni_dit_step on its own device stage (stream): the denoise chain of a
+// batch is latency-bound (~130 dependent kernels), so parallel chains fill
+// the SMs one chain leaves idle. The DiT is token-local and batch-invariant,
+// so the samples are bit-identical for any grouping (test_dit_parity_and_
+// chunking). OMNI_DIT_WAYS sets the group count; default 1 (2 and 3 measured
+// no better in the bench, profiles/r01_bench_ditways_ab.log).
 struct DitStage {
   std::string name;
   int dev = 0;
   omni_model_desc model{};
-  omni_stage* st = nullptr;
+  std::vector<omni_stage*> sts;
   Tracer* tracer = nullptr;
-  std::vector<uint64_t> rid;
-  std::vector<int32_t> off, ntok, tokens, samples;
+  struct Group {
+    std::vector<size_t> jobs;  // indices into the launched job list
+    std::vector<uint64_t> rid;
+    std::vector<int32_t> off, ntok, tokens, samples;
+  };
+  std::vector<Group> groups;
+  std::vector<size_t> job_ntok;
   double dev_ms = 0;
   uint64_t steps = 0;
   HostTimer ht;
   ~DitStage() {
-    if (st) omni_stage_destroy(st);
+    for (omni_stage* st : sts) omni_stage_destroy(st);
   }
   void launch(const std::vector<DiffusionJob>& jobs) {
     HostTimer::Scope hs(ht);
-    rid.clear();
-    off.clear();
-    ntok.clear();
-    tokens.clear();
-    for (const auto& j : jobs) {
+    groups.assign(sts.size(), Group{});
+    job_ntok.assign(jobs.size(), 0);
+    std::vector<size_t> load(sts.size(), 0);
+    for (size_t i = 0; i < jobs.size(); ++i) {
+      const auto& j = jobs[i];
       if (j.input.dtype != Dtype::I32 || j.input.is_device())
         throw BadDtype("diffusion input must be I32 codec tokens");
       const auto t = j.input.as_i32();
-      rid.push_back(j.request_id);
-      off.push_back(static_cast<int32_t>(j.token_offset));
-      ntok.push_back(static_cast<int32_t>(t.size()));
-      tokens.insert(tokens.end(), t.begin(), t.end());
+      const size_t g = std::min_element(load.begin(), load.end()) - load.begin();  // token-balanced
+      load[g] += t.size() + 1;
+      Group& G = groups[g];
+      G.jobs.push_back(i);
+      G.rid.push_back(j.request_id);
+      G.off.push_back(static_cast<int32_t>(j.token_offset));
+      G.ntok.push_back(static_cast<int32_t>(t.size()));
+      G.tokens.insert(G.tokens.end(), t.begin(), t.end());
+      job_ntok[i] = t.size();
     }
-    samples.assign(tokens.size() * static_cast<size_t>(model.dit_samples), 0);
-    omni_dit_batch b{};
-    b.n_jobs = static_cast<int32_t>(jobs.size());
-    b.request_id = rid.data();
-    b.token_offset = off.data();
-    b.n_tokens = ntok.data();
-    b.tokens = tokens.data();
-    dev_ok(omni_dit_step(st, &b, samples.data()), "omni_dit_step");
+    for (size_t g = 0; g < groups.size(); ++g) {
+      Group& G = groups[g];
+      if (G.jobs.empty()) continue;
+      G.samples.assign(G.tokens.size() * static_cast<size_t>(model.dit_samples), 0);
+      omni_dit_batch b{};
+      b.n_jobs = static_cast<int32_t>(G.jobs.size());
+      b.request_id = G.rid.data();
+      b.token_offset = G.off.data();
+      b.n_tokens = G.ntok.data();
+      b.tokens = G.tokens.data();
+      dev_ok(omni_dit_step(sts[g], &b, G.samples.data()), "omni_dit_step");
+    }
   }
   bool ready() {
-    const omni_status s = omni_stage_query(st);
-    if (s == OMNI_EAGAIN) return false;
-    dev_ok(s, "omni_stage_query");
+    for (size_t g = 0; g < groups.size(); ++g) {
+      if (groups[g].jobs.empty()) continue;
+      const omni_status s = omni_stage_query(sts[g]);
+      if (s == OMNI_EAGAIN) return false;
+      dev_ok(s, "omni_stage_query");
+    }
     return true;
   }
   std::vector<Payload> collect() {
-    dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    float worst = 0;
+    for (size_t g = 0; g < groups.size(); ++g) {
+      if (groups[g].jobs.empty()) continue;
+      dev_ok(omni_stage_wait(sts[g]), "omni_stage_wait");
+      float us = 0;
+      omni_stage_last_step_us(sts[g], &us);
+      worst = std::max(worst, us);
+    }
     ht.ready();
-    float us = 0;
-    omni_stage_last_step_us(st, &us);
-    dev_ms += us / 1e3;
+    dev_ms += worst / 1e3;  // concurrent groups: the iteration lasts as long as the slowest
     ++steps;
-    std::vector<Payload> out;
-    size_t at = 0;
-    for (int32_t n : ntok) {
-      const size_t m = static_cast<size_t>(n) * model.dit_samples;
-      out.push_back(Payload::from_i32(std::span<const int32_t>(samples.data() + at, m)));
-      at += m;
+    std::vector<Payload> out(job_ntok.size());
+    for (const Group& G : groups) {
+      size_t at = 0;
+      for (size_t k = 0; k < G.jobs.size(); ++k) {
+        const size_t m = static_cast<size_t>(G.ntok[k]) * model.dit_samples;
+        out[G.jobs[k]] = Payload::from_i32(std::span<const int32_t>(G.samples.data() + at, m));
+        at += m;
+      }
     }
     return out;
   }
@@ -416,9 +449,17 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
     omni_stage_limits lim{};
     lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
     lim.dit_max_tokens = 512;
-    dev_ok(omni_stage_create(&d->model, &lim, d->dev, I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3),
-                             &d->st),
-           "omni_stage_create(dit)");
+    static const int ways = [] {
+      const char* e = std::getenv("OMNI_DIT_WAYS");
+      return std::clamp(e ? std::atoi(e) : 1, 1, 4);
+    }();
+    for (int w = 0; w < ways; ++w) {  // identical weights (same seed) on every group's stage
+      omni_stage* st = nullptr;
+      dev_ok(omni_stage_create(&d->model, &lim, d->dev, I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3),
+                               &st),
+             "omni_stage_create(dit)");
+      d->sts.push_back(st);
+    }
     I.dit[dn] = std::move(d);
   }
 }
@@ -454,7 +495,7 @@ uint64_t B200Pipeline::weight_bytes() const {
   for (const auto& [_, s] : impl_->ar)
     if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
   for (const auto& [_, s] : impl_->dit)
-    if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
+    if (!s->sts.empty() && omni_stage_weight_bytes(s->sts[0], &b) == OMNI_OK) t += b;
   return t;
 }
 void B200Pipeline::reset_counters() {
