@@ -129,6 +129,12 @@ typedef struct omni_ar_batch {
  * omni_stage_query. PREFILL entries emit nothing (ar_engine.hpp:313-324). */
 omni_status omni_ar_step(omni_stage* st, const omni_ar_batch* batch, int32_t* token_out,
                          float* margin_out);
+/* Execution mode of small AR steps (<= 16 token rows): 1 (default) runs the
+ * whole step as ONE "step chain" launch (work items with device-side
+ * dependency counters), 0 as the per-kernel PDL chain. Results are
+ * bit-identical; the switch exists for A/B measurement and tests. */
+omni_status omni_stage_set_chain(omni_stage* st, int32_t on);
+
 /* Frees the KV pages / hidden ring / conditioning rows of a sequence
  * (finish, recompute-preemption ar_engine.hpp:233-257, or failure). */
 omni_status omni_seq_release(omni_stage* st, uint64_t seq_id);

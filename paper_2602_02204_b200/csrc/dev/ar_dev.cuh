@@ -1,0 +1,399 @@
+// Device bodies of the non-GEMM AR step kernels, shared by the per-kernel
+// launches (ar_kernels.cu) and the one-launch step chain (chain.cu). Each
+// takes its work index explicitly and a `Dep` functor that performs the wait
+// on the producer of its inputs (griddepcontrol.wait for PDL launches, the
+// chain's completion counters inside the step-chain kernel). Internal.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "ar_kernels.h"
+#include "ptx.cuh"
+
+namespace omni_dev {
+
+struct PdlDep {
+  __device__ __forceinline__ void operator()() const {
+    pdl_wait();
+    pdl_trigger();
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Embedding.  Thinker: x = E[tok].  Talker prefill token j:
+//   cond_j = E_t[tok] + (W_h h_j) (precomputed GEMM rows in `hproj`), stored
+//   to the sequence's conditioning table, x = cond_j.  Talker decode step m:
+//   x = E_c[prev] + cond_{m/4}.
+// Also emits the first layer's fused-RMSNorm inputs: xb = bf16(x) and the
+// per-128-feature sums of squares ss[row][tile] (same fixed 16-lane order as
+// the EPI_RESID_NORM GEMM epilogue).
+// ---------------------------------------------------------------------------
+template <class Dep>
+__device__ __forceinline__ void embed_row(int r, const ArStepDev& s, const __nv_bfloat16* __restrict__ emb,
+                             const __nv_bfloat16* __restrict__ emb2, const float* __restrict__ hproj,
+                             float* __restrict__ cond_table, int cond_rows, int d, int start_id,
+                             float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                             float* __restrict__ ss_out, int ss_ld, Dep dep) {
+  dep();
+  const ArRowDesc rd = s.rows[r];
+  const ArEntryDesc ed = s.entries[rd.entry];
+  const int tok = rd.token < 0 ? start_id : rd.token;
+  float* xr = x + (size_t)r * d;
+  const int mode = emb2 == nullptr ? 0 : (ed.is_decode ? 2 : 1);
+  float* cond = mode ? cond_table + ((size_t)ed.slot * cond_rows + rd.cond_row) * d : nullptr;
+  const __nv_bfloat16* e = mode == 2 ? emb2 + (size_t)tok * d : emb + (size_t)tok * d;
+  for (int base = 0; base < d; base += blockDim.x * 8) {
+    const int i0 = base + threadIdx.x * 8;
+    const bool live = i0 < d;
+    float ss = 0.f;
+    if (live) {
+      float v[8];
+      const uint4 raw = *reinterpret_cast<const uint4*>(e + i0);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 f = __bfloat1622float2(h2[k]);
+        v[2 * k] = f.x, v[2 * k + 1] = f.y;
+      }
+      if (mode == 1) {
+        const float* hp = hproj + (size_t)r * d + i0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += hp[k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cond[i0 + k] = v[k];
+      } else if (mode == 2) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] += cond[i0 + k];
+      }
+      uint4 ob;
+      __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&ob);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o2[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      *reinterpret_cast<uint4*>(xb + (size_t)r * d + i0) = ob;
+      reinterpret_cast<float4*>(xr + i0)[0] = make_float4(v[0], v[1], v[2], v[3]);
+      reinterpret_cast<float4*>(xr + i0)[1] = make_float4(v[4], v[5], v[6], v[7]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss += v[k] * v[k];
+    }
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (live && (threadIdx.x & 15) == 0) ss_out[(size_t)r * ss_ld + i0 / 128] = ss;
+  }
+}
+
+// Talker: gather the upstream FIX16 hidden rows (2-byte aligned inside the
+// packed connector payload) into an aligned bf16 GEMM input.
+template <class Dep>
+__device__ __forceinline__ void gather_cond_row(int r, const ArStepDev& s, int d, __nv_bfloat16* __restrict__ out,
+                                                Dep dep) {
+  dep();
+  const uint64_t src = s.rows[r].cond_src;
+  __nv_bfloat16* o = out + (size_t)r * d;
+  if (src == 0) {
+    for (int i = threadIdx.x; i < d; i += blockDim.x) o[i] = __float2bfloat16_rn(0.f);
+    return;
+  }
+  const unsigned short* p = reinterpret_cast<const unsigned short*>(src);
+  unsigned short* q = reinterpret_cast<unsigned short*>(o);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) q[i] = p[i];
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) t += red[i];  // fixed order: deterministic
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Paged causal attention (K3). Grid (query block, kv_head), 8 warps.
+// A query block is up to kAttnQTok tokens of one entry (decode: 1 token) and
+// holds their `group` query heads that share the KV head. The block's causal
+// context [0, pos0 + tok0 + ntok) is staged into smem in 128-key chunks by
+// 1-D bulk TMA copies of whole 16-token pages (double buffered, one mbarrier
+// per chunk). Each warp owns query vectors; QK^T has lanes split KEYS (rotated
+// column order -> conflict-free smem), the chunk softmax merges online, P.V
+// has lanes split the 128 head dims.
+// ---------------------------------------------------------------------------
+constexpr int kAttnQMax = kAttnQTok * 8;  // query vectors per block (group <= 8)
+
+template <int kAttnWarps, int kAttnChunk>
+struct AttnSmem {
+  __nv_bfloat16 k[2][kAttnChunk * kHeadDim];
+  __nv_bfloat16 v[2][kAttnChunk * kHeadDim];
+  float2 q[kAttnQMax][kHeadDim / 2];
+  float p[kAttnWarps][kAttnChunk];
+  float ml[kAttnWarps][2];  // decode split: partial (max, sum) per warp
+  float mrg[kAttnWarps][kHeadDim];  // decode split: partial P.V rows per warp
+  uint64_t bar[2];
+};
+
+template <int kAttnWarps, int kAttnChunk, class Dep>
+__device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const ArStepDev& s,
+                                                const __nv_bfloat16* __restrict__ q, int n_heads, int n_kv,
+                                                int layer, int n_layers, const __nv_bfloat16* __restrict__ kv,
+                                                __nv_bfloat16* __restrict__ out, float scale,
+                                                AttnSmem<kAttnWarps, kAttnChunk>& sm, Dep dep) {
+  constexpr int HD = kHeadDim;
+  constexpr uint32_t PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB K or V slice of one page
+  constexpr int kAttnPagesPerChunk = kAttnChunk / kPageTokens;
+  // The step descriptors come from the H2D copy that completed before the
+  // step's first kernel started, so they are readable before pdl_wait.
+  const AttnBlockDesc blk = s.attn_blocks[blk_idx];
+  const int kh = kh_idx;
+  const ArEntryDesc ed = s.entries[blk.entry];
+  const int group = n_heads / n_kv;
+  const int nq = blk.ntok * group;
+  const int kend = ed.pos0 + blk.tok0 + blk.ntok;  // causal context of the block
+  const int n_chunks = (kend + kAttnChunk - 1) / kAttnChunk;
+  const int warp = warp_id(), lane = lane_id();
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_barrier_init();
+  }
+  // KV pages holding only positions < pos0 were written by EARLIER steps:
+  // they stream in before waiting on this step's QKV GEMM (PDL); only the
+  // page(s) receiving this step's K/V rows are loaded after the wait.
+  auto issue = [&](int c, int buf, int part) {  // part 0: history pages (+ expect_tx), 1: the rest
+    const int first = c * kAttnPagesPerChunk;
+    const int keys = min(kAttnChunk, kend - c * kAttnChunk);
+    const int np = (keys + kPageTokens - 1) / kPageTokens;
+    if (part == 0) mbar_expect_tx(&sm.bar[buf], 2u * PAGE_BYTES * np);
+    for (int i = 0; i < np; ++i) {
+      const bool history = (first + i + 1) * kPageTokens <= ed.pos0;
+      if (history != (part == 0)) continue;
+      const int page = s.page_table[blk.entry * s.max_pages + first + i];
+      const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
+      bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
+      bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
+                &sm.bar[buf]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    issue(0, 0, 0);
+    if (n_chunks > 1) issue(1, 1, 0);
+  }
+  dep();
+  if (threadIdx.x == 0) {
+    issue(0, 0, 1);
+    if (n_chunks > 1) issue(1, 1, 1);
+  }
+  // stage the (pre-scaled) query vectors
+  for (int t = threadIdx.x; t < nq * (HD / 2); t += blockDim.x) {
+    const int qi = t / (HD / 2), c2 = t % (HD / 2);
+    const int tok = blk.tok0 + qi / group, hq = kh * group + qi % group;
+    const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(
+        q + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD)[c2];
+    sm.q[qi][c2] = make_float2(__low2float(v) * scale, __high2float(v) * scale);
+  }
+  __syncthreads();
+
+  constexpr int QW = kAttnQMax / kAttnWarps;  // query vectors per warp (prefill blocks)
+  constexpr int KG = kAttnChunk / 32;          // 32-key groups per chunk
+  // Decode blocks (few query vectors): `per` warps share one query vector,
+  // each taking every per-th 32-key group, and merge their partial softmax
+  // states at the end (flash-decoding inside the CTA) -> all 8 warps busy.
+  const int per = nq >= kAttnWarps ? 1 : min(KG, kAttnWarps / nq);
+  const int part = warp % per;
+  float m[QW], l[QW], acc[QW][4];
+#pragma unroll
+  for (int j = 0; j < QW; ++j) {
+    m[j] = -INFINITY;
+    l[j] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) acc[j][t] = 0.f;
+  }
+
+  for (int c = 0; c < n_chunks; ++c) {
+    const int buf = c & 1;
+    mbar_wait(&sm.bar[buf], (c >> 1) & 1);
+    const int kbase = c * kAttnChunk;
+    const __nv_bfloat162* K2 = reinterpret_cast<const __nv_bfloat162*>(sm.k[buf]);
+    const __nv_bfloat16* V = sm.v[buf];
+#pragma unroll
+    for (int j = 0; j < QW; ++j) {
+      const int qi = per > 1 ? (j == 0 ? warp / per : nq) : warp + j * kAttnWarps;
+      if (qi >= nq) break;  // warp-uniform
+      const int qpos = ed.pos0 + blk.tok0 + qi / group;
+      const int nk = min(kAttnChunk, qpos + 1 - kbase);  // causal keys of this chunk
+      if (nk <= 0) continue;
+      float sc[KG];
+      float cmax = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < KG; ++i) {
+        const int key = lane + 32 * i;
+        float d = -INFINITY;
+        if (key < nk && i % per == part) {
+          const __nv_bfloat162* kr = K2 + key * (HD / 2);
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+          for (int cp = 0; cp < HD / 2; ++cp) {
+            const int x = (cp + lane) & (HD / 2 - 1);  // rotated: distinct banks per lane
+            const float2 kv2 = __bfloat1622float2(kr[x]);
+            const float2 qv = sm.q[qi][x];
+            a0 += qv.x * kv2.x;
+            a1 += qv.y * kv2.y;
+          }
+          d = a0 + a1;
+        }
+        sc[i] = d;
+        cmax = fmaxf(cmax, d);
+      }
+      cmax = warp_max(cmax);
+      if (cmax == -INFINITY) continue;  // none of this warp's keys are in range (warp-uniform)
+      const float mn = fmaxf(m[j], cmax);
+      const float corr = __expf(m[j] - mn);
+      float ps = 0.f;
+#pragma unroll
+      for (int i = 0; i < KG; ++i) {
+        if (i % per != part) continue;
+        const float pv = (lane + 32 * i < nk) ? __expf(sc[i] - mn) : 0.f;
+        sm.p[warp][lane + 32 * i] = pv;
+        ps += pv;
+      }
+      ps = warp_sum(ps);
+      l[j] = l[j] * corr + ps;
+      m[j] = mn;
+      __syncwarp();
+      float o0 = acc[j][0] * corr, o1 = acc[j][1] * corr, o2 = acc[j][2] * corr, o3 = acc[j][3] * corr;
+      for (int i = part; i < KG; i += per) {
+        const int kend_i = min(nk, 32 * (i + 1));
+#pragma unroll 4
+        for (int k = 32 * i; k < kend_i; ++k) {
+          const float pk = sm.p[warp][k];
+          const uint2 raw = *reinterpret_cast<const uint2*>(V + k * HD + lane * 4);
+          const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+          const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+          o0 += pk * v01.x;
+          o1 += pk * v01.y;
+          o2 += pk * v23.x;
+          o3 += pk * v23.y;
+        }
+      }
+      acc[j][0] = o0, acc[j][1] = o1, acc[j][2] = o2, acc[j][3] = o3;
+      __syncwarp();
+    }
+    __syncthreads();  // every warp is done with `buf`
+    if (threadIdx.x == 0 && c + 2 < n_chunks) {
+      issue(c + 2, buf, 0);
+      issue(c + 2, buf, 1);
+    }
+  }
+  if (per > 1) {
+    // merge the `per` partial (max, sum, acc) states of each query vector
+    const int qi = warp / per;
+    if (qi < nq) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) sm.mrg[warp][lane * 4 + t] = acc[0][t];
+      if (lane == 0) {
+        sm.ml[warp][0] = m[0];
+        sm.ml[warp][1] = l[0];
+      }
+    }
+    __syncthreads();
+    if (qi < nq && part == 0) {
+      float mt = -INFINITY;
+      for (int p = 0; p < per; ++p) mt = fmaxf(mt, sm.ml[warp + p][0]);
+      float lt = 0.f, o[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int p = 0; p < per; ++p) {
+        const float mp = sm.ml[warp + p][0];
+        const float f = mp == -INFINITY ? 0.f : __expf(mp - mt);
+        lt += sm.ml[warp + p][1] * f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) o[t] += sm.mrg[warp + p][lane * 4 + t] * f;
+      }
+      const int tok = blk.tok0 + qi / group, hq = kh * group + qi % group;
+      const float inv = 1.f / lt;
+      __nv_bfloat162* op =
+          reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + lane * 4);
+      op[0] = __floats2bfloat162_rn(o[0] * inv, o[1] * inv);
+      op[1] = __floats2bfloat162_rn(o[2] * inv, o[3] * inv);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < QW; ++j) {
+    const int qi = warp + j * kAttnWarps;
+    if (qi >= nq) break;
+    const int tok = blk.tok0 + qi / group, hq = kh * group + qi % group;
+    const float inv = 1.f / l[j];
+    __nv_bfloat162* op = reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + lane * 4);
+    op[0] = __floats2bfloat162_rn(acc[j][0] * inv, acc[j][1] * inv);
+    op[1] = __floats2bfloat162_rn(acc[j][2] * inv, acc[j][3] * inv);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Final norm of DECODE rows -> compact hidden rows (+ hidden ring for the
+// thinker, row `out_index` of the sequence's slot).
+// ---------------------------------------------------------------------------
+template <class Dep>
+__device__ __forceinline__ void final_gather_row(int di, const ArStepDev& s, const float* __restrict__ x, int d,
+                                                 float eps, __nv_bfloat16* __restrict__ hout,
+                                                 __nv_bfloat16* __restrict__ ring, int ring_rows, float* red,
+                                                 Dep dep) {
+  dep();
+  const int e = s.dec_entries[di];
+  const ArEntryDesc ed = s.entries[e];
+  const float* xr = x + (size_t)ed.row0 * d;  // decode entries have exactly one row
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+  const float tot = block_sum(ss, red);
+  const float inv = rsqrtf(tot / d + eps);
+  __nv_bfloat16* h = hout + (size_t)di * d;
+  __nv_bfloat16* rg = ring ? ring + ((size_t)ed.slot * ring_rows + ed.out_index) * d : nullptr;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const __nv_bfloat16 v = f2bf(xr[i] * inv);
+    h[i] = v;
+    if (rg) rg[i] = v;
+  }
+}
+
+// Greedy id over [lo, hi) of the logits row; ties -> lowest id. Also the
+// top-2 margin used by the teacher-forced parity rule.
+// One warp (lanes 0-31 of the block) per row.
+template <class Dep>
+__device__ __forceinline__ void argmax_row(int r, const float* __restrict__ logits, int ld, int lo, int hi,
+                                           int* __restrict__ tok_out, float* __restrict__ margin_out, Dep dep) {
+  dep();
+  if (threadIdx.x >= 32) return;
+  const float* row = logits + (size_t)r * ld;
+  float b1 = -INFINITY, b2 = -INFINITY;
+  int i1 = 0x7fffffff;
+  for (int i = lo + threadIdx.x; i < hi; i += 32) {
+    const float v = row[i];
+    if (v > b1 || (v == b1 && i < i1)) {
+      b2 = b1;
+      b1 = v;
+      i1 = i;
+    } else if (v > b2) {
+      b2 = v;
+    }
+  }
+  // warp merge (blockDim == 32)
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
+    const float ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+    const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+    if (ob1 > b1 || (ob1 == b1 && oi1 < i1)) {
+      b2 = fmaxf(b1, ob2);
+      b1 = ob1;
+      i1 = oi1;
+    } else {
+      b2 = fmaxf(b2, ob1);
+    }
+  }
+  if (threadIdx.x == 0) {
+    tok_out[r] = i1;
+    margin_out[r] = b1 - b2;
+  }
+}
+
+}  // namespace omni_dev

@@ -119,5 +119,9 @@ bool gemm_make_weight(GemmWeight& w, const __nv_bfloat16* ptr, int N, int N_pad,
 bool gemm_make_input(GemmInput& x, const __nv_bfloat16* ptr, int rows_cap, int K);
 cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi,
                      const GemmEpilogue& e, cudaStream_t st);
+// Validates (w, x, M, epi, e) and fills the kernel argument block (the step
+// chain, chain.cu, launches GEMM tiles itself).
+cudaError_t gemm_make_args(const GemmWeight& w, const GemmInput& x, int M, int epi, const GemmEpilogue& e,
+                           GemmArgs& a);
 
 }  // namespace omni_dev

@@ -190,6 +190,29 @@ void build_ar(omni_stage* st) {
   st->rope = dev_alloc<float2>(st, rt.size());
   OMNI_CUDA(cudaMemcpyAsync(st->rope, rt.data(), rt.size() * sizeof(float2), cudaMemcpyHostToDevice,
                             st->stream));
+  // step-chain resources (chain.cu): TMA descriptors in global memory, op
+  // completion counters, split-K workspace (tile slots reused across layers)
+  {
+    std::vector<CUtensorMap> maps;
+    for (const auto& ly : st->layers) maps.insert(maps.end(), {ly.gqkv.tmap, ly.go.tmap, ly.ggu.tmap, ly.gd.tmap});
+    maps.push_back(st->glm.tmap);
+    maps.push_back(talker ? st->ghid.tmap : st->glm.tmap);
+    maps.push_back(st->in_xn.tmaps[0]);
+    maps.push_back(st->in_attn.tmaps[0]);
+    maps.push_back(st->in_act.tmaps[0]);
+    maps.push_back(st->in_hbuf.tmaps[0]);
+    maps.push_back(talker ? st->in_cond.tmaps[0] : st->in_xn.tmaps[0]);
+    st->chain_maps = dev_alloc<CUtensorMap>(st, maps.size());
+    OMNI_CUDA(cudaMemcpyAsync(st->chain_maps, maps.data(), maps.size() * sizeof(CUtensorMap),
+                              cudaMemcpyHostToDevice, st->stream));
+    const auto& l0 = st->layers[0];
+    st->chain_ws_tiles = (talker ? st->ghid.N_pad / 128 : 0) + (l0.gqkv.N_pad + l0.go.N_pad + l0.ggu.N_pad +
+                                                                  l0.gd.N_pad + st->glm.N_pad) / 128;
+    st->chain_ws = dev_alloc<float>(st, (size_t)st->chain_ws_tiles * kChainMaxSplits * 16 * 128);
+    st->chain_tile_cnt = dev_alloc<int>(st, st->chain_ws_tiles);
+    OMNI_CUDA(cudaMemsetAsync(st->chain_tile_cnt, 0, st->chain_ws_tiles * sizeof(int), st->stream));
+    st->chain_done = dev_alloc<int>(st, kChainMaxOps + 1);
+  }
   OMNI_CUDA(cudaMallocHost(&st->h_tok, R * sizeof(int32_t)));
   OMNI_CUDA(cudaMallocHost(&st->h_margin, R * sizeof(float)));
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
@@ -378,6 +401,145 @@ void run_graph(omni_stage* st, uint64_t key, F&& body) {
   counters().launches += it->second.nodes;
 }
 
+// The whole AR step as one launch (chain.cu): the same ops, epilogues and
+// split-K factors as the per-kernel path below, as an op table.
+void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_blocks, int n_dec, bool cond) {
+  const auto& m = st->m;
+  const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
+  const bool talker = m.kind == OMNI_MODEL_TALKER;
+  ChainParams P{};
+  P.sd = sd;
+  P.maps = st->chain_maps;
+  P.done = st->chain_done;
+  P.ticket = st->chain_done + kChainMaxOps;
+  P.ws = st->chain_ws;
+  P.tile_cnt = st->chain_tile_cnt;
+  P.emb = st->emb.p;
+  P.emb2 = talker ? st->emb2.p : nullptr;
+  P.hproj = st->hproj;
+  P.cond_table = st->cond_table;
+  P.cond_rows = st->cond_rows;
+  P.d = d;
+  P.start_id = st->start_id;
+  P.x = st->x;
+  P.xb = st->xn;
+  P.ss = st->ss;
+  P.ss_ld = d / 128;
+  P.cond_dim = m.cond_dim;
+  P.condin = st->condin;
+  P.q = st->q;
+  P.n_heads = H;
+  P.n_kv = KVH;
+  P.n_layers = L;
+  P.kv = st->kv;
+  P.attn = st->attn;
+  P.attn_scale = 1.0f / std::sqrt((float)kHeadDim);
+  P.eps = kNormEps;
+  P.hbuf = st->hbuf;
+  P.ring = talker ? nullptr : st->ring;
+  P.ring_rows = st->ring_rows;
+  P.logits = st->logits;
+  P.vocab_pad = st->vocab_pad;
+  P.argmax_lo = st->argmax_lo;
+  P.argmax_hi = st->argmax_hi;
+  P.tok = st->d_tok;
+  P.margin = st->d_margin;
+  int total = 0;
+  auto add = [&](ChainOp op) {
+    OMNI_REQUIRE(P.n_ops < kChainMaxOps, OMNI_E_BADARG, "step chain: too many ops");
+    if (op.n_items <= 0) return;
+    op.first = total;
+    total += op.n_items;
+    P.ops[P.n_ops++] = op;
+  };
+  auto simple = [&](int kind, int items) {
+    ChainOp op{};
+    op.kind = kind;
+    op.n_items = op.units = items;
+    return op;
+  };
+  // split-K workspace tile slots: one range per GEMM position, reused by every layer
+  const auto& l0 = st->layers[0];
+  const int slot_ghid = 0;
+  const int slot_qkv = talker ? st->ghid.N_pad / 128 : 0;
+  const int slot_o = slot_qkv + l0.gqkv.N_pad / 128;
+  const int slot_gu = slot_o + l0.go.N_pad / 128;
+  const int slot_d = slot_gu + l0.ggu.N_pad / 128;
+  const int slot_lm = slot_d + l0.gd.N_pad / 128;
+  auto gemm = [&](const GemmWeight& w, int w_map, int x_map, const GemmInput& xin, int M, int epi,
+                  const GemmEpilogue& e, int slot) {
+    ChainOp op{};
+    op.kind = CHAIN_GEMM;
+    OMNI_CUDA(gemm_make_args(w, xin, M, epi, e, op.a));
+    op.w_map = w_map;
+    op.x_map = x_map;
+    op.epi = epi;
+    op.n_tiles = w.N_pad / 128;
+    op.splits = w.splits;
+    op.kb_per = (w.K / 64) / w.splits;
+    op.n_items = op.n_tiles * op.splits;
+    op.units = op.n_tiles;
+    op.ws_tile0 = slot;
+    add(op);
+  };
+  const int mx = 4 * L + 2;  // input descriptor indices: xn, attn, act, hbuf, cond
+  if (cond) {
+    add(simple(CHAIN_GATHER_COND, n_rows));
+    GemmEpilogue e;
+    e.out = st->hproj;
+    e.ldo = d;
+    gemm(st->ghid, 4 * L + 1, mx + 4, st->in_cond, n_rows, EPI_F32, e, slot_ghid);
+  }
+  add(simple(CHAIN_EMBED, n_rows));
+  GemmEpilogue norm_in;
+  norm_in.ss_in = st->ss;
+  norm_in.ss_ld = d / 128;
+  norm_in.ss_n = d / 128;
+  norm_in.norm_d = (float)d;
+  norm_in.norm_eps = kNormEps;
+  for (int l = 0; l < L; ++l) {
+    const auto& ly = st->layers[l];
+    GemmEpilogue e = norm_in;
+    e.out = st->q;
+    e.ldo = H * kHeadDim;
+    e.rope.rows = sd.rows;
+    e.rope.page_table = sd.page_table;
+    e.rope.max_pages = sd.max_pages;
+    e.rope.table = st->rope;
+    e.rope.q_out = st->q;
+    e.rope.kv = st->kv;
+    e.rope.n_heads = H;
+    e.rope.n_kv = KVH;
+    e.rope.layer = l;
+    e.rope.n_layers = L;
+    gemm(ly.gqkv, 4 * l + 0, mx + 0, st->in_xn, n_rows, EPI_ROPE_KV, e, slot_qkv);
+    ChainOp at = simple(CHAIN_ATTN, n_blocks * KVH);
+    at.layer = l;
+    add(at);
+    GemmEpilogue r;
+    r.out = st->x;
+    r.ldo = d;
+    r.xb = st->xn;
+    r.ss_out = st->ss;
+    r.ss_ld = d / 128;
+    gemm(ly.go, 4 * l + 1, mx + 1, st->in_attn, n_rows, EPI_RESID_NORM, r, slot_o);
+    e = norm_in;
+    e.out = st->act;
+    e.ldo = m.d_ff;
+    gemm(ly.ggu, 4 * l + 2, mx + 0, st->in_xn, n_rows, EPI_SWIGLU, e, slot_gu);
+    gemm(ly.gd, 4 * l + 3, mx + 2, st->in_act, n_rows, EPI_RESID_NORM, r, slot_d);
+  }
+  if (n_dec > 0) {
+    add(simple(CHAIN_FINAL, n_dec));
+    GemmEpilogue e;
+    e.out = st->logits;
+    e.ldo = st->vocab_pad;
+    gemm(st->glm, 4 * L, mx + 3, st->in_hbuf, n_dec, EPI_F32, e, slot_lm);
+    add(simple(CHAIN_ARGMAX, n_dec));
+  }
+  OMNI_KERNEL(chain_launch(P, total, st->stream));
+}
+
 void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* margin_out) {
   ensure_idle(st);
   const int ne = b->n_entries;
@@ -475,7 +637,9 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   if (n_rows > 0) {
     const uint64_t key = ((uint64_t)n_rows << 40) | ((uint64_t)n_blocks << 20) | ((uint64_t)n_dec << 1) |
                          (talker && n_prefill_rows > 0 ? 1u : 0u);
-    run_graph(st, key, [&] {
+    if (st->chain_on && n_rows <= chain_max_rows()) {
+      run_graph(st, key, [&] { launch_step_chain(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0); });
+    } else run_graph(st, key, [&] {
       if (talker && n_prefill_rows > 0) {
         OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
         GemmEpilogue e;
@@ -784,6 +948,8 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     st->lim = *limits;
     st->dev = dev;
     st->seed = weight_seed;
+    const char* ce = std::getenv("OMNI_CHAIN");  // OMNI_CHAIN=0: per-kernel PDL path for every step
+    st->chain_on = !(ce && ce[0] == '0');
     if (st->lim.max_batch_tokens <= 0) st->lim.max_batch_tokens = 256;
     if (st->lim.max_resident <= 0) st->lim.max_resident = 64;
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;
@@ -812,6 +978,15 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
   });
   if (rc != OMNI_OK && st) destroy_stage(st);
   return rc;
+}
+
+omni_status omni_stage_set_chain(omni_stage* st, int32_t on) {
+  return guarded([&] {
+    OMNI_REQUIRE(st != nullptr, OMNI_E_BADARG, "null stage");
+    ensure_idle(st);
+    if (st->chain_on != (on != 0)) drop_graphs(st);  // cached step graphs bake the mode in
+    st->chain_on = on != 0;
+  });
 }
 
 omni_status omni_stage_destroy(omni_stage* st) {
@@ -845,12 +1020,33 @@ omni_status omni_stage_tensor(const omni_stage* st, const char* name, uint64_t* 
       if (cols) *cols = st->m.dit_channels;
       return;
     }
+    if (n == "buf.hproj" && st->hproj) {
+      *dev_ptr = reinterpret_cast<uint64_t>(st->hproj);
+      if (rows) *rows = st->rows_cap;
+      if (cols) *cols = st->m.d_model;
+      return;
+    }
     if (n == "buf.x") {
       *dev_ptr = reinterpret_cast<uint64_t>(st->x);
       if (rows) *rows = st->rows_cap;
       if (cols) *cols = st->m.d_model;
       return;
     }
+    // bf16 activations of the last step (debug / tests): name -> (ptr, cols)
+    const std::pair<const char*, std::pair<const void*, int64_t>> bf[] = {
+        {"buf.xn", {st->xn, st->m.d_model}},
+        {"buf.q", {st->q, (int64_t)st->m.n_heads * kHeadDim}},
+        {"buf.attn", {st->attn, (int64_t)st->m.n_heads * kHeadDim}},
+        {"buf.act", {st->act, st->m.d_ff}},
+        {"buf.hbuf", {st->hbuf, st->m.d_model}},
+        {"buf.ss", {st->ss, st->m.d_model / 128}}};
+    for (const auto& [nm, pc] : bf)
+      if (n == nm && pc.first) {
+        *dev_ptr = reinterpret_cast<uint64_t>(pc.first);
+        if (rows) *rows = st->rows_cap;
+        if (cols) *cols = pc.second;
+        return;
+      }
     throw DevError(OMNI_E_BADARG, "unknown tensor " + n);
   });
 }

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "ar_kernels.h"
+#include "chain.h"
 #include "dit_kernels.h"
 #include "gemm.h"
 #include "omni_dev.h"
@@ -116,5 +117,12 @@ struct omni_stage {
   int64_t pending_samples = 0;
   float last_step_us = 0.f;
   std::unordered_map<uint64_t, omni_dev::StepGraph> graphs;  // step graphs by launch geometry
+  // step chain (chain.cu): global TMA descriptors, counters, split-K workspace
+  CUtensorMap* chain_maps = nullptr;
+  int* chain_done = nullptr;
+  float* chain_ws = nullptr;
+  int* chain_tile_cnt = nullptr;
+  int chain_ws_tiles = 0;
+  bool chain_on = true;  // small steps (rows <= 16) run as one step-chain launch
 
 };

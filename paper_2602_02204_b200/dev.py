@@ -88,6 +88,9 @@ class Stage:
         check(self.lib.omni_stage_tensor(self.h, name.encode(), C.byref(p), C.byref(r), C.byref(c)))
         return p.value, r.value, c.value
 
+    def set_chain(self, on: bool) -> None:
+        check(self.lib.omni_stage_set_chain(self.h, 1 if on else 0))
+
     def weight_bytes(self) -> int:
         b = C.c_uint64()
         check(self.lib.omni_stage_weight_bytes(self.h, C.byref(b)))

@@ -122,3 +122,51 @@ def test_kv_pool_exhaustion_is_oom():
     st.release(1)
     st.ar_step([2], [D.PREFILL], [20], [0], [-1], [9] * 20)  # pages returned by release
     st.close()
+
+
+@pytest.mark.parametrize("kind", [D.THINKER, D.TALKER])
+def test_step_chain_bit_identical_to_kernel_chain(kind):
+    """The one-launch step chain (chain.cu) and the per-kernel PDL path give
+    bit-identical tokens and hidden rows (same tiles, same split-K order)."""
+    kw = dict(SMALL)
+    if kind == D.TALKER:
+        kw["cond_dim"] = 512
+    m = D.model_default(kind, **kw)
+    rng = np.random.default_rng(11)
+    prompts = {s: list(rng.integers(1, 256, size=n)) for s, n in ((1, 9), (2, 14), (3, 5))}
+    outs = []
+    for chain in (True, False):
+        st = D.Stage(m, D.StageLimits(256, 16, 256, 0, 16), seed=17)
+        st.set_chain(chain)
+        cond = None
+        if kind == D.TALKER:
+            cond = D.mem_alloc(2 * 512 * 16)
+            bits = ((rng.standard_normal(512 * 16).astype(np.float32) * 0.5).view(np.uint32) >> 16).astype(np.uint16)
+            D.h2d(cond, bits)
+        for s, p in prompts.items():
+            if kind == D.TALKER:
+                st.ar_step([s], [D.PREFILL], [len(p)], [0], [-1], p,
+                           cond_src=[cond + 2 * 512 * (j % 16) for j in range(len(p))],
+                           cond_row=list(range(len(p))))
+            else:
+                st.ar_step([s], [D.PREFILL], [len(p)], [0], [-1], p)
+        seqs = sorted(prompts)
+        toks = {s: [] for s in seqs}
+        hids = []
+        for k in range(4):
+            tin = [-1 if k == 0 else toks[s][-1] for s in seqs]
+            pos = [len(prompts[s]) + k for s in seqs]
+            extra = dict(cond_src=[0] * 3, cond_row=[k // 4] * 3) if kind == D.TALKER else {}
+            t, mg = st.ar_step(seqs, [D.DECODE] * 3, [1] * 3, pos, [k] * 3, tin, **extra)
+            for i, s in enumerate(seqs):
+                toks[s].append(int(t[i]))
+            if kind == D.THINKER:
+                hids.append(np.stack([D.d2h(st.hidden_row(s, k), (512,), np.uint16) for s in seqs]))
+            else:
+                lg = D.d2h(st.tensor("buf.logits")[0], (3, st.tensor("buf.logits")[2]), np.float32)
+                hids.append(lg[:, :m.vocab])  # columns >= vocab are padding (never written)
+        outs.append((toks, hids))
+        st.close()
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
