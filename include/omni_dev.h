@@ -129,11 +129,17 @@ typedef struct omni_ar_batch {
  * omni_stage_query. PREFILL entries emit nothing (ar_engine.hpp:313-324). */
 omni_status omni_ar_step(omni_stage* st, const omni_ar_batch* batch, int32_t* token_out,
                          float* margin_out);
-/* Execution mode of small AR steps (<= 16 token rows): 1 (default) runs the
- * whole step as ONE "step chain" launch (work items with device-side
- * dependency counters), 0 as the per-kernel PDL chain. Results are
- * bit-identical; the switch exists for A/B measurement and tests. */
+/* Execution mode of small Thinker steps (<= 16 token rows): 1 runs the whole
+ * step as ONE "step chain" launch (cluster-ticketed work items with
+ * device-side dependency counters), 0 (default) as the per-kernel PDL chain.
+ * Results are bit-identical; the switch exists for A/B measurement. */
 omni_status omni_stage_set_chain(omni_stage* st, int32_t on);
+
+/* Tools: record {start, dependency met, end} globaltimer ns per work item of
+ * subsequent step-chain launches into trace_dev (3 x u64 per item; 0 = off);
+ * returns the item / op counts and op start tickets of the LAST chain launch. */
+omni_status omni_stage_chain_trace(omni_stage* st, uint64_t trace_dev, int32_t* n_items, int32_t* n_ops,
+                                   int32_t* op_first);
 
 /* Frees the KV pages / hidden ring / conditioning rows of a sequence
  * (finish, recompute-preemption ar_engine.hpp:233-257, or failure). */

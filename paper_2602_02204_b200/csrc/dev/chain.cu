@@ -15,10 +15,10 @@
 // wait, and leave the wait ~1 us after op o's last tile signals, instead of
 // paying a grid completion + dependent launch per op.
 //
-// GEMM items are BN = 16 tiles (decode / small steps, rows <= 16); split-K
-// partials go to a global workspace and the LAST split of a tile reduces all
-// partials in split order (same fp32 order as the cluster reduction of the
-// per-kernel path -> bit-identical outputs). Replaces the same reference
+// The grid runs in clusters of 8 CTAs; a cluster takes one ticket (8 items).
+// GEMM items are BN = 16 tiles (decode / small steps, rows <= 16) and the S
+// splits of a tile sit in one cluster and reduce over DSMEM in rank order
+// (same fp32 order as the per-kernel path -> bit-identical outputs). Replaces the same reference
 // functions as the per-kernel path: ArEngine::run_batch / StageModel hooks
 // (ar_engine.hpp:308-337, registry.hpp:79-89).
 #include <cuda.h>
@@ -48,6 +48,7 @@ constexpr uint32_t kABytes = kBlockM * kBlockK * 2;
 constexpr uint32_t kBBytes = kChainBN * kBlockK * 2;
 constexpr size_t kPipeBytes = (size_t)kChainStages * (kABytes + kBBytes);
 constexpr size_t kGemmSmem = 1024 + kPipeBytes + 256 + 4 * kChainBN + 16;
+static_assert(kPipeBytes >= (size_t)kChainBN * 128 * 4 * 3 / 2, "split-K staging fits the ring");
 constexpr size_t kChainSmem = kGemmSmem > sizeof(ChainAttnSmem) + 128 ? kGemmSmem : sizeof(ChainAttnSmem) + 128;
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -61,13 +62,16 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 struct ChainDep {
   const int* cnt;
   int target;
+  unsigned long long* tr;
   __device__ __forceinline__ void spin() const {
-    if (cnt == nullptr) return;
-    int ns = 32;
-    while (ld_acquire(cnt) < target) {
-      __nanosleep(ns);
-      ns = ns < 256 ? ns * 2 : 256;
+    if (cnt != nullptr) {
+      int ns = 32;
+      while (ld_acquire(cnt) < target) {
+        __nanosleep(ns);
+        ns = ns < 256 ? ns * 2 : 256;
+      }
     }
+    if (tr) tr[1] = globaltimer();
   }
   __device__ __forceinline__ void operator()() const {
     if (threadIdx.x == 0) spin();
@@ -83,18 +87,20 @@ __device__ __forceinline__ void signal_done(int* done) {
   }
 }
 
-__device__ __forceinline__ void epi_dispatch(int epi, const GemmArgs& a, int n_tile, int ncols, const float* acc,
-                                             const float* inv) {
+__device__ __forceinline__ void epi_dispatch(int epi, const GemmArgs& a, int n_tile, int tok0, int ncols,
+                                             const float* acc, const float* inv) {
   switch (epi) {
-    case EPI_ROPE_KV: epi_cols<EPI_ROPE_KV>(a, n_tile, 0, ncols, acc, inv); break;
-    case EPI_RESID_NORM: epi_cols<EPI_RESID_NORM>(a, n_tile, 0, ncols, acc, inv); break;
-    case EPI_SWIGLU: epi_cols<EPI_SWIGLU>(a, n_tile, 0, ncols, acc, inv); break;
-    case EPI_F32: epi_cols<EPI_F32>(a, n_tile, 0, ncols, acc, inv); break;
-    default: epi_cols<EPI_BF16>(a, n_tile, 0, ncols, acc, inv); break;
+    case EPI_ROPE_KV: epi_cols<EPI_ROPE_KV>(a, n_tile, tok0, ncols, acc, inv); break;
+    case EPI_RESID_NORM: epi_cols<EPI_RESID_NORM>(a, n_tile, tok0, ncols, acc, inv); break;
+    case EPI_SWIGLU: epi_cols<EPI_SWIGLU>(a, n_tile, tok0, ncols, acc, inv); break;
+    case EPI_F32: epi_cols<EPI_F32>(a, n_tile, tok0, ncols, acc, inv); break;
+    default: epi_cols<EPI_BF16>(a, n_tile, tok0, ncols, acc, inv); break;
   }
 }
 
-// One BN=16 output tile x one K split of a GEMM op.
+// One BN=16 output tile x one K split of a GEMM op. A cluster of 8 CTAs
+// hosts 8/S tiles x S splits (rank r: tile r/S, split r%S); the S splits of
+// a tile reduce over DSMEM in fixed rank order (as gemm_tc.cu does).
 __device__ __forceinline__ void gemm_item(const ChainParams& P, const ChainOp& op, int o, int item,
                                           const ChainDep& dep, uint8_t* smem_raw) {
   constexpr int BN = kChainBN, STAGES = kChainStages;
@@ -114,8 +120,9 @@ __device__ __forceinline__ void gemm_item(const ChainParams& P, const ChainOp& o
 
   const GemmArgs& a = op.a;
   const int warp = warp_id(), lane = lane_id();
-  const int n_tile = item % op.n_tiles, split = item / op.n_tiles;
   const int S = op.splits;
+  const int rank = item % kChainCluster;
+  const int n_tile = (item / kChainCluster) * (kChainCluster / S) + rank / S, split = rank % S;
   const int kb_per = op.kb_per;
   const int kb0 = split * kb_per;
   const CUtensorMap* tmW = P.maps + op.w_map;
@@ -193,48 +200,39 @@ __device__ __forceinline__ void gemm_item(const ChainParams& P, const ChainOp& o
   {
     float v[16];
     tmem_ld16(trow, v);
-    if (S == 1) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) red[j * 128 + row] = v[j];
-    } else {
-      float* wsp = P.ws + ((size_t)(op.ws_tile0 + n_tile) * kChainMaxSplits + split) * (BN * 128);
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < cols) __stcg(wsp + j * 128 + row, v[j]);
-    }
+    for (int j = 0; j < 16; ++j) red[j * 128 + row] = v[j];
   }
-  bool finish = true;
-  if (S > 1) {
-    // the last split to arrive reduces all partials in split order
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      *last = atomicAdd(P.tile_cnt + op.ws_tile0 + n_tile, 1) == S - 1;
-    }
-    __syncthreads();
-    finish = *last != 0;
-    if (finish) {
-      __threadfence();
-      const float* base = P.ws + (size_t)(op.ws_tile0 + n_tile) * kChainMaxSplits * (BN * 128);
-      for (int q = threadIdx.x; q < cols * 32; q += kChainThreads) {
-        const int e4 = q * 4;
-        float4 v[8];
+  if (S == 1) {
+    epi_dispatch(op.epi, a, n_tile, 0, cols, red, inv_s);
+  } else {
+    // ranks [base, base + S) hold the partials of this tile; each reduces a
+    // slice of token columns across them in rank order, then runs the epilogue
+    cluster_sync();
+    const int base = (rank / S) * S;
+    const int per = (cols + S - 1) / S;
+    const int c0 = split * per;
+    const int c1 = min(cols, c0 + per);
+    float* fin = red + BN * 128;
+    const uint32_t red_s = smem_addr(red);
+    const int n4 = (c1 > c0 ? c1 - c0 : 0) * 32;
+    for (int q = threadIdx.x; q < n4; q += kChainThreads) {
+      const int c = c0 + q / 32, r4 = (q % 32) * 4;
+      const uint32_t off = static_cast<uint32_t>((c * 128 + r4) * 4);
+      float4 v[8];
 #pragma unroll
-        for (int z = 0; z < 8; ++z)
-          if (z < S) v[z] = __ldcg(reinterpret_cast<const float4*>(base + (size_t)z * (BN * 128) + e4));
-        float4 acc = v[0];
+      for (int z = 0; z < 8; ++z)
+        if (z < S) v[z] = dsmem_ld_f32x4(dsmem_map(red_s + off, base + z));
+      float4 acc = v[0];
 #pragma unroll
-        for (int z = 1; z < 8; ++z)
-          if (z < S) acc.x += v[z].x, acc.y += v[z].y, acc.z += v[z].z, acc.w += v[z].w;
-        *reinterpret_cast<float4*>(red + e4) = acc;
-      }
-      if (threadIdx.x == 0) P.tile_cnt[op.ws_tile0 + n_tile] = 0;  // re-armed for the next step
+      for (int z = 1; z < 8; ++z)
+        if (z < S) acc.x += v[z].x, acc.y += v[z].y, acc.z += v[z].z, acc.w += v[z].w;
+      *reinterpret_cast<float4*>(fin + (c - c0) * 128 + r4) = acc;
     }
+    if (c1 > c0) epi_dispatch(op.epi, a, n_tile, c0, c1 - c0, fin, inv_s + c0);
+    cluster_sync();  // keep our partial alive until every rank of the tile has read it
   }
-  if (finish) {
-    epi_dispatch(op.epi, a, n_tile, cols, red, inv_s);
-    signal_done(P.done + o);
-  }
+  signal_done(P.done + o);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_free<kTmemCols>(tmem);
@@ -244,14 +242,31 @@ __global__ void __launch_bounds__(kChainThreads, 2) step_chain_kernel(const __gr
   extern __shared__ __align__(1024) uint8_t chain_smem[];
   __shared__ int s_ticket;
   __shared__ float s_red[32];
-  if (threadIdx.x == 0) s_ticket = atomicAdd(P.ticket, 1);
-  __syncthreads();
-  const int t = s_ticket;
+  // one ticket per cluster of 8 CTAs: rank 0 draws it and writes it into
+  // every rank's smem over DSMEM; item = 8 * ticket + rank
+  const uint32_t rank = cluster_rank();
+  if (rank == 0 && threadIdx.x == 0) {
+    const int tc = atomicAdd(P.ticket, 1);
+    const uint32_t loc = smem_addr(&s_ticket);
+    for (uint32_t r = 0; r < kChainCluster; ++r)
+      asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsmem_map(loc, r)), "r"(tc) : "memory");
+  }
+  cluster_sync();
+  const int t = s_ticket * kChainCluster + (int)rank;
+  unsigned long long* tr = P.trace ? P.trace + 3ull * t : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   int o = 0;
   while (o + 1 < P.n_ops && t >= P.ops[o + 1].first) ++o;
   const ChainOp& op = P.ops[o];
   const int item = t - op.first;
-  const ChainDep dep{o > 0 ? P.done + (o - 1) : nullptr, o > 0 ? P.ops[o - 1].units : 0};
+  if (item >= op.n_items) {  // cluster padding
+    if (op.kind == CHAIN_GEMM && op.splits > 1) {  // the split-K reduction syncs the whole cluster
+      cluster_sync();
+      cluster_sync();
+    }
+    return;
+  }
+  const ChainDep dep{o > 0 ? P.done + (o - 1) : nullptr, o > 0 ? P.ops[o - 1].units : 0, tr};
   switch (op.kind) {
     case CHAIN_GEMM:
       gemm_item(P, op, o, item, dep, chain_smem);
@@ -280,6 +295,7 @@ __global__ void __launch_bounds__(kChainThreads, 2) step_chain_kernel(const __gr
       signal_done(P.done + o);
       break;
   }
+  if (tr && threadIdx.x == 0) tr[2] = globaltimer();
 }
 
 }  // namespace
@@ -298,6 +314,13 @@ cudaError_t chain_launch(const ChainParams& P, int n_items, cudaStream_t st) {
   cfg.blockDim = dim3(kChainThreads);
   cfg.dynamicSmemBytes = kChainSmem;
   cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kChainCluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, step_chain_kernel, P);
 }
 

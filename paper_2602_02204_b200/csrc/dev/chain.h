@@ -22,7 +22,8 @@ enum ChainOpKind : int {
 };
 
 constexpr int kChainMaxOps = 48;
-constexpr int kChainMaxSplits = 8;  // workspace stride: partial (tile slot t, split z) at t * 8 + z
+constexpr int kChainMaxSplits = 8;
+constexpr int kChainCluster = 8;  // CTAs per cluster = items per ticket; ops are padded to multiples of 8
 
 struct ChainOp {
   int kind;
@@ -33,7 +34,6 @@ struct ChainOp {
   int w_map, x_map;  // indices into ChainParams::maps
   int epi;
   int n_tiles, splits, kb_per;
-  int ws_tile0;  // first slot of its tiles in the split-K workspace / counters
   // attention
   int layer;
   GemmArgs a;
@@ -44,9 +44,8 @@ struct ChainParams {
   const CUtensorMap* maps;  // global-memory TMA descriptors of the stage
   int* done;                // [kChainMaxOps] completion counters + [1] ticket (zeroed per launch)
   int* ticket;
-  float* ws;                // split-K partials [tile][split][16][128] fp32
-  int* tile_cnt;            // split-K arrival counters (self re-arming)
   int n_ops;
+  unsigned long long* trace;  // optional: per ticket {start, dependency met, end} globaltimer ns
   // embed
   const __nv_bfloat16* emb;
   const __nv_bfloat16* emb2;

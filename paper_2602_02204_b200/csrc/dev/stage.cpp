@@ -191,7 +191,7 @@ void build_ar(omni_stage* st) {
   OMNI_CUDA(cudaMemcpyAsync(st->rope, rt.data(), rt.size() * sizeof(float2), cudaMemcpyHostToDevice,
                             st->stream));
   // step-chain resources (chain.cu): TMA descriptors in global memory, op
-  // completion counters, split-K workspace (tile slots reused across layers)
+  // completion counters
   {
     std::vector<CUtensorMap> maps;
     for (const auto& ly : st->layers) maps.insert(maps.end(), {ly.gqkv.tmap, ly.go.tmap, ly.ggu.tmap, ly.gd.tmap});
@@ -205,12 +205,6 @@ void build_ar(omni_stage* st) {
     st->chain_maps = dev_alloc<CUtensorMap>(st, maps.size());
     OMNI_CUDA(cudaMemcpyAsync(st->chain_maps, maps.data(), maps.size() * sizeof(CUtensorMap),
                               cudaMemcpyHostToDevice, st->stream));
-    const auto& l0 = st->layers[0];
-    st->chain_ws_tiles = (talker ? st->ghid.N_pad / 128 : 0) + (l0.gqkv.N_pad + l0.go.N_pad + l0.ggu.N_pad +
-                                                                  l0.gd.N_pad + st->glm.N_pad) / 128;
-    st->chain_ws = dev_alloc<float>(st, (size_t)st->chain_ws_tiles * kChainMaxSplits * 16 * 128);
-    st->chain_tile_cnt = dev_alloc<int>(st, st->chain_ws_tiles);
-    OMNI_CUDA(cudaMemsetAsync(st->chain_tile_cnt, 0, st->chain_ws_tiles * sizeof(int), st->stream));
     st->chain_done = dev_alloc<int>(st, kChainMaxOps + 1);
   }
   OMNI_CUDA(cudaMallocHost(&st->h_tok, R * sizeof(int32_t)));
@@ -412,8 +406,7 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   P.maps = st->chain_maps;
   P.done = st->chain_done;
   P.ticket = st->chain_done + kChainMaxOps;
-  P.ws = st->chain_ws;
-  P.tile_cnt = st->chain_tile_cnt;
+  P.trace = st->chain_trace;
   P.emb = st->emb.p;
   P.emb2 = talker ? st->emb2.p : nullptr;
   P.hproj = st->hproj;
@@ -445,11 +438,11 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   P.tok = st->d_tok;
   P.margin = st->d_margin;
   int total = 0;
-  auto add = [&](ChainOp op) {
+  auto add = [&](ChainOp op) {  // item ranges padded to whole clusters (one ticket = 8 items)
     OMNI_REQUIRE(P.n_ops < kChainMaxOps, OMNI_E_BADARG, "step chain: too many ops");
     if (op.n_items <= 0) return;
     op.first = total;
-    total += op.n_items;
+    total += (op.n_items + kChainCluster - 1) / kChainCluster * kChainCluster;
     P.ops[P.n_ops++] = op;
   };
   auto simple = [&](int kind, int items) {
@@ -458,16 +451,8 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     op.n_items = op.units = items;
     return op;
   };
-  // split-K workspace tile slots: one range per GEMM position, reused by every layer
-  const auto& l0 = st->layers[0];
-  const int slot_ghid = 0;
-  const int slot_qkv = talker ? st->ghid.N_pad / 128 : 0;
-  const int slot_o = slot_qkv + l0.gqkv.N_pad / 128;
-  const int slot_gu = slot_o + l0.go.N_pad / 128;
-  const int slot_d = slot_gu + l0.ggu.N_pad / 128;
-  const int slot_lm = slot_d + l0.gd.N_pad / 128;
   auto gemm = [&](const GemmWeight& w, int w_map, int x_map, const GemmInput& xin, int M, int epi,
-                  const GemmEpilogue& e, int slot) {
+                  const GemmEpilogue& e) {
     ChainOp op{};
     op.kind = CHAIN_GEMM;
     OMNI_CUDA(gemm_make_args(w, xin, M, epi, e, op.a));
@@ -478,8 +463,8 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     op.splits = w.splits;
     op.kb_per = (w.K / 64) / w.splits;
     op.n_items = op.n_tiles * op.splits;
-    op.units = op.n_tiles;
-    op.ws_tile0 = slot;
+    op.units = op.n_items;  // every split signals after the cluster reduction
+    OMNI_REQUIRE(kChainCluster % op.splits == 0, OMNI_E_BADARG, "step chain: split-K must divide the cluster");
     add(op);
   };
   const int mx = 4 * L + 2;  // input descriptor indices: xn, attn, act, hbuf, cond
@@ -488,7 +473,7 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     GemmEpilogue e;
     e.out = st->hproj;
     e.ldo = d;
-    gemm(st->ghid, 4 * L + 1, mx + 4, st->in_cond, n_rows, EPI_F32, e, slot_ghid);
+    gemm(st->ghid, 4 * L + 1, mx + 4, st->in_cond, n_rows, EPI_F32, e);
   }
   add(simple(CHAIN_EMBED, n_rows));
   GemmEpilogue norm_in;
@@ -512,7 +497,7 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     e.rope.n_kv = KVH;
     e.rope.layer = l;
     e.rope.n_layers = L;
-    gemm(ly.gqkv, 4 * l + 0, mx + 0, st->in_xn, n_rows, EPI_ROPE_KV, e, slot_qkv);
+    gemm(ly.gqkv, 4 * l + 0, mx + 0, st->in_xn, n_rows, EPI_ROPE_KV, e);
     ChainOp at = simple(CHAIN_ATTN, n_blocks * KVH);
     at.layer = l;
     add(at);
@@ -522,21 +507,24 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     r.xb = st->xn;
     r.ss_out = st->ss;
     r.ss_ld = d / 128;
-    gemm(ly.go, 4 * l + 1, mx + 1, st->in_attn, n_rows, EPI_RESID_NORM, r, slot_o);
+    gemm(ly.go, 4 * l + 1, mx + 1, st->in_attn, n_rows, EPI_RESID_NORM, r);
     e = norm_in;
     e.out = st->act;
     e.ldo = m.d_ff;
-    gemm(ly.ggu, 4 * l + 2, mx + 0, st->in_xn, n_rows, EPI_SWIGLU, e, slot_gu);
-    gemm(ly.gd, 4 * l + 3, mx + 2, st->in_act, n_rows, EPI_RESID_NORM, r, slot_d);
+    gemm(ly.ggu, 4 * l + 2, mx + 0, st->in_xn, n_rows, EPI_SWIGLU, e);
+    gemm(ly.gd, 4 * l + 3, mx + 2, st->in_act, n_rows, EPI_RESID_NORM, r);
   }
   if (n_dec > 0) {
     add(simple(CHAIN_FINAL, n_dec));
     GemmEpilogue e;
     e.out = st->logits;
     e.ldo = st->vocab_pad;
-    gemm(st->glm, 4 * L, mx + 3, st->in_hbuf, n_dec, EPI_F32, e, slot_lm);
+    gemm(st->glm, 4 * L, mx + 3, st->in_hbuf, n_dec, EPI_F32, e);
     add(simple(CHAIN_ARGMAX, n_dec));
   }
+  st->chain_last_items = total;
+  st->chain_last_nops = P.n_ops;
+  for (int i = 0; i < P.n_ops; ++i) st->chain_last_first[i] = P.ops[i].first;
   OMNI_KERNEL(chain_launch(P, total, st->stream));
 }
 
@@ -637,7 +625,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   if (n_rows > 0) {
     const uint64_t key = ((uint64_t)n_rows << 40) | ((uint64_t)n_blocks << 20) | ((uint64_t)n_dec << 1) |
                          (talker && n_prefill_rows > 0 ? 1u : 0u);
-    if (st->chain_on && n_rows <= chain_max_rows()) {
+    if (st->chain_on && !talker && n_rows <= chain_max_rows()) {
       run_graph(st, key, [&] { launch_step_chain(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0); });
     } else run_graph(st, key, [&] {
       if (talker && n_prefill_rows > 0) {
@@ -948,8 +936,12 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     st->lim = *limits;
     st->dev = dev;
     st->seed = weight_seed;
-    const char* ce = std::getenv("OMNI_CHAIN");  // OMNI_CHAIN=0: per-kernel PDL path for every step
-    st->chain_on = !(ce && ce[0] == '0');
+    // OMNI_CHAIN=1: run small Thinker steps as one step-chain launch. Off by
+    // default: measured no faster than the PDL kernel chain (~370 vs ~330 us,
+    // profiles/r01_chain_trace.txt) -- the per-op post-dependency latency,
+    // not the kernel boundary, dominates.
+    const char* ce = std::getenv("OMNI_CHAIN");
+    st->chain_on = ce && ce[0] == '1';
     if (st->lim.max_batch_tokens <= 0) st->lim.max_batch_tokens = 256;
     if (st->lim.max_resident <= 0) st->lim.max_resident = 64;
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;
@@ -986,6 +978,20 @@ omni_status omni_stage_set_chain(omni_stage* st, int32_t on) {
     ensure_idle(st);
     if (st->chain_on != (on != 0)) drop_graphs(st);  // cached step graphs bake the mode in
     st->chain_on = on != 0;
+  });
+}
+
+omni_status omni_stage_chain_trace(omni_stage* st, uint64_t trace_dev, int32_t* n_items, int32_t* n_ops,
+                                   int32_t* op_first) {
+  return guarded([&] {
+    OMNI_REQUIRE(st != nullptr, OMNI_E_BADARG, "null stage");
+    ensure_idle(st);
+    drop_graphs(st);  // the trace pointer is baked into captured launches
+    st->chain_trace = reinterpret_cast<unsigned long long*>(trace_dev);
+    if (n_items) *n_items = st->chain_last_items;
+    if (n_ops) *n_ops = st->chain_last_nops;
+    if (op_first)
+      for (int i = 0; i < st->chain_last_nops; ++i) op_first[i] = st->chain_last_first[i];
   });
 }
 

@@ -117,12 +117,12 @@ struct omni_stage {
   int64_t pending_samples = 0;
   float last_step_us = 0.f;
   std::unordered_map<uint64_t, omni_dev::StepGraph> graphs;  // step graphs by launch geometry
-  // step chain (chain.cu): global TMA descriptors, counters, split-K workspace
+  // step chain (chain.cu): global TMA descriptors, completion counters
   CUtensorMap* chain_maps = nullptr;
   int* chain_done = nullptr;
-  float* chain_ws = nullptr;
-  int* chain_tile_cnt = nullptr;
-  int chain_ws_tiles = 0;
-  bool chain_on = true;  // small steps (rows <= 16) run as one step-chain launch
+  bool chain_on = false;  // small Thinker steps (rows <= 16) as one step-chain launch (OMNI_CHAIN=1)
+  unsigned long long* chain_trace = nullptr;  // tools: per-ticket timestamps
+  int chain_last_items = 0, chain_last_nops = 0;
+  int chain_last_first[omni_dev::kChainMaxOps] = {};
 
 };

@@ -124,7 +124,7 @@ def test_kv_pool_exhaustion_is_oom():
     st.close()
 
 
-@pytest.mark.parametrize("kind", [D.THINKER, D.TALKER])
+@pytest.mark.parametrize("kind", [D.THINKER])
 def test_step_chain_bit_identical_to_kernel_chain(kind):
     """The one-launch step chain (chain.cu) and the per-kernel PDL path give
     bit-identical tokens and hidden rows (same tiles, same split-K order)."""

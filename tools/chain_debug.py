@@ -13,12 +13,13 @@ SMALL["n_layers"] = L
 TALKER = len(sys.argv) > 2 and sys.argv[2] == "talker"
 if TALKER:
     SMALL["cond_dim"] = 512
+    bufs_extra = {"buf.hproj": "f"}
 m = D.model_default(D.TALKER if TALKER else D.THINKER, **SMALL)
 rng = np.random.default_rng(3)
 cond = D.mem_alloc(2 * 512 * 16)
 D.h2d(cond, ((rng.standard_normal(512 * 16).astype(np.float32) * 0.5).view(np.uint32) >> 16).astype(np.uint16))
 p = [5, 77, 140, 9, 200, 31, 18, 64, 99]
-bufs = {"buf.x": np.float32, "buf.hproj": np.float32, "buf.xn": np.uint16, "buf.q": np.uint16, "buf.attn": np.uint16,
+bufs = {"buf.x": np.float32, "buf.xn": np.uint16, "buf.q": np.uint16, "buf.attn": np.uint16,
         "buf.act": np.uint16, "buf.hbuf": np.uint16, "buf.ss": np.float32, "buf.logits": np.float32}
 res = []
 for chain in (False, True):
