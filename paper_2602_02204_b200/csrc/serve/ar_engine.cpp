@@ -348,6 +348,8 @@ void ArEngine::send_chunk(Resident& r, EmitPlan& plan, size_t b, size_t e, bool 
   c.seq = plan.next_seq++;
   c.eos = eos;
   c.payload = model_.pack_chunk(r.seq, b, e);
+  if (plan.tokens_i32 && (c.payload.dtype != Dtype::I32 || c.payload.is_device()))
+    c.payload = Payload::from_i32(std::span<const int32_t>(r.seq.emitted.data() + b, e - b));
   plan.sender.send(c);
 }
 

@@ -584,6 +584,8 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
     env.submit_ar(std::move(sub));
   });
   reg.register_transfer("Talker2Vocoder", [](TransferEnv& env) { env.wire_diffusion({4, 16}); });
+  // branching graphs (BASELINE config 5): Thinker text ids -> image DiT
+  reg.register_transfer("Thinker2Image", [](TransferEnv& env) { env.wire_diffusion({4, 16}); });
 
   for (auto& [name, dp] : I.dit) {
     DitStage* d = dp.get();

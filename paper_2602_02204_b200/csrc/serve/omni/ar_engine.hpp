@@ -31,6 +31,7 @@ struct EmitPlan {
   StreamSender sender;
   size_t sent_tokens = 0;
   uint32_t next_seq = 0;
+  bool tokens_i32 = false;  // diffusion consumer: ship emitted ids as I32 (per-edge pack)
 };
 
 struct ArAdmission {

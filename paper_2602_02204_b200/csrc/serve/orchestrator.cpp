@@ -392,6 +392,12 @@ void Orchestrator::admit_request(Pending s, uint64_t now) {
       plan.mode = mode;
       plan.chunk_size = e.streaming_chunk_size ? e.streaming_chunk_size : 1;
       plan.sender = conn.open_stream(rid);
+      // per-edge payload: a diffusion consumer conditions on the token ids
+      // (I32, the reference's AR pack, reference_pipeline.hpp:227-234) even
+      // when the producer's model packs something else for AR consumers
+      // (the Thinker's FIX16 hidden rows) -- the reference has one pack per
+      // model and fails branching graphs with BadDtype.
+      plan.tokens_i32 = plan_.graph.find_node(e.to)->kind == StageKind::DIFFUSION;
       f->stage_plans[e.from].push_back(std::move(plan));
       StreamReceiver recv = conn.subscribe(rid);
       const bool to_ar = plan_.graph.find_node(e.to)->kind == StageKind::AR;

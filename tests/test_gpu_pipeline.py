@@ -78,6 +78,23 @@ def test_ar_dit_and_single_stage_configs():
         p.close()
 
 
+def test_branching_graph_config5():
+    """BASELINE config 5 (Ming-Omni-style branching): one Thinker feeding a
+    Talker -> Code2Wav audio branch AND an image DiT branch. The reference
+    cannot run it (BadDtype: its Thinker packs FIX16-free U8 rows for every
+    edge, diffusion_engine.hpp:29-30); here the edge to a diffusion consumer
+    carries the token ids (per-edge pack) and each exit assembles its own
+    waveform (per-exit waves)."""
+    p = Pipeline((ROOT / "configs" / "ming_branch.json").read_text(), weight_seed=5, small_models=True)
+    for clock in ("virtual", "device"):
+        r = p.bench(n=12, seed=3, concurrency=4, clock=clock)
+        assert r["completed"] == 12 and r["failed"] == 0, r
+        assert r["codec_tokens"] == 4 * r["text_tokens"]
+        # the reported waveform is one exit's (16 samples per conditioning token)
+        assert r["wave_samples"] in (16 * r["codec_tokens"], 16 * r["text_tokens"])
+    p.close()
+
+
 def test_full_size_omni3_device():
     p = Pipeline((ROOT / "configs" / "omni3.json").read_text(), weight_seed=7)
     r = p.bench(n=16, seed=7, concurrency=16, clock="device")
