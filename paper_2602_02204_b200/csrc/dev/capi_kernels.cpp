@@ -169,9 +169,16 @@ omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, i
     OMNI_REQUIRE(n_w > 0 && iters > 0, OMNI_E_BADARG, "gemm_time_multi: empty");
     const int N_pad = (N + 127) / 128 * 128;
     std::vector<GemmWeight> ws(n_w);
-    for (int i = 0; i < n_w; ++i)
-      OMNI_REQUIRE(gemm_make_weight(ws[i], reinterpret_cast<const __nv_bfloat16*>(Ws[i]), N, N_pad, K, max_splits),
+    // max_splits < 0: a compute-bound (DiT-style) weight, split cap -max_splits,
+    // token tile chosen by the fill-the-SMs cost model (gemm_tc.cu bn_for)
+    const bool fill = max_splits < 0;
+    const int cap = fill ? -max_splits : max_splits;
+    for (int i = 0; i < n_w; ++i) {
+      OMNI_REQUIRE(gemm_make_weight(ws[i], reinterpret_cast<const __nv_bfloat16*>(Ws[i]), N, N_pad, K, cap,
+                                    fill ? 64 : 192),
                    OMNI_E_BADARG, "weight tensor map");
+      ws[i].fill_sms = fill;
+    }
     GemmInput x;
     OMNI_REQUIRE(gemm_make_input(x, reinterpret_cast<const __nv_bfloat16*>(X), M, K), OMNI_E_BADARG, "input map");
     GemmEpilogue e;
