@@ -59,7 +59,7 @@ bool gemm_make_weight(GemmWeight& w, const __nv_bfloat16* ptr, int N, int N_pad,
   w.N = N;
   w.N_pad = N_pad;
   w.K = K;
-  w.splits = gemm_choose_splits(N_pad, K, max_splits < 1 ? 1 : (max_splits > 8 ? 8 : max_splits), target_ctas);
+  w.splits = gemm_choose_splits(N_pad, K, max_splits < 1 ? 1 : (max_splits > 16 ? 16 : max_splits), target_ctas);
   return encode_2d(w.tmap, ptr, N_pad, K, 128);
 }
 

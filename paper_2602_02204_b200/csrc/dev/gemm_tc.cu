@@ -178,13 +178,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int q = threadIdx.x; q < n4; q += kThreads) {
       const int c = c0 + q / 32, r4 = (q % 32) * 4;
       const uint32_t off = static_cast<uint32_t>((c * 128 + r4) * 4);
-      float4 v[8];
+      float4 v[16];
 #pragma unroll
-      for (int z = 0; z < 8; ++z)
+      for (int z = 0; z < 16; ++z)
         if (z < S) v[z] = dsmem_ld_f32x4(dsmem_map(red_s + off, z));
       float4 acc = v[0];
 #pragma unroll
-      for (int z = 1; z < 8; ++z)
+      for (int z = 1; z < 16; ++z)
         if (z < S) acc.x += v[z].x, acc.y += v[z].y, acc.z += v[z].z, acc.w += v[z].w;
       *reinterpret_cast<float4*>(fin + (c - c0) * 128 + r4) = acc;
     }
@@ -228,6 +228,18 @@ cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a
   constexpr size_t smem = smem_for<BN, STAGES>();
   static std::atomic<uint64_t> configured{0};  // per instantiation, per device
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
+  if (a.splits > 8) {  // 16-CTA clusters are non-portable (opt-in)
+    static std::atomic<uint64_t> np{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(np.load() & bit)) {
+      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          e != cudaSuccess)
+        return e;
+      np.fetch_or(bit);
+    }
+  }
   return launch_k(kern, dim3(w.N_pad / kBlockM, (a.M + BN - 1) / BN, a.splits), dim3(kThreads), smem, st,
                   a.splits, w.tmap, x.tmap_for(BN), a);
 }
@@ -329,7 +341,7 @@ cudaError_t gemm_make_args(const GemmWeight& w, const GemmInput& x, int M, int e
                              w.K % 64 != 0 || w.N != (e.rope.n_heads + 2 * e.rope.n_kv) * 128))
     return cudaErrorInvalidValue;
   if (e.ss_in && (e.ss_n <= 0 || e.norm_d <= 0.f)) return cudaErrorInvalidValue;
-  if (w.splits > 8 || (a.K / kBlockK) % w.splits != 0) return cudaErrorInvalidValue;
+  if (w.splits > 16 || (a.K / kBlockK) % w.splits != 0) return cudaErrorInvalidValue;
   return cudaSuccess;
 }
 

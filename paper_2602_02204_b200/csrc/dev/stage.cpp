@@ -143,7 +143,11 @@ void build_ar(omni_stage* st) {
     ly.gqkv = gemm_of(ly.wqkv, 8);
     ly.go = gemm_of(ly.wo, 8);
     ly.ggu = gemm_of(ly.wgu, 8);
-    ly.gd = gemm_of(ly.wd, 8);
+    static const int down_split = [] {  // OMNI_DOWN_SPLIT (experiments): split cap / CTA target of the down proj
+      const char* e = std::getenv("OMNI_DOWN_SPLIT");
+      return e ? std::atoi(e) : 8;
+    }();
+    ly.gd = gemm_of(ly.wd, down_split, down_split > 8 ? 256 : 192);
   }
 
   // activations
@@ -156,8 +160,9 @@ void build_ar(omni_stage* st) {
   st->act = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
   st->hbuf = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
   st->logits = dev_alloc<float>(st, (size_t)R * st->vocab_pad);
-  st->d_tok = dev_alloc<int32_t>(st, R);
-  st->d_margin = dev_alloc<float>(st, R);
+  // per-step results [n_dec tokens | n_dec margins] contiguous -> one D2H copy
+  st->d_tok = dev_alloc<int32_t>(st, 2 * (size_t)R);
+  st->d_margin = reinterpret_cast<float*>(st->d_tok + R);  // unused slot kept for the struct
   st->in_xn = input_of(st->xn, R, d);
   st->in_attn = input_of(st->attn, R, H * kHeadDim);
   st->in_act = input_of(st->act, R, ff);
@@ -207,8 +212,7 @@ void build_ar(omni_stage* st) {
                               cudaMemcpyHostToDevice, st->stream));
     st->chain_done = dev_alloc<int>(st, kChainMaxOps + 1);
   }
-  OMNI_CUDA(cudaMallocHost(&st->h_tok, R * sizeof(int32_t)));
-  OMNI_CUDA(cudaMallocHost(&st->h_margin, R * sizeof(float)));
+  OMNI_CUDA(cudaMallocHost(&st->h_tok, 2 * (size_t)R * sizeof(int32_t)));
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
 }
 
@@ -312,7 +316,6 @@ void destroy_stage(omni_stage* st) {
     if (s->in_use) cudaEventDestroy(s->in_use);
   }
   if (st->h_tok) cudaFreeHost(st->h_tok);
-  if (st->h_margin) cudaFreeHost(st->h_margin);
   if (st->h_samples) cudaFreeHost(st->h_samples);
   for (cudaEvent_t e : {st->ev_start, st->ev_done, st->ev_link})
     if (e) cudaEventDestroy(e);
@@ -436,7 +439,7 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   P.argmax_lo = st->argmax_lo;
   P.argmax_hi = st->argmax_hi;
   P.tok = st->d_tok;
-  P.margin = st->d_margin;
+  P.margin = reinterpret_cast<float*>(st->d_tok + n_dec);
   int total = 0;
   auto add = [&](ChainOp op) {  // item ranges padded to whole clusters (one ticket = 8 items)
     OMNI_REQUIRE(P.n_ops < kChainMaxOps, OMNI_E_BADARG, "step chain: too many ops");
@@ -710,14 +713,13 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
         e.ldo = st->vocab_pad;
         OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
         OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
-                                st->d_tok, st->d_margin, s));
+                                st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
       }
     });
     if (n_dec > 0) {
-      OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      // tokens and margins in one copy: [n_dec x i32 | n_dec x f32]
+      OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, 2 * n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       counters().d2h_bytes += n_dec * (sizeof(int32_t) + sizeof(float));
-      OMNI_CUDA(cudaMemcpyAsync(st->h_margin, st->d_margin, n_dec * sizeof(float),
-                                cudaMemcpyDeviceToHost, s));
     }
   }
   OMNI_CUDA(cudaEventRecord(st->ev_done, s));
@@ -846,7 +848,7 @@ void finish_pending(omni_stage* st) {
       for (size_t i = 0; i < st->pending_dec_entries.size(); ++i) {
         const int e = st->pending_dec_entries[i];
         if (st->user_tok) st->user_tok[e] = st->h_tok[i];
-        if (st->user_margin) st->user_margin[e] = st->h_margin[i];
+        if (st->user_margin) st->user_margin[e] = reinterpret_cast<const float*>(st->h_tok)[st->pending_dec_entries.size() + i];
       }
     }
   } else if (st->pending_kind == 2 && st->user_samples) {

@@ -105,7 +105,6 @@ struct omni_stage {
   // ---- step staging / results ----
   omni_dev::Staging desc, pack;
   int32_t* h_tok = nullptr;
-  float* h_margin = nullptr;
   int32_t* h_samples = nullptr;
   bool pending = false;
   int pending_kind = 0;  // 1 = AR, 2 = DiT
