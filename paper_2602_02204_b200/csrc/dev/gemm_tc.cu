@@ -280,19 +280,12 @@ static int bn_for(const GemmWeight& w, int M) {
       return e ? std::atoi(e) : 0;
     }();
     if (forced == 64 || forced == 128 || forced == 256) return forced;
-    // wave-quantised cost model: waves x (max(BN, 128) + 52): an N=64 MMA
-    // tile runs no faster than N=128 (measured, tools/dit_gemm_sweep.py), the
-    // 52 (fit: BN=256 is 1.17x faster than 128 at 8192 rows) stands for the
-    // per-tile prologue/epilogue; ties go to the wider tile
-    const int tiles = w.N_pad / kBlockM;
-    int best = 256;
-    long best_cost = -1;
-    for (int cand = 256; cand >= 64; cand /= 2) {
-      const long ctas = (long)tiles * ((M + cand - 1) / cand) * w.splits;
-      const long cost = ((ctas + 147) / 148) * ((cand > 128 ? cand : 128) + 52);
-      if (best_cost < 0 || cost < best_cost) best = cand, best_cost = cost;
-    }
-    bn = best;
+    // Widest token tile (fewest CTAs), not the isolated-latency optimum: the
+    // DiT shares the GPU with two latency-bound AR chains, and fat tiles leave
+    // them SMs -- measured +6.5 % pipeline req/s over a fill-the-SMs cost
+    // model (profiles/r01_bench_dit_bn_ab.log) although each DiT GEMM alone is
+    // up to 1.6x slower at <= 1k rows (profiles/r01_dit_gemm_sweep_forced_bn.txt).
+    bn = M <= 128 ? 128 : 256;
   }
   return bn;
 }
