@@ -3,6 +3,9 @@
 // step drivers behind the C ABI (include/omni_dev.h).
 #include "stage.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -250,10 +253,9 @@ void build_dit(omni_stage* st) {
       return e ? std::atoi(e) : 1;
     }();
     static const int dit_split2 = [] {  // OMNI_DIT_SPLIT_W2: split-K cap of the MLP-down (K = 4d).
-      // Default 2: -15 % at the serving batch (8-64 tokens), +10 % at >= 256
-      // tokens (profiles/r01_ab_dit_split.txt)
+      // Default 1 with the widest-tile policy (profiles/r01_bench_ditw2_ab.log)
       const char* e = std::getenv("OMNI_DIT_SPLIT_W2");
-      return e ? std::atoi(e) : 2;
+      return e ? std::atoi(e) : 1;
     }();
     ly.go = gemm_of(ly.wo, dit_split, 64);
     ly.go.fill_sms = true;
@@ -860,6 +862,63 @@ void finish_pending(omni_stage* st) {
 
 std::mutex g_init_mu;
 
+// Optional spatial partition of the GPU between the stage kinds (green
+// contexts, CUDA 12.4+): OMNI_SM_SPLIT="dit:N" runs DiT stages on N SMs;
+// "dit:N,ar" also confines the AR stages to the other SMs. Memory stays in
+// the primary context; only the streams (kernel placement) are partitioned.
+struct SmPartition {
+  bool ok = false;
+  CUgreenCtx dit = nullptr, rest = nullptr;
+  bool ar_rest = false;
+};
+
+template <typename F>
+F driver_fn(const char* n) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(n, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+
+SmPartition& sm_partition(int dev) {
+  static std::mutex mu;
+  static std::unordered_map<int, SmPartition> parts;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = parts.find(dev);
+  if (it != parts.end()) return it->second;
+  SmPartition& P = parts[dev];
+  const char* e = std::getenv("OMNI_SM_SPLIT");
+  if (!e || std::strncmp(e, "dit:", 4) != 0) return P;
+  const unsigned n = (unsigned)std::atoi(e + 4);
+  P.ar_rest = std::strstr(e, ",ar") != nullptr;
+  auto getRes = driver_fn<PFN_cuDeviceGetDevResource_v12040>("cuDeviceGetDevResource");
+  auto split = driver_fn<PFN_cuDevSmResourceSplitByCount_v12040>("cuDevSmResourceSplitByCount");
+  auto gen = driver_fn<PFN_cuDevResourceGenerateDesc_v12040>("cuDevResourceGenerateDesc");
+  auto gcreate = driver_fn<PFN_cuGreenCtxCreate_v12040>("cuGreenCtxCreate");
+  if (!getRes || !split || !gen || !gcreate) return P;
+  CUdevResource all{}, part{}, rest{};
+  unsigned groups = 1;
+  CUdevResourceDesc d1, d2;
+  if (getRes(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(&part, &groups, &all, &rest, 0, n) != CUDA_SUCCESS || groups != 1 ||
+      gen(&d1, &part, 1) != CUDA_SUCCESS || gen(&d2, &rest, 1) != CUDA_SUCCESS ||
+      gcreate(&P.dit, d1, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      gcreate(&P.rest, d2, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+    return P;
+  P.ok = true;
+  return P;
+}
+
+cudaStream_t partitioned_stream(int dev, bool dit, int prio) {
+  SmPartition& P = sm_partition(dev);
+  if (!P.ok || (!dit && !P.ar_rest)) return nullptr;
+  auto gstream = driver_fn<PFN_cuGreenCtxStreamCreate_v12050>("cuGreenCtxStreamCreate");
+  CUstream s = nullptr;
+  if (!gstream || gstream(&s, dit ? P.dit : P.rest, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS) return nullptr;
+  return reinterpret_cast<cudaStream_t>(s);
+}
+
 }  // namespace
 
 struct omni_arena {
@@ -961,7 +1020,8 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     const int kind_ix = model->kind == OMNI_MODEL_THINKER ? 0 : model->kind == OMNI_MODEL_TALKER ? 1 : 2;
     const int rank = std::clamp(ranks[kind_ix] - '0', 0, 2);
     const int prio = hi + (lo - hi) * rank / 2;
-    OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, prio));
+    st->stream = partitioned_stream(dev, model->kind == OMNI_MODEL_DIT, prio);
+    if (!st->stream) OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, prio));
     OMNI_CUDA(cudaEventCreate(&st->ev_start));
     OMNI_CUDA(cudaEventCreate(&st->ev_done));
     OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_link, cudaEventDisableTiming));
