@@ -6,7 +6,7 @@ IFS='|' read -ra CFGS <<< "${BENCH_AB:-OMNI_X=0}"
 for r in $(seq 1 ${REPS:-3}); do
 for cfg in "${CFGS[@]}"; do
   echo "== $cfg" >> gpurun_out/bench_rep.log
-  env $cfg timeout 600 python bench.py --no-cpu-baseline --warmup 2 --steps 4 >> gpurun_out/bench_rep.log 2>&1
+  env $cfg timeout 600 python bench.py --no-cpu-baseline --warmup 2 --steps ${STEPS:-4} >> gpurun_out/bench_rep.log 2>&1
 done
 done
 python - <<'PY'
