@@ -259,6 +259,8 @@ def main() -> None:
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         lib.omni_dev_counters(C.byref(l0), C.byref(h0), C.byref(d0))
+        gc0, gr0 = C.c_uint64(), C.c_uint64()
+        lib.omni_dev_graph_counters(C.byref(gc0), C.byref(gr0))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
         e0.record()
@@ -271,6 +273,8 @@ def main() -> None:
         dist.barrier()
     l1, h1, d1 = C.c_uint64(), C.c_uint64(), C.c_uint64()
     lib.omni_dev_counters(C.byref(l1), C.byref(h1), C.byref(d1))
+    gc1, gr1 = C.c_uint64(), C.c_uint64()
+    lib.omni_dev_graph_counters(C.byref(gc1), C.byref(gr1))
     dev_ms = e0.elapsed_time(e1)
     agg = aggregate(sum(r["completed"] for r in results), dev_ms, wall, dist)
     t_max_ms, wall_max, done_all, value = agg["t_max_ms"], agg["wall_max_s"], agg["completed"], agg["value"]
@@ -341,6 +345,8 @@ def main() -> None:
                 "note": "host-clock time of the public C-ABI bench call incl. orchestrator setup, per-step "
                         "descriptor H2D copies from pinned memory and token/sample D2H reads"},
         "gpu_launches": int(l1.value - l0.value),
+        "step_graphs": {"captured_in_timed_region": int(gc1.value - gc0.value),
+                        "replayed": int(gr1.value - gr0.value)},
         "clocks": clk.summary(),
     }
     print(json.dumps(out))

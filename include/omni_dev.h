@@ -208,6 +208,8 @@ omni_status omni_device_sync(void);
 /* Process-wide counters: kernels launched by libomni_dev, bytes copied
  * host->device / device->host by the step / pack entry points. */
 omni_status omni_dev_counters(uint64_t* launches, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
+/* Step-graph cache: graphs captured (first use of a launch geometry) and replayed. */
+omni_status omni_dev_graph_counters(uint64_t* captures, uint64_t* replays);
 
 /* ------------------------------------------------------------------------ */
 /* Kernel-level entry points (parity tests / microbenchmarks). All pointers */

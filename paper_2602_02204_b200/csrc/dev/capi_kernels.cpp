@@ -106,6 +106,13 @@ omni_status omni_device_count(int32_t* n) {
   });
 }
 
+omni_status omni_dev_graph_counters(uint64_t* captures, uint64_t* replays) {
+  return guarded([&] {
+    if (captures) *captures = counters().graph_captures;
+    if (replays) *replays = counters().graph_replays;
+  });
+}
+
 omni_status omni_dev_counters(uint64_t* launches, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
   return guarded([&] {
     const auto& c = counters();

@@ -31,6 +31,7 @@ void set_last_error(const std::string& msg);
 // of OUR kernels ran and how many bytes crossed PCIe).
 struct DevCounters {
   uint64_t launches = 0, h2d_bytes = 0, d2h_bytes = 0;
+  uint64_t graph_captures = 0, graph_replays = 0;
 };
 DevCounters& counters();
 

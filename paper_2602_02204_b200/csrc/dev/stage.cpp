@@ -92,6 +92,7 @@ bool staging_reserve(Staging& s, size_t bytes) {
 void drop_graphs(omni_stage* st) {
   for (auto& kv : st->graphs) cudaGraphExecDestroy(kv.second.exec);
   st->graphs.clear();
+  st->key_hits.clear();
 }
 
 void require_device() {
@@ -351,6 +352,8 @@ void ensure_pages(omni_stage* st, SeqSlot& s, int upto) {
 
 size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
+constexpr int kGraphAfterHits = 3;  // eager launches of a geometry before it is captured
+
 // OMNI_GRAPHS=0 launches every step eagerly (A/B measurements).
 bool graphs_enabled() {
   static const bool on = [] {
@@ -375,6 +378,14 @@ void run_graph(omni_stage* st, uint64_t key, F&& body) {
   }
   auto it = st->graphs.find(key);
   if (it == st->graphs.end()) {
+    // Capture + instantiate costs ~1 ms of host time: a launch geometry is
+    // only graphed once it has recurred (timing-dependent batches produce a
+    // long tail of one-off geometries); until then the step runs eagerly
+    // (still PDL-chained).
+    if (++st->key_hits[key] < kGraphAfterHits) {
+      body();
+      return;
+    }
     if (st->graphs.size() >= 4096) drop_graphs(st);
     const uint64_t l0 = counters().launches;
     OMNI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
@@ -395,7 +406,9 @@ void run_graph(omni_stage* st, uint64_t key, F&& body) {
     cudaGraphDestroy(g);
     OMNI_CUDA(e);
     it = st->graphs.emplace(key, sg).first;
+    ++counters().graph_captures;
   }
+  ++counters().graph_replays;
   OMNI_CUDA(cudaGraphLaunch(it->second.exec, s));
   counters().launches += it->second.nodes;
 }

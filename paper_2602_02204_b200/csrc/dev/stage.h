@@ -116,6 +116,7 @@ struct omni_stage {
   int64_t pending_samples = 0;
   float last_step_us = 0.f;
   std::unordered_map<uint64_t, omni_dev::StepGraph> graphs;  // step graphs by launch geometry
+  std::unordered_map<uint64_t, int> key_hits;                 // eager runs per geometry before capture
   // step chain (chain.cu): global TMA descriptors, completion counters
   CUtensorMap* chain_maps = nullptr;
   int* chain_done = nullptr;
