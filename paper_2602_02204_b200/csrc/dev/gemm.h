@@ -18,6 +18,7 @@ enum GemmEpi : int {
   EPI_GELU = 5,         // Y_bf16[tok, n] = gelu_tanh(acc)
   EPI_RESID_NORM = 6,   // R_f32[tok, n] += acc; Xb_bf16[tok, n] = bf16(R); ss_out[tok, tile] = sum R^2
   EPI_ROPE_KV = 7,      // one tile = one 128-dim head of QKV: RoPE(q,k), q -> q_out rows, k/v -> paged KV
+  EPI_EULER = 8,        // DiT Euler update: x_f32[tok, n] += dt * acc; xb = bf16(x); last step: int32 sample of ch 0
 };
 
 // Fused RoPE + paged-KV append (EPI_ROPE_KV): the QKV GEMM tile n is head n
@@ -81,6 +82,10 @@ struct GemmEpilogue {
   // EPI_F32 only: out[tok, n] = acc + row_bias[tok % bias_period, n] (bf16 rows of width N)
   const __nv_bfloat16* row_bias = nullptr;
   int bias_period = 1;
+  // EPI_EULER: step size, and on the final step the int32 sample output
+  // (rint(sample_scale * x[tok, 0]) clamped to [-64, 63]; nullptr otherwise)
+  float dt = 0.f, sample_scale = 0.f;
+  int32_t* samples = nullptr;
   // phase trace (tools only): per CTA 8 u64 = globaltimer at entry / exit and
   // clock64 deltas of setup, producer-wait, last-load, mainloop-done, drain, end
   unsigned long long* trace = nullptr;
@@ -106,6 +111,8 @@ struct GemmArgs {
   const __nv_bfloat16* row_bias;
   int bias_period;
   unsigned long long* trace;
+  float dt, sample_scale;
+  int32_t* samples;
 };
 
 int gemm_block_n(int M);

@@ -189,6 +189,19 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] += g[i] * v[i];
         st8(r, x);
+      } else if constexpr (EPI == EPI_EULER) {
+        float* xr = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
+        float x[8];
+        ld8(xr, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] += a.dt * v[i];
+        st8(xr, x);
+        st8_bf16(a.xb + (size_t)tok * a.ldo + n0, x);
+        if (a.samples && n0 == 0) {
+          float q = rintf(a.sample_scale * x[0]);
+          q = fminf(fmaxf(q, -64.f), 63.f);
+          a.samples[tok] = (int32_t)q;
+        }
       } else if constexpr (EPI == EPI_GELU) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = gelu_tanh(v[i]);

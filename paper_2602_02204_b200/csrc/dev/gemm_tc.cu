@@ -253,7 +253,8 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
     const char* e = std::getenv("OMNI_DIT_2CTA");
     return e && e[0] == '1';
   }();
-  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_GATED_RESID || EPI == EPI_F32) {
+  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_GATED_RESID || EPI == EPI_F32 ||
+                EPI == EPI_EULER) {
     if (dit2 && w.fill_sms) {
       switch (bn_for(w, a.M)) {
         case 64: return launch_bn<64, EPI, 4>(w, x, a, st);
@@ -323,6 +324,10 @@ cudaError_t gemm_make_args(const GemmWeight& w, const GemmInput& x, int M, int e
   a.ss_out = e.ss_out;
   a.rope = e.rope;
   a.trace = e.trace;
+  a.dt = e.dt;
+  a.sample_scale = e.sample_scale;
+  a.samples = e.samples;
+  if (epi == EPI_EULER && (e.xb == nullptr || e.ss_in != nullptr)) return cudaErrorInvalidValue;
   a.row_bias = e.row_bias;
   a.bias_period = e.bias_period > 0 ? e.bias_period : 1;
   if (e.row_bias && (epi != EPI_F32 || w.N != w.N_pad)) return cudaErrorInvalidValue;
@@ -352,6 +357,7 @@ cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi, co
     case EPI_GELU: return launch_epi<EPI_GELU>(w, x, a, st);
     case EPI_RESID_NORM: return launch_epi<EPI_RESID_NORM>(w, x, a, st);
     case EPI_ROPE_KV: return launch_epi<EPI_ROPE_KV>(w, x, a, st);
+    case EPI_EULER: return launch_epi<EPI_EULER>(w, x, a, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -795,11 +795,16 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
       OMNI_KERNEL(gemm_run(ly.g2, st->din_u, rows, EPI_GATED_RESID, e, s));
     }
     OMNI_KERNEL(dit_ln_mod(st->dh, rows, d, nullptr, toks_dev, 0, 0, 0, S, st->da, s));
+    // output projection with the Euler update fused: x += dt * v, next
+    // step's bf16 input, and on the last step the int32 samples
     GemmEpilogue eo;
-    eo.out = st->dv;
+    eo.out = st->dx;
     eo.ldo = C;
-    OMNI_KERNEL(gemm_run(st->g_out, st->din_a, rows, EPI_F32, eo, s));
-    OMNI_KERNEL(dit_euler(st->dx, st->dxin, st->dv, C, rows, 1.f / T, t == T - 1, samples_dev, s));
+    eo.xb = st->dxin;
+    eo.dt = 1.f / T;
+    eo.sample_scale = kSampleScale;
+    eo.samples = t == T - 1 ? samples_dev : nullptr;
+    OMNI_KERNEL(gemm_run(st->g_out, st->din_a, rows, EPI_EULER, eo, s));
   }
 }
 
