@@ -396,4 +396,110 @@ __device__ __forceinline__ void argmax_row(int r, const float* __restrict__ logi
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused step head for small vocabularies (V <= 256): final RMSNorm of one
+// DECODE row -> bf16 hidden row (+ Thinker hidden ring), LM-head dot
+// products on the CUDA cores (one warp per output id, 16-byte loads of the
+// L2-resident head weights), greedy id + top-2 margin. Replaces
+// final_gather + LM-head GEMM + argmax (two kernel boundaries less on the
+// per-token critical path). A row's ids [v0, v1) may be split over `parts`
+// CTAs: each recomputes the (cheap) norm, the last one to finish (ticket in
+// cnt[di], reset for the next replay) runs the argmax over the row in global
+// memory. Hidden rows are bit-identical to final_gather_row; each logit is
+// one warp's fixed-order dot product, so the split does not change it.
+// smem: hs[d] floats (+ red[32]).
+// ---------------------------------------------------------------------------
+
+template <class Dep>
+__device__ __forceinline__ void head_row(int di, int v0, int v1, int parts, int* __restrict__ cnt,
+                                         const ArStepDev& s, const float* __restrict__ x, int d, float eps,
+                                         __nv_bfloat16* __restrict__ hout, __nv_bfloat16* __restrict__ ring,
+                                         int ring_rows, const __nv_bfloat16* __restrict__ lm,
+                                         float* __restrict__ logits, int ld, int lo, int hi,
+                                         int* __restrict__ tok_out, float* __restrict__ margin_out, float* hs,
+                                         float* red, Dep dep) {
+  dep();
+  const int e = s.dec_entries[di];
+  const ArEntryDesc ed = s.entries[e];
+  const float* xr = x + (size_t)ed.row0 * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
+  const float tot = block_sum(ss, red);
+  const float inv = rsqrtf(tot / d + eps);
+  __nv_bfloat16* h = hout + (size_t)di * d;
+  __nv_bfloat16* rg = (ring && v0 == 0) ? ring + ((size_t)ed.slot * ring_rows + ed.out_index) * d : nullptr;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const __nv_bfloat16 v = f2bf(xr[i] * inv);
+    if (v0 == 0) h[i] = v;
+    if (rg) rg[i] = v;
+    hs[i] = bf2f(v);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  float* lrow = logits + (size_t)di * ld;
+  for (int v = v0 + warp; v < v1; v += nw) {
+    const __nv_bfloat16* wr = lm + (size_t)v * d;
+    float acc = 0.f;
+#pragma unroll 4
+    for (int i0 = lane * 8; i0 < d; i0 += 32 * 8) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(wr + i0);
+      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      const float4 ha = *reinterpret_cast<const float4*>(hs + i0);
+      const float4 hb = *reinterpret_cast<const float4*>(hs + i0 + 4);
+      const float2 f0 = __bfloat1622float2(w2[0]), f1 = __bfloat1622float2(w2[1]);
+      const float2 f2 = __bfloat1622float2(w2[2]), f3 = __bfloat1622float2(w2[3]);
+      acc += f0.x * ha.x + f0.y * ha.y;
+      acc += f1.x * ha.z + f1.y * ha.w;
+      acc += f2.x * hb.x + f2.y * hb.y;
+      acc += f3.x * hb.z + f3.y * hb.w;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) lrow[v] = acc;
+  }
+  if (parts > 1) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int t = atomicAdd(cnt + di, 1);
+      s_last = (t == parts - 1);
+      if (s_last) cnt[di] = 0;
+      __threadfence();
+    }
+    __syncthreads();
+    if (!s_last) return;
+  } else {
+    __syncthreads();
+  }
+  if (warp != 0) return;
+  float b1 = -INFINITY, b2 = -INFINITY;
+  int i1 = 0x7fffffff;
+  for (int i = lo + lane; i < hi; i += 32) {
+    const float v = __ldcg(lrow + i);
+    if (v > b1 || (v == b1 && i < i1)) {
+      b2 = b1;
+      b1 = v;
+      i1 = i;
+    } else if (v > b2) {
+      b2 = v;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
+    const float ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+    const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+    if (ob1 > b1 || (ob1 == b1 && oi1 < i1)) {
+      b2 = fmaxf(b1, ob2);
+      b1 = ob1;
+      i1 = oi1;
+    } else {
+      b2 = fmaxf(b2, ob1);
+    }
+  }
+  if (lane == 0) {
+    tok_out[di] = i1;
+    margin_out[di] = b1 - b2;
+  }
+}
+
 }  // namespace omni_dev

@@ -61,6 +61,19 @@ __global__ void final_gather_kernel(const ArStepDev s, const float* __restrict__
   final_gather_row(blockIdx.x, s, x, d, eps, hout, ring, ring_rows, red, PdlDep{});
 }
 
+__global__ void __launch_bounds__(256)
+    head_kernel(const ArStepDev s, const float* __restrict__ x, int d, float eps, __nv_bfloat16* __restrict__ hout,
+                __nv_bfloat16* __restrict__ ring, int ring_rows, const __nv_bfloat16* __restrict__ lm, int vocab,
+                float* __restrict__ logits, int ld, int lo, int hi, int* __restrict__ tok_out,
+                float* __restrict__ margin_out, int* __restrict__ cnt) {
+  extern __shared__ float head_smem[];  // hs[d]
+  __shared__ float red[32];
+  const int per = (vocab + gridDim.x - 1) / gridDim.x;
+  const int v0 = blockIdx.x * per;
+  head_row(blockIdx.y, v0, min(vocab, v0 + per), gridDim.x, cnt, s, x, d, eps, hout, ring, ring_rows, lm, logits,
+           ld, lo, hi, tok_out, margin_out, head_smem, red, PdlDep{});
+}
+
 __global__ void argmax_kernel(const float* __restrict__ logits, int ld, int lo, int hi,
                               int* __restrict__ tok_out, float* __restrict__ margin_out) {
   argmax_row(blockIdx.x, logits, ld, lo, hi, tok_out, margin_out, PdlDep{});
@@ -98,6 +111,19 @@ cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, i
                                 cudaStream_t st) {
   return launch_k(final_gather_kernel, dim3(n_dec), dim3(256), 0, st, 1, s, x, d, eps, hout, ring,
                   ring_rows);
+}
+cudaError_t launch_head(const ArStepDev& s, int n_dec, const float* x, int d, float eps, __nv_bfloat16* hout,
+                        __nv_bfloat16* ring, int ring_rows, const __nv_bfloat16* lm, int vocab, float* logits,
+                        int ld, int lo, int hi, int* tok, float* margin, int* cnt, cudaStream_t st) {
+  if (vocab > kHeadMaxVocab || d % 256 != 0) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)d * sizeof(float);
+  // kHeadIdsPerCta ids per CTA (2 per warp): the LM head streams from L2 over many SMs
+  const int parts = (vocab + kHeadIdsPerCta - 1) / kHeadIdsPerCta;
+  static std::atomic<uint64_t> configured{0};
+  if (smem > 48 * 1024)
+    if (cudaError_t e = smem_attr_once(head_kernel, smem, configured); e != cudaSuccess) return e;
+  return launch_k(head_kernel, dim3(parts, n_dec), dim3(256), smem, st, 1, s, x, d, eps, hout, ring, ring_rows, lm,
+                  vocab, logits, ld, lo, hi, tok, margin, cnt);
 }
 cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
                           cudaStream_t st) {

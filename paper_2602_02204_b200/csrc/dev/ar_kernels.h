@@ -60,6 +60,13 @@ cudaError_t launch_attention(const ArStepDev& s, int n_blocks, const __nv_bfloat
 cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, int d, float eps,
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
                                 cudaStream_t st);
+// Fused final RMSNorm + LM head (CUDA cores) + greedy argmax, vocab <= 256.
+// Grid (vocab / kHeadIdsPerCta, n_dec); cnt = n_dec zeroed tickets (self-resetting).
+constexpr int kHeadMaxVocab = 256;
+constexpr int kHeadIdsPerCta = 16;
+cudaError_t launch_head(const ArStepDev& s, int n_dec, const float* x, int d, float eps, __nv_bfloat16* hout,
+                        __nv_bfloat16* ring, int ring_rows, const __nv_bfloat16* lm, int vocab, float* logits,
+                        int ld, int lo, int hi, int* tok, float* margin, int* cnt, cudaStream_t st);
 cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
                           cudaStream_t st);
 

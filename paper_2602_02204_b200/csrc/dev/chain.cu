@@ -294,6 +294,13 @@ __global__ void __launch_bounds__(kChainThreads, 2) step_chain_kernel(const __gr
       argmax_row(item, P.logits, P.vocab_pad, P.argmax_lo, P.argmax_hi, P.tok, P.margin, dep);
       signal_done(P.done + o);
       break;
+    case CHAIN_HEAD: {
+      float* hs = reinterpret_cast<float*>(chain_smem);
+      head_row(item, 0, P.vocab, 1, nullptr, P.sd, P.x, P.d, P.eps, P.hbuf, P.ring, P.ring_rows, P.lm, P.logits,
+               P.vocab_pad, P.argmax_lo, P.argmax_hi, P.tok, P.margin, hs, s_red, dep);
+      signal_done(P.done + o);
+      break;
+    }
   }
   if (tr && threadIdx.x == 0) tr[2] = globaltimer();
 }

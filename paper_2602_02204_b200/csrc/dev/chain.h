@@ -19,6 +19,7 @@ enum ChainOpKind : int {
   CHAIN_ATTN = 3,         // item = attention block * n_kv + kv head
   CHAIN_FINAL = 4,        // item = decode row
   CHAIN_ARGMAX = 5,       // item = decode row
+  CHAIN_HEAD = 6,         // fused final norm + LM head + argmax, item = decode row
 };
 
 constexpr int kChainMaxOps = 48;
@@ -70,7 +71,9 @@ struct ChainParams {
   __nv_bfloat16* hbuf;
   __nv_bfloat16* ring;
   int ring_rows;
-  const float* logits;
+  float* logits;
+  const __nv_bfloat16* lm;
+  int vocab;
   int vocab_pad, argmax_lo, argmax_hi;
   int* tok;
   float* margin;

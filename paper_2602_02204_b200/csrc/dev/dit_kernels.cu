@@ -44,44 +44,6 @@ __global__ void dit_cond_kernel(const DitTokDesc* __restrict__ toks, const __nv_
   }
 }
 
-// dmod[p] = table[id_p]: the adaLN modulation rows are a function of
-// (conditioning id, Euler step) only, precomputed once per stage.
-__global__ void dit_mod_gather_kernel(const DitTokDesc* __restrict__ toks, const float* __restrict__ table,
-                                      int ld4, float4* __restrict__ out) {
-  pdl_wait();
-  pdl_trigger();
-  const int p = blockIdx.x;
-  const float4* src = reinterpret_cast<const float4*>(table) + (size_t)toks[p].id * ld4;
-  float4* dst = out + (size_t)p * ld4;
-  for (int i = threadIdx.x; i < ld4; i += blockDim.x) dst[i] = src[i];
-}
-
-__global__ void dit_to_bf16_kernel(const float* __restrict__ x, int64_t n, __nv_bfloat16* __restrict__ y) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) y[i] = f2bf(x[i]);
-}
-
-__global__ void dit_add_pos_kernel(float* __restrict__ h, const __nv_bfloat16* __restrict__ pos_emb,
-                                   int S, int d, int rows) {
-  pdl_wait();
-  pdl_trigger();
-  const int r = blockIdx.x;
-  const __nv_bfloat16* pe = pos_emb + (size_t)(r % S) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) h[(size_t)r * d + i] += bf2f(pe[i]);
-}
-
-__device__ __forceinline__ float block_sum2(float v, float* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  float t = 0.f;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-  return t;
-}
 
 // a = bf16(LN(h) * (1 + scale) + shift); mod_base == nullptr -> plain LN.
 // LN without affine params, eps 1e-6, two-pass (mean, then centred variance).
@@ -245,24 +207,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// x += dt * v; on the final step also quantise channel 0 to an int32 sample.
-__global__ void dit_euler_kernel(float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
-                                 const float* __restrict__ v, int C, int rows, float dt, int last,
-                                 int32_t* __restrict__ samples) {
-  pdl_wait();
-  pdl_trigger();
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)rows * C) return;
-  const float nx = x[i] + dt * v[i];
-  x[i] = nx;
-  xb[i] = f2bf(nx);  // the next step's input-projection operand (fused to_bf16)
-  if (last && (i % C) == 0) {
-    float q = rintf(kSampleScale * nx);
-    q = fminf(fmaxf(q, -64.f), 63.f);
-    samples[i / C] = (int32_t)q;
-  }
-}
-
 // ---------------------------------------------------------------------------
 cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t seed, float* x,
                       __nv_bfloat16* xb, cudaStream_t st) {
@@ -273,18 +217,6 @@ cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t 
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st) {
   return launch_k(dit_cond_kernel, dim3(n_tok), dim3(256), 0, st, 1, toks, tok_emb, t_emb, step, d, cvec);
-}
-cudaError_t dit_mod_gather(const DitTokDesc* toks, int n_tok, const float* table, int ld_mod, float* out,
-                           cudaStream_t st) {
-  if (ld_mod % 4 != 0) return cudaErrorInvalidValue;
-  return launch_k(dit_mod_gather_kernel, dim3(n_tok), dim3(256), 0, st, 1, toks, table, ld_mod / 4,
-                  reinterpret_cast<float4*>(out));
-}
-cudaError_t dit_to_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st) {
-  return launch_k(dit_to_bf16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, x, n, y);
-}
-cudaError_t dit_add_pos(float* h, const __nv_bfloat16* pos_emb, int S, int d, int rows, cudaStream_t st) {
-  return launch_k(dit_add_pos_kernel, dim3(rows), dim3(256), 0, st, 1, h, pos_emb, S, d, rows);
 }
 cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod_base, const DitTokDesc* toks,
                        int ld_mod, int shift_off, int scale_off, int S, __nv_bfloat16* a, cudaStream_t st) {
@@ -301,11 +233,6 @@ cudaError_t dit_attn(const __nv_bfloat16* qkv, int n_tok, int d, int n_heads, __
                      cudaStream_t st) {
   return launch_k(dit_attn_kernel, dim3((n_tok * n_heads + 7) / 8), dim3(256), 0, st, 1, qkv, n_tok, d, n_heads,
                   out);
-}
-cudaError_t dit_euler(float* x, __nv_bfloat16* xb, const float* v, int C, int rows, float dt, int last,
-                      int32_t* samples, cudaStream_t st) {
-  const int64_t n = (int64_t)rows * C;
-  return launch_k(dit_euler_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, x, xb, v, C, rows, dt, last, samples);
 }
 
 }  // namespace omni_dev

@@ -23,17 +23,11 @@ cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t 
                       __nv_bfloat16* xb, cudaStream_t st);
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st);
-cudaError_t dit_mod_gather(const DitTokDesc* toks, int n_tok, const float* table, int ld_mod, float* out,
-                           cudaStream_t st);
-cudaError_t dit_to_bf16(const float* x, int64_t n, __nv_bfloat16* y, cudaStream_t st);
-cudaError_t dit_add_pos(float* h, const __nv_bfloat16* pos_emb, int S, int d, int rows, cudaStream_t st);
 // mod_base: adaLN table rows of this Euler step ([vocab][ld_mod]); the row of
 // token p is mod_base + toks[p].id * ld_mod. nullptr -> plain LayerNorm.
 cudaError_t dit_ln_mod(const float* h, int rows, int d, const float* mod_base, const DitTokDesc* toks,
                        int ld_mod, int shift_off, int scale_off, int S, __nv_bfloat16* a, cudaStream_t st);
 cudaError_t dit_attn(const __nv_bfloat16* qkv, int n_tok, int d, int n_heads, __nv_bfloat16* out,
                      cudaStream_t st);
-cudaError_t dit_euler(float* x, __nv_bfloat16* xb, const float* v, int C, int rows, float dt, int last,
-                      int32_t* samples, cudaStream_t st);
 
 }  // namespace omni_dev

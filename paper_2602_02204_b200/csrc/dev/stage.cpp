@@ -167,6 +167,8 @@ void build_ar(omni_stage* st) {
   // per-step results [n_dec tokens | n_dec margins] contiguous -> one D2H copy
   st->d_tok = dev_alloc<int32_t>(st, 2 * (size_t)R);
   st->d_margin = reinterpret_cast<float*>(st->d_tok + R);  // unused slot kept for the struct
+  st->head_cnt = dev_alloc<int32_t>(st, (size_t)R);
+  OMNI_CUDA(cudaMemsetAsync(st->head_cnt, 0, (size_t)R * sizeof(int32_t), st->stream));
   st->in_xn = input_of(st->xn, R, d);
   st->in_attn = input_of(st->attn, R, H * kHeadDim);
   st->in_act = input_of(st->act, R, ff);
@@ -274,7 +276,6 @@ void build_dit(omni_stage* st) {
   st->dqkv = dev_alloc<__nv_bfloat16>(st, (size_t)R * 3 * d);
   st->dout = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
   st->du = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
-  st->dv = dev_alloc<float>(st, (size_t)R * C);
   const int cvec_rows = std::max(T, m.vocab);  // per-step rows / adaLN table rows
   st->dcvec = dev_alloc<__nv_bfloat16>(st, (size_t)cvec_rows * d);
   st->dsamples = dev_alloc<int32_t>(st, R);
@@ -450,6 +451,8 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   P.ring = talker ? nullptr : st->ring;
   P.ring_rows = st->ring_rows;
   P.logits = st->logits;
+  P.lm = st->lm.p;
+  P.vocab = m.vocab;
   P.vocab_pad = st->vocab_pad;
   P.argmax_lo = st->argmax_lo;
   P.argmax_hi = st->argmax_hi;
@@ -532,7 +535,9 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     gemm(ly.ggu, 4 * l + 2, mx + 0, st->in_xn, n_rows, EPI_SWIGLU, e);
     gemm(ly.gd, 4 * l + 3, mx + 2, st->in_act, n_rows, EPI_RESID_NORM, r);
   }
-  if (n_dec > 0) {
+  if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
+    add(simple(CHAIN_HEAD, n_dec));
+  } else if (n_dec > 0) {
     add(simple(CHAIN_FINAL, n_dec));
     GemmEpilogue e;
     e.out = st->logits;
@@ -720,15 +725,21 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
         std::tie(r.pf_ptr, r.pf_bytes) = l + 1 < L ? part(st->layers[l + 1].gqkv, 0) : part(st->glm, 0);
         OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, r, s));
       }
-      if (n_dec > 0) {
+      if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
+        // one kernel: final norm (+ hidden ring) -> LM head -> argmax
+        OMNI_KERNEL(launch_head(sd, n_dec, st->x, d, kNormEps, st->hbuf, talker ? nullptr : st->ring,
+                                st->ring_rows, st->lm.p, m.vocab, st->logits, st->vocab_pad, st->argmax_lo,
+                                st->argmax_hi, st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec),
+                                st->head_cnt, s));
+      } else if (n_dec > 0) {
         OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
-                                      talker ? nullptr : st->ring, st->ring_rows, s));
+                                        talker ? nullptr : st->ring, st->ring_rows, s));
         GemmEpilogue e;
         e.out = st->logits;
         e.ldo = st->vocab_pad;
         OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
         OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
-                                st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
+                                  st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
       }
     });
     if (n_dec > 0) {
@@ -1021,6 +1032,9 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     // not the kernel boundary, dominates.
     const char* ce = std::getenv("OMNI_CHAIN");
     st->chain_on = ce && ce[0] == '1';
+    // OMNI_FUSED_HEAD=1: one-kernel head (measured flat at 1 row, slower at 16; default off)
+    const char* fh = std::getenv("OMNI_FUSED_HEAD");
+    st->fused_head = fh && fh[0] == '1';
     if (st->lim.max_batch_tokens <= 0) st->lim.max_batch_tokens = 256;
     if (st->lim.max_resident <= 0) st->lim.max_resident = 64;
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;

@@ -81,6 +81,7 @@ struct omni_stage {
   float* hproj = nullptr;
   float* logits = nullptr;
   int32_t* d_tok = nullptr;
+  int32_t* head_cnt = nullptr;  // fused head: per-decode-row CTA tickets
   float* d_margin = nullptr;
   float* cond_table = nullptr;
   __nv_bfloat16* ring = nullptr;
@@ -95,7 +96,7 @@ struct omni_stage {
   omni_dev::GemmWeight g_in, g_out, g_mod;
   std::vector<omni_dev::DitLayer> dlayers;
   int tok_cap = 0, drows_cap = 0;
-  float *dx = nullptr, *dh = nullptr, *dv = nullptr;
+  float *dx = nullptr, *dh = nullptr;
   float* mod_table = nullptr;  // [T][vocab][L*6*d] adaLN modulation rows
   __nv_bfloat16 *dxin = nullptr, *da = nullptr, *dqkv = nullptr, *dout = nullptr, *du = nullptr,
                 *dcvec = nullptr;
@@ -120,6 +121,7 @@ struct omni_stage {
   // step chain (chain.cu): global TMA descriptors, completion counters
   CUtensorMap* chain_maps = nullptr;
   int* chain_done = nullptr;
+  bool fused_head = false;  // final norm + LM head + argmax in one kernel (vocab <= 256)
   bool chain_on = false;  // small Thinker steps (rows <= 16) as one step-chain launch (OMNI_CHAIN=1)
   unsigned long long* chain_trace = nullptr;  // tools: per-ticket timestamps
   int chain_last_items = 0, chain_last_nops = 0;

@@ -170,3 +170,37 @@ def test_step_chain_bit_identical_to_kernel_chain(kind):
     assert outs[0][0] == outs[1][0]
     for a, b in zip(outs[0][1], outs[1][1]):
         assert np.array_equal(a, b)
+
+
+def test_fused_head_matches_kernel_head(monkeypatch):
+    """OMNI_FUSED_HEAD=1 (final norm + CUDA-core LM head + argmax in one
+    kernel, split over CTAs with a last-CTA argmax) gives the same tokens and
+    bit-identical hidden rows as final_gather + tcgen05 LM GEMM + argmax;
+    logits agree to fp32 summation-order tolerance."""
+    m = D.model_default(D.THINKER, **SMALL)
+    rng = np.random.default_rng(21)
+    prompts = {s: list(rng.integers(1, 256, size=n)) for s, n in ((1, 7), (2, 12), (3, 20), (4, 3))}
+    outs = []
+    for fused in ("1", "0"):
+        monkeypatch.setenv("OMNI_FUSED_HEAD", fused)
+        st = D.Stage(m, D.StageLimits(256, 16, 256, 0, 16), seed=23)
+        for s, p in prompts.items():
+            st.ar_step([s], [D.PREFILL], [len(p)], [0], [-1], p)
+        seqs = sorted(prompts)
+        toks = {s: [] for s in seqs}
+        hids, lgs = [], []
+        for k in range(6):  # repeated steps replay the self-resetting CTA tickets
+            tin = [-1 if k == 0 else toks[s][-1] for s in seqs]
+            t, _ = st.ar_step(seqs, [D.DECODE] * 4, [1] * 4, [len(prompts[s]) + k for s in seqs], [k] * 4, tin)
+            for i, s in enumerate(seqs):
+                toks[s].append(int(t[i]))
+            hids.append(np.stack([D.d2h(st.hidden_row(s, k), (512,), np.uint16) for s in seqs]))
+            lg = st.tensor("buf.logits")
+            lgs.append(D.d2h(lg[0], (4, lg[2]), np.float32)[:, :m.vocab])
+        outs.append((toks, hids, lgs))
+        st.close()
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert np.array_equal(a, b)
+    for a, b in zip(outs[0][2], outs[1][2]):
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-4)
