@@ -36,7 +36,14 @@ namespace {
 
 using namespace gemm_dev;
 
-template <int BN, int STAGES, int EPI>
+// PUSH (decode tiles BN <= 32 with split-K): instead of cluster barrier ->
+// DSMEM pull -> cluster barrier, every split CTA pushes its fp32 partials for
+// the column slice each peer owns straight from the TMEM registers into that
+// peer's receive buffer (st.async, complete_tx on the owner's mbarrier); the
+// owner waits for its bytes only and sums in the same fixed rank order, so
+// results are bit-identical to the pull variant. No barrier at exit: a CTA's
+// smem is only written by peers before its own wait completes.
+template <int BN, int STAGES, int EPI, bool PUSH = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const GemmArgs a) {
@@ -52,11 +59,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = smem + STAGES * kABytes;
   constexpr size_t kPipe = (size_t)STAGES * (kABytes + kBBytes);
   constexpr size_t kEpi = (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (kPipe > kEpi ? kPipe : kEpi));
+  constexpr size_t kMain = kPipe > kEpi ? kPipe : kEpi;
+  constexpr size_t kRecv = PUSH ? (size_t)BN * 128 * 4 : 0;  // [S][128][per] fp32, S * per <= BN
+  float* recv = reinterpret_cast<float*>(smem + kMain);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMain + kRecv);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   float* inv_s = reinterpret_cast<float*>(done + 2);  // [BN] input-RMS scales
+  uint64_t* recv_bar = reinterpret_cast<uint64_t*>(inv_s + BN);
 
   const int warp = warp_id(), lane = lane_id();
   const int n_tile = blockIdx.x, m_tile = blockIdx.y, split = blockIdx.z;
@@ -75,12 +86,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    if (PUSH) mbar_init(recv_bar, 1);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (PUSH) cluster_arrive_relaxed();  // recv_bar initialised; waited on before the first push
   const uint32_t tmem = *tmem_slot;
   pdl_trigger();  // the next kernel may start its own prologue / weight prefetch
   if (tr && threadIdx.x == 0) tr[1] = clock64() - c0;
@@ -153,6 +166,63 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int cols = min(BN, a.M - m0);           // live token columns
   const int chunks = (cols + 15) / 16;
   float* red = reinterpret_cast<float*>(smem);  // pipeline smem is free now
+  if constexpr (PUSH) {
+    const int S = a.splits;
+    const int per = (cols + S - 1) / S;
+    const int cb0 = split * per;
+    const int cb1 = min(cols, cb0 + per);
+    const int n_me = cb1 > cb0 ? cb1 - cb0 : 0;
+    if (threadIdx.x == 0 && n_me > 0) mbar_expect_tx(recv_bar, (uint32_t)((S - 1) * 128 * n_me * 4));
+    cluster_wait();  // every peer's recv_bar is initialised
+    const uint32_t recv_s = smem_addr(recv), bar_s = smem_addr(recv_bar);
+    for (int c = 0; c < chunks; ++c) {
+      float v[16];
+      tmem_ld16(trow + c * 16, v);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const int col = c * 16 + j;
+        if (col >= cols) break;
+        const int r0 = col / per;
+        const bool pair = col + 1 < cols && (col + 1) / per == r0 && ((col - r0 * per) & 1) == 0 && (per & 1) == 0;
+        if (pair) {
+          if (r0 == split) {
+            red[(col - cb0) * 128 + row] = v[j];
+            red[(col + 1 - cb0) * 128 + row] = v[j + 1];
+          } else {
+            const uint32_t off = (uint32_t)(((split * 128 + row) * per + (col - r0 * per)) * 4);
+            st_async_f32x2(dsmem_map(recv_s + off, r0), v[j], v[j + 1], dsmem_map(bar_s, r0));
+          }
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = col + h;
+            if (cc >= cols) break;
+            const int r = cc / per;
+            if (r == split) {
+              red[(cc - cb0) * 128 + row] = v[j + h];
+            } else {
+              const uint32_t off = (uint32_t)(((split * 128 + row) * per + (cc - r * per)) * 4);
+              st_async_f32(dsmem_map(recv_s + off, r), v[j + h], dsmem_map(bar_s, r));
+            }
+          }
+        }
+      }
+    }
+    if (tr && threadIdx.x == 0) tr[5] = clock64() - c0;
+    if (n_me > 0) {
+      mbar_wait(recv_bar, 0);
+      // fixed rank order, own partial in place: identical sums to the pull variant
+      for (int k = 0; k < n_me; ++k) {
+        float acc = 0.f;
+        for (int z = 0; z < S; ++z) {
+          const float x = z == split ? red[k * 128 + row] : recv[(z * 128 + row) * per + k];
+          acc = z == 0 ? x : acc + x;
+        }
+        red[k * 128 + row] = acc;
+      }
+      epi_cols<EPI>(a, n_tile, m0 + cb0, n_me, red, inv_s + cb0);  // syncs before reading the slice
+    }
+  } else {
   for (int c = 0; c < chunks; ++c) {
     float v[16];
     tmem_ld16(trow + c * 16, v);
@@ -191,6 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (c1 > c0) epi_cols<EPI>(a, n_tile, m0 + c0, c1 - c0, fin, inv_s + c0);
     cluster_sync();  // keep our partial alive until every rank has read it
   }
+  }  // !PUSH
 
   tc_fence_before();
   __syncthreads();
@@ -214,18 +285,23 @@ template <int BN>
 constexpr size_t epi_smem_for() {
   return (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
 }
-template <int BN, int STAGES = stages_for<BN>()>
+template <int BN, int STAGES = stages_for<BN>(), bool PUSH = false>
 constexpr size_t smem_for() {
   constexpr size_t pipe = STAGES * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
-  // + barriers / tmem slot (256 B) + per-column input-RMS scales (4 B x BN) + flag
-  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + 256 + 4 * BN + 16;
+  // + [push receive buffer] + barriers / tmem slot (256 B) + per-column
+  // input-RMS scales (4 B x BN) + flag / receive barrier
+  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + (PUSH ? (size_t)BN * 128 * 4 : 0) + 256 +
+         4 * BN + 16;
 }
+// push split-K variants keep two CTAs per SM (<= ~113 KB): one stage less
+static_assert(smem_for<16, 5, true>() <= 113 * 1024, "BN16 push tile must fit twice per SM");
+static_assert(smem_for<32, 4, true>() <= 113 * 1024, "BN32 push tile must fit twice per SM");
 
-template <int BN, int EPI, int STAGES = stages_for<BN>()>
+template <int BN, int EPI, int STAGES = stages_for<BN>(), bool PUSH = false>
 cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                       cudaStream_t st) {
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI>;
-  constexpr size_t smem = smem_for<BN, STAGES>();
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, PUSH>;
+  constexpr size_t smem = smem_for<BN, STAGES, PUSH>();
   static std::atomic<uint64_t> configured{0};  // per instantiation, per device
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
   if (a.splits > 8) {  // 16-CTA clusters are non-portable (opt-in)
@@ -262,9 +338,15 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
       }
     }
   }
+  static const bool push = [] {  // OMNI_SPLITK_PUSH=0: cluster-barrier + DSMEM-pull reduction
+    const char* e = std::getenv("OMNI_SPLITK_PUSH");
+    return !(e && e[0] == '0');
+  }();
   switch (bn_for(w, a.M)) {
-    case 16: return launch_bn<16, EPI>(w, x, a, st);
-    case 32: return launch_bn<32, EPI>(w, x, a, st);
+    case 16:
+      return push && a.splits > 1 ? launch_bn<16, EPI, 5, true>(w, x, a, st) : launch_bn<16, EPI>(w, x, a, st);
+    case 32:
+      return push && a.splits > 1 ? launch_bn<32, EPI, 4, true>(w, x, a, st) : launch_bn<32, EPI>(w, x, a, st);
     case 64: return launch_bn<64, EPI>(w, x, a, st);
     case 128: return launch_bn<128, EPI>(w, x, a, st);
     default: return launch_bn<256, EPI>(w, x, a, st);

@@ -179,6 +179,27 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Split cluster barrier: arrive early (relaxed: orders nothing but the
+// preceding mbarrier init fence), wait much later.
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+// Remote (DSMEM) register stores that complete_tx on the TARGET CTA's
+// mbarrier: fire-and-forget, no source buffer to keep alive.
+__device__ __forceinline__ void st_async_f32(uint32_t cluster_saddr, float v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [%0], %1, [%2];" ::"r"(cluster_saddr),
+               "f"(v), "r"(cluster_bar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_f32x2(uint32_t cluster_saddr, float v0, float v1, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+                   cluster_saddr),
+               "f"(v0), "f"(v1), "r"(cluster_bar)
+               : "memory");
+}
 // Address of the same smem variable in CTA `rank` of this cluster.
 __device__ __forceinline__ uint32_t dsmem_map(uint32_t local_saddr, uint32_t rank) {
   uint32_t r;
