@@ -242,6 +242,12 @@ omni_status omni_k_gemm_trace(const uint64_t* Ws, int32_t n_w, int32_t N, int32_
                               int32_t epi, uint64_t out, int32_t ldo, int32_t max_splits, uint64_t trace_dev,
                               int32_t* grid_ctas);
 
+/* Debug phase traces (tools/attn_trace.py); 0 disables. attn_trace: 8 u64
+ * globaltimer stamps per attention CTA, indexed (layer, kv_head, block);
+ * gemm_marks: 3 u64 atomic-max marks (last QKV CTA exit, last O-projection
+ * producer past its PDL wait, last O-projection CTA exit). */
+omni_status omni_k_debug_traces(uint64_t attn_trace, uint64_t gemm_marks);
+
 #ifdef __cplusplus
 }
 #endif

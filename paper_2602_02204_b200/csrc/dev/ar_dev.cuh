@@ -138,7 +138,8 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
                                                 const __nv_bfloat16* __restrict__ q, int n_heads, int n_kv,
                                                 int layer, int n_layers, const __nv_bfloat16* __restrict__ kv,
                                                 __nv_bfloat16* __restrict__ out, float scale,
-                                                AttnSmem<kAttnWarps, kAttnChunk>& sm, Dep dep) {
+                                                AttnSmem<kAttnWarps, kAttnChunk>& sm, Dep dep,
+                                                unsigned long long* tr = nullptr) {
   constexpr int HD = kHeadDim;
   constexpr uint32_t PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB K or V slice of one page
   constexpr int kAttnPagesPerChunk = kAttnChunk / kPageTokens;
@@ -177,10 +178,12 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
     }
   };
   if (threadIdx.x == 0) {
+    if (tr) tr[0] = globaltimer();
     issue(0, 0, 0);
     if (n_chunks > 1) issue(1, 1, 0);
   }
   dep();
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer();
   if (threadIdx.x == 0) {
     issue(0, 0, 1);
     if (n_chunks > 1) issue(1, 1, 1);
@@ -194,6 +197,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
     sm.q[qi][c2] = make_float2(__low2float(v) * scale, __high2float(v) * scale);
   }
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[2] = globaltimer();
 
   constexpr int QW = kAttnQMax / kAttnWarps;  // query vectors per warp (prefill blocks)
   constexpr int KG = kAttnChunk / 32;          // 32-key groups per chunk
@@ -214,6 +218,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
   for (int c = 0; c < n_chunks; ++c) {
     const int buf = c & 1;
     mbar_wait(&sm.bar[buf], (c >> 1) & 1);
+    if (tr && c == 0 && threadIdx.x == 0) tr[3] = globaltimer();
     const int kbase = c * kAttnChunk;
     const __nv_bfloat162* K2 = reinterpret_cast<const __nv_bfloat162*>(sm.k[buf]);
     const __nv_bfloat16* V = sm.v[buf];
@@ -236,7 +241,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
 #pragma unroll 8
           for (int cp = 0; cp < HD / 2; ++cp) {
             const int x = (cp + lane) & (HD / 2 - 1);  // rotated: distinct banks per lane
-            const float2 kv2 = __bfloat1622float2(kr[x]);
+            const float2 kv2 = __bfloat1622float2(kr[(kv_swz(x >> 2, key) << 2) | (x & 3)]);
             const float2 qv = sm.q[qi][x];
             a0 += qv.x * kv2.x;
             a1 += qv.y * kv2.y;
@@ -268,7 +273,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
 #pragma unroll 4
         for (int k = 32 * i; k < kend_i; ++k) {
           const float pk = sm.p[warp][k];
-          const uint2 raw = *reinterpret_cast<const uint2*>(V + k * HD + lane * 4);
+          const uint2 raw = *reinterpret_cast<const uint2*>(V + k * HD + (kv_swz(lane >> 1, k) << 3) + (lane & 1) * 4);
           const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
           const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
           o0 += pk * v01.x;
@@ -286,6 +291,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
       issue(c + 2, buf, 1);
     }
   }
+  if (tr && threadIdx.x == 0) tr[4] = globaltimer();
   if (per > 1) {
     // merge the `per` partial (max, sum, acc) states of each query vector
     const int qi = warp / per;
@@ -316,6 +322,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
       op[0] = __floats2bfloat162_rn(o[0] * inv, o[1] * inv);
       op[1] = __floats2bfloat162_rn(o[2] * inv, o[3] * inv);
     }
+    if (tr && threadIdx.x == 0) tr[5] = globaltimer();
     return;
   }
 #pragma unroll
@@ -328,6 +335,252 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
     op[0] = __floats2bfloat162_rn(acc[j][0] * inv, acc[j][1] * inv);
     op[1] = __floats2bfloat162_rn(acc[j][2] * inv, acc[j][3] * inv);
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Paged causal attention on the warp MMA (blocks with <= 16 query vectors:
+// every decode block, and prefill blocks of <= 16 / group tokens). The block's
+// query vectors are the M = 16 rows of mma.sync m16n8k16; each warp owns 16
+// keys of every staged chunk (CHUNK = 16 * W): S = Q K^T from ldmatrix'ed K
+// rows (swizzled page rows, conflict-free), online softmax on the accumulator
+// fragments (fp32, exp2), O += P V with P split into bf16 hi + lo halves
+// (two MMAs: ~fp32 precision of the probabilities), V by ldmatrix.trans.
+// The W per-warp (max, sum, O) states merge in fixed warp order at the end.
+// Same staging / PDL structure as attention_block. ~10x fewer instructions
+// than the CUDA-core loop (which issue-bound the decode step).
+// ---------------------------------------------------------------------------
+template <int W, int CHUNK, class Dep>
+__device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const ArStepDev& s,
+                                                    const __nv_bfloat16* __restrict__ q, int n_heads, int n_kv,
+                                                    int layer, int n_layers, const __nv_bfloat16* __restrict__ kv,
+                                                    __nv_bfloat16* __restrict__ out, float scale,
+                                                    AttnSmem<W, CHUNK>& sm, Dep dep,
+                                                    unsigned long long* tr = nullptr) {
+  static_assert(CHUNK == 16 * W, "one 16-key MMA slab per warp per chunk");
+  constexpr int HD = kHeadDim;
+  constexpr uint32_t PAGE_BYTES = kPageTokens * HD * 2;
+  constexpr int kPagesPerChunk = CHUNK / kPageTokens;
+  const AttnBlockDesc blk = s.attn_blocks[blk_idx];
+  const ArEntryDesc ed = s.entries[blk.entry];
+  const int group = n_heads / n_kv;
+  const int nq = blk.ntok * group;  // <= 16
+  const int kend = ed.pos0 + blk.tok0 + blk.ntok;
+  const int n_chunks = (kend + CHUNK - 1) / CHUNK;
+  const int warp = warp_id(), lane = lane_id();
+  const int g = lane >> 2, t4 = lane & 3;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    fence_barrier_init();
+  }
+  auto issue = [&](int c, int buf, int part) {
+    const int first = c * kPagesPerChunk;
+    const int keys = min(CHUNK, kend - c * CHUNK);
+    const int np = (keys + kPageTokens - 1) / kPageTokens;
+    if (part == 0) mbar_expect_tx(&sm.bar[buf], 2u * PAGE_BYTES * np);
+    for (int i = 0; i < np; ++i) {
+      const bool history = (first + i + 1) * kPageTokens <= ed.pos0;
+      if (history != (part == 0)) continue;
+      const int page = s.page_table[blk.entry * s.max_pages + first + i];
+      const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
+      bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
+      bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
+                &sm.bar[buf]);
+    }
+  };
+  if (threadIdx.x == 0) {
+    if (tr) tr[0] = globaltimer();
+    issue(0, 0, 0);
+    if (n_chunks > 1) issue(1, 1, 0);
+  }
+  dep();
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer();
+  if (threadIdx.x == 0) {
+    issue(0, 0, 1);
+    if (n_chunks > 1) issue(1, 1, 1);
+  }
+  __syncthreads();  // barrier init visible before any wait
+
+  // Q fragments (rows g, g + 8; 8 k-steps of 16 head dims) straight from the bf16 q rows
+  uint32_t qa[8][4];
+  int qpos_lo = -1, qpos_hi = -1;  // causal limit of rows g and g + 8 (-1: padding row)
+  {
+    const __nv_bfloat16* r_lo = nullptr;
+    const __nv_bfloat16* r_hi = nullptr;
+    if (g < nq) {
+      r_lo = q + (size_t)(ed.row0 + blk.tok0 + g / group) * n_heads * HD + (kh * group + g % group) * HD;
+      qpos_lo = ed.pos0 + blk.tok0 + g / group;
+    }
+    if (g + 8 < nq) {
+      r_hi = q + (size_t)(ed.row0 + blk.tok0 + (g + 8) / group) * n_heads * HD + (kh * group + (g + 8) % group) * HD;
+      qpos_hi = ed.pos0 + blk.tok0 + (g + 8) / group;
+    }
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int d0 = ks * 16 + 2 * t4;
+      qa[ks][0] = r_lo ? *reinterpret_cast<const uint32_t*>(r_lo + d0) : 0u;
+      qa[ks][1] = r_hi ? *reinterpret_cast<const uint32_t*>(r_hi + d0) : 0u;
+      qa[ks][2] = r_lo ? *reinterpret_cast<const uint32_t*>(r_lo + d0 + 8) : 0u;
+      qa[ks][3] = r_hi ? *reinterpret_cast<const uint32_t*>(r_hi + d0 + 8) : 0u;
+    }
+  }
+  if (tr && threadIdx.x == 0) tr[2] = globaltimer();
+  const float sl2 = scale * 1.4426950408889634f;  // scores in log2 units
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+  float o[16][4];
+#pragma unroll
+  for (int nd = 0; nd < 16; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
+
+  for (int c = 0; c < n_chunks; ++c) {
+    const int buf = c & 1;
+    mbar_wait(&sm.bar[buf], (c >> 1) & 1);
+    if (tr && c == 0 && threadIdx.x == 0) tr[3] = globaltimer();
+    const int k0 = c * CHUNK + warp * 16;  // this warp's first key
+    // warp-uniform skip: no key of the slab is visible to any row of the block
+    const int blk_qmax = ed.pos0 + blk.tok0 + blk.ntok - 1;
+    if (k0 <= blk_qmax) {
+      const uint32_t kb = smem_addr(sm.k[buf]), vb = smem_addr(sm.v[buf]);
+      // ---- S = Q K^T (16 x 16 keys) ----
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      {
+        // ldmatrix x4: matrices (keys 0-7 | 8-15) x (dims lo 8 | hi 8) of k-step ks
+        const int mi = lane >> 3, ri = lane & 7;
+        const int key = warp * 16 + (mi >> 1) * 8 + ri;  // row within the chunk buffer
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int chunk = ks * 2 + (mi & 1);
+          uint32_t b[4];
+          ldsm_x4(b, kb + (uint32_t)((key * HD + kv_swz(chunk, key) * 8) * 2));
+          mma_bf16_16816(sc[0], qa[ks], b[0], b[1]);
+          mma_bf16_16816(sc[1], qa[ks], b[2], b[3]);
+        }
+      }
+      // ---- causal mask + online softmax (rows g / g + 8; 4 lanes per row) ----
+      float mx_lo = -INFINITY, mx_hi = -INFINITY;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = k0 + nb * 8 + 2 * t4 + e;
+          sc[nb][e] = key <= qpos_lo ? sc[nb][e] * sl2 : -INFINITY;
+          sc[nb][2 + e] = key <= qpos_hi ? sc[nb][2 + e] * sl2 : -INFINITY;
+          mx_lo = fmaxf(mx_lo, sc[nb][e]);
+          mx_hi = fmaxf(mx_hi, sc[nb][2 + e]);
+        }
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+      mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+      mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+      const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
+      const float cr_lo = mn_lo == -INFINITY ? 1.f : exp2f(m_lo - mn_lo);
+      const float cr_hi = mn_hi == -INFINITY ? 1.f : exp2f(m_hi - mn_hi);
+      float ps_lo = 0.f, ps_hi = 0.f;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          sc[nb][e] = mn_lo == -INFINITY ? 0.f : exp2f(sc[nb][e] - mn_lo);
+          sc[nb][2 + e] = mn_hi == -INFINITY ? 0.f : exp2f(sc[nb][2 + e] - mn_hi);
+          ps_lo += sc[nb][e];
+          ps_hi += sc[nb][2 + e];
+        }
+      ps_lo += __shfl_xor_sync(0xffffffffu, ps_lo, 1);
+      ps_lo += __shfl_xor_sync(0xffffffffu, ps_lo, 2);
+      ps_hi += __shfl_xor_sync(0xffffffffu, ps_hi, 1);
+      ps_hi += __shfl_xor_sync(0xffffffffu, ps_hi, 2);
+      l_lo = l_lo * cr_lo + ps_lo;
+      l_hi = l_hi * cr_hi + ps_hi;
+      m_lo = mn_lo;
+      m_hi = mn_hi;
+#pragma unroll
+      for (int nd = 0; nd < 16; ++nd) {
+        o[nd][0] *= cr_lo, o[nd][1] *= cr_lo;
+        o[nd][2] *= cr_hi, o[nd][3] *= cr_hi;
+      }
+      // ---- O += P V: P as bf16 hi + lo A fragments ----
+      uint32_t ph[4], pl[4];
+      {
+        const float p[4][2] = {{sc[0][0], sc[0][1]}, {sc[0][2], sc[0][3]}, {sc[1][0], sc[1][1]}, {sc[1][2], sc[1][3]}};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const __nv_bfloat162 h = __floats2bfloat162_rn(p[r][0], p[r][1]);
+          const float2 hf = __bfloat1622float2(h);
+          ph[r] = *reinterpret_cast<const uint32_t*>(&h);
+          pl[r] = pack_bf16x2(p[r][0] - hf.x, p[r][1] - hf.y);
+        }
+      }
+      {
+        // ldmatrix.trans x4: (keys 0-7 | 8-15) x (dims nd*8 | (nd+1)*8)
+        const int mi = lane >> 3, ri = lane & 7;
+        const int vk = blk_qmax + 1 - k0;  // valid keys of the slab (>= 1)
+        auto pair_mask = [&](int k) {
+          return (k < vk ? 0x0000ffffu : 0u) | (k + 1 < vk ? 0xffff0000u : 0u);
+        };
+        const uint32_t vm_lo = pair_mask(2 * t4), vm_hi = pair_mask(8 + 2 * t4);
+        const int key = warp * 16 + (mi & 1) * 8 + ri;
+#pragma unroll
+        for (int nd = 0; nd < 16; nd += 2) {
+          const int chunk = nd + (mi >> 1);
+          uint32_t b[4];
+          ldsm_x4_t(b, vb + (uint32_t)((key * HD + kv_swz(chunk, key) * 8) * 2));
+          // keys past the context hold stale smem / page bytes: P is 0 there,
+          // and V must be too (0 * NaN)
+          b[0] &= vm_lo, b[2] &= vm_lo;
+          b[1] &= vm_hi, b[3] &= vm_hi;
+          mma_bf16_16816(o[nd], ph, b[0], b[1]);
+          mma_bf16_16816(o[nd], pl, b[0], b[1]);
+          mma_bf16_16816(o[nd + 1], ph, b[2], b[3]);
+          mma_bf16_16816(o[nd + 1], pl, b[2], b[3]);
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with `buf`
+    if (threadIdx.x == 0 && c + 2 < n_chunks) {
+      issue(c + 2, buf, 0);
+      issue(c + 2, buf, 1);
+    }
+  }
+  if (tr && threadIdx.x == 0) tr[4] = globaltimer();
+  // ---- merge the W warp states in fixed warp order (K/V buffers are free) ----
+  float* mo = reinterpret_cast<float*>(&sm.k[0][0]);  // [W][16][HD]
+  float* ml = reinterpret_cast<float*>(&sm.v[0][0]);  // [W][16][2]
+  if (t4 == 0) {
+    ml[(warp * 16 + g) * 2 + 0] = m_lo;
+    ml[(warp * 16 + g) * 2 + 1] = l_lo;
+    ml[(warp * 16 + g + 8) * 2 + 0] = m_hi;
+    ml[(warp * 16 + g + 8) * 2 + 1] = l_hi;
+  }
+#pragma unroll
+  for (int nd = 0; nd < 16; ++nd) {
+    const int d0 = nd * 8 + 2 * t4;
+    if (g < nq) *reinterpret_cast<float2*>(mo + (warp * 16 + g) * HD + d0) = make_float2(o[nd][0], o[nd][1]);
+    if (g + 8 < nq)
+      *reinterpret_cast<float2*>(mo + (warp * 16 + g + 8) * HD + d0) = make_float2(o[nd][2], o[nd][3]);
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < nq * (HD / 2); idx += W * 32) {
+    const int r = idx / (HD / 2), d0 = (idx % (HD / 2)) * 2;
+    float mt = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < W; ++w) mt = fmaxf(mt, ml[(w * 16 + r) * 2]);
+    float lt = 0.f, a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const float mw = ml[(w * 16 + r) * 2];
+      const float f = mw == -INFINITY ? 0.f : exp2f(mw - mt);
+      lt += ml[(w * 16 + r) * 2 + 1] * f;
+      const float2 v = *reinterpret_cast<const float2*>(mo + (w * 16 + r) * HD + d0);
+      a0 += v.x * f;
+      a1 += v.y * f;
+    }
+    const float inv = 1.f / lt;
+    const int tok = blk.tok0 + r / group, hq = kh * group + r % group;
+    *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + d0) =
+        __floats2bfloat162_rn(a0 * inv, a1 * inv);
+  }
+  if (tr && threadIdx.x == 0) tr[5] = globaltimer();
 }
 
 // ---------------------------------------------------------------------------

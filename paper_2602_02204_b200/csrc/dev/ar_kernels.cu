@@ -37,6 +37,11 @@ __global__ void gather_cond_kernel(const ArStepDev s, int d, __nv_bfloat16* __re
   gather_cond_row(blockIdx.x, s, d, out, PdlDep{});
 }
 
+// Debug phase trace of the attention CTAs (omni_k_attn_trace; null = off):
+// 8 globaltimer stamps per CTA of the LAST attention launch.
+__device__ unsigned long long* g_attn_trace = nullptr;
+cudaError_t attn_trace_set(void* p) { return cudaMemcpyToSymbol(g_attn_trace, &p, sizeof(p)); }
+
 constexpr int kAttnWarps = 8;
 constexpr int kAttnChunk = 128;
 using AttnSmemK = AttnSmem<kAttnWarps, kAttnChunk>;
@@ -50,8 +55,16 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   // static weights of a later GEMM (OMNI_PF_MB, default off)
   prefetch_l2_share(pf_ptr, pf_bytes, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y,
                     threadIdx.x, blockDim.x);
-  attention_block<kAttnWarps, kAttnChunk>(blockIdx.x, blockIdx.y, s, q, n_heads, n_kv, layer, n_layers, kv, out,
-                                          scale, *reinterpret_cast<AttnSmemK*>(attn_smem_raw), PdlDep{});
+  unsigned long long* tr = g_attn_trace;
+  if (tr) tr += 8ull * ((layer * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+  const AttnBlockDesc blk = s.attn_blocks[blockIdx.x];
+  if (blk.ntok * (n_heads / n_kv) <= 16)
+    attention_block_mma<kAttnWarps, kAttnChunk>(blockIdx.x, blockIdx.y, s, q, n_heads, n_kv, layer, n_layers, kv,
+                                                out, scale, *reinterpret_cast<AttnSmemK*>(attn_smem_raw), PdlDep{},
+                                                tr);
+  else
+    attention_block<kAttnWarps, kAttnChunk>(blockIdx.x, blockIdx.y, s, q, n_heads, n_kv, layer, n_layers, kv, out,
+                                            scale, *reinterpret_cast<AttnSmemK*>(attn_smem_raw), PdlDep{}, tr);
 }
 
 __global__ void final_gather_kernel(const ArStepDev s, const float* __restrict__ x, int d, float eps,

@@ -61,6 +61,7 @@ cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, i
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
                                 cudaStream_t st);
 // Fused final RMSNorm + LM head (CUDA cores) + greedy argmax, vocab <= 256.
+cudaError_t attn_trace_set(void* p);  // debug: per-CTA phase stamps of attention launches
 // Grid (vocab / kHeadIdsPerCta, n_dec); cnt = n_dec zeroed tickets (self-resetting).
 constexpr int kHeadMaxVocab = 256;
 constexpr int kHeadIdsPerCta = 16;

@@ -11,6 +11,8 @@
 #include "omni_dev.h"
 
 namespace omni_dev {
+cudaError_t gemm_marks_set(void* p);
+cudaError_t attn_trace_set(void* p);
 
 namespace {
 thread_local std::string g_last_error;
@@ -249,6 +251,13 @@ omni_status omni_k_gemm_trace(const uint64_t* Ws, int32_t n_w, int32_t N, int32_
     OMNI_CUDA(cudaStreamSynchronize(cs));
     cudaStreamDestroy(cs);
     if (grid_ctas) *grid_ctas = (N_pad / 128) * ((M + gemm_block_n(M) - 1) / gemm_block_n(M)) * ws[0].splits;
+  });
+}
+
+omni_status omni_k_debug_traces(uint64_t attn_trace, uint64_t gemm_marks) {
+  return guarded([&] {
+    OMNI_CUDA(attn_trace_set(reinterpret_cast<void*>(attn_trace)));
+    OMNI_CUDA(gemm_marks_set(reinterpret_cast<void*>(gemm_marks)));
   });
 }
 

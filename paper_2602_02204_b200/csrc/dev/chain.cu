@@ -281,9 +281,14 @@ __global__ void __launch_bounds__(kChainThreads, 2) step_chain_kernel(const __gr
       signal_done(P.done + o);
       break;
     case CHAIN_ATTN:
-      attention_block<kChainAttnWarps, kChainAttnChunk>(
-          item / P.n_kv, item % P.n_kv, P.sd, P.q, P.n_heads, P.n_kv, op.layer, P.n_layers, P.kv, P.attn,
-          P.attn_scale, *reinterpret_cast<ChainAttnSmem*>(chain_smem), dep);
+      if (P.sd.attn_blocks[item / P.n_kv].ntok * (P.n_heads / P.n_kv) <= 16)
+        attention_block_mma<kChainAttnWarps, kChainAttnChunk>(
+            item / P.n_kv, item % P.n_kv, P.sd, P.q, P.n_heads, P.n_kv, op.layer, P.n_layers, P.kv, P.attn,
+            P.attn_scale, *reinterpret_cast<ChainAttnSmem*>(chain_smem), dep);
+      else
+        attention_block<kChainAttnWarps, kChainAttnChunk>(
+            item / P.n_kv, item % P.n_kv, P.sd, P.q, P.n_heads, P.n_kv, op.layer, P.n_layers, P.kv, P.attn,
+            P.attn_scale, *reinterpret_cast<ChainAttnSmem*>(chain_smem), dep);
       signal_done(P.done + o);
       break;
     case CHAIN_FINAL:

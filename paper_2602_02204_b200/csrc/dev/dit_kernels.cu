@@ -101,14 +101,6 @@ __global__ void __launch_bounds__(256)
 // bf16 QKV rows), softmax in fp32 on the accumulator fragments (row = 4
 // lanes), P.V in fp32 on the CUDA cores (lane = 4 head dims, V rows read
 // once per warp, coalesced).
-__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
-                                               uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
 __global__ void __launch_bounds__(256)
     dit_attn_kernel(const __nv_bfloat16* __restrict__ qkv, int n_tok, int d, int n_heads,

@@ -115,9 +115,13 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
         const int is_v = head >= rp.n_heads + rp.n_kv;
         const int kh = head - rp.n_heads - (is_v ? rp.n_kv : 0);
         const int page = rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens];
+        const int pt = rd.pos % kPageTokens;
         dst = rp.kv +
               ((((size_t)page * rp.n_layers + rp.layer) * 2 + is_v) * rp.n_kv + kh) * kPageTokens * 128 +
-              (size_t)(rd.pos % kPageTokens) * 128;
+              (size_t)pt * 128;
+        st8_bf16(dst + kv_swz(f0 >> 3, pt) * 8, o0);  // swizzled 16-byte chunks (ptx.cuh kv_swz)
+        st8_bf16(dst + kv_swz(8 + (f0 >> 3), pt) * 8, o1);
+        continue;
       }
       st8_bf16(dst + f0, o0);
       st8_bf16(dst + 64 + f0, o1);

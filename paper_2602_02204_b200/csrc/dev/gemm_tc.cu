@@ -30,6 +30,10 @@
 
 namespace omni_dev {
 
+// debug marks (omni_k_debug_traces, tools/attn_trace.py; null = off)
+__device__ unsigned long long* g_gemm_marks = nullptr;
+cudaError_t gemm_marks_set(void* p) { return cudaMemcpyToSymbol(g_gemm_marks, &p, sizeof(p)); }
+
 static int bn_for(const GemmWeight& w, int M);  // token-tile width for (weight, batch)
 
 namespace {
@@ -110,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(sA + i * kABytes, &tmW, &full[i], (kb0 + i) * kBlockK, n_tile * kBlockM, pol_w);
       }
       pdl_wait();
+      if (g_gemm_marks && EPI == EPI_RESID_NORM && a.K == 2048) atomicMax(g_gemm_marks + 1, globaltimer());
       if (tr) tr[2] = clock64() - c0;
       for (int i = 0; i < pre; ++i)
         tma_load_2d(sB + i * kBBytes, &tmX, &full[i], (kb0 + i) * kBlockK, m_tile * BN, pol_x);
@@ -266,6 +271,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_free<kTmemCols>(tmem);
+  if (g_gemm_marks && threadIdx.x == 0) {
+    if (EPI == EPI_ROPE_KV) atomicMax(g_gemm_marks + 0, globaltimer());
+    if (EPI == EPI_RESID_NORM && a.K == 2048) atomicMax(g_gemm_marks + 2, globaltimer());
+  }
   if (tr && threadIdx.x == 0) {
     tr[6] = clock64() - c0;
     tr[7] = globaltimer();
