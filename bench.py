@@ -325,7 +325,7 @@ def main() -> None:
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic: gen_workload(n=100, seed=7) prompts, random-init weights (counter RNG)",
-        "config": {"workload": "omni3 = reference.json Thinker->Talker->Code2Wav, closed loop 16, "
+        "config": {"workload": f"omni3 = reference.json Thinker->Talker->Code2Wav, closed loop {args.concurrency}, "
                                "streaming chunks 4/8, all stages on each GPU (replica per rank)",
                    "n_requests_per_step": args.n, "concurrency": args.concurrency,
                    "models": "thinker 8L d2048 (16q/4kv heads, ffn 8192, V256); talker 4L d2048 (V64); "
