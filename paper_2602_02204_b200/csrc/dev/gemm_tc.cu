@@ -47,10 +47,11 @@ using namespace gemm_dev;
 // owner waits for its bytes only and sums in the same fixed rank order, so
 // results are bit-identical to the pull variant. No barrier at exit: a CTA's
 // smem is only written by peers before its own wait completes.
-template <int BN, int STAGES, int EPI, bool PUSH = false>
+template <int BN, int STAGES, int EPI, int kPushS = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const GemmArgs a) {
+  constexpr bool PUSH = kPushS > 0;
   constexpr uint32_t kABytes = kBlockM * kBlockK * 2;
   constexpr uint32_t kBBytes = BN * kBlockK * 2;
   constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
@@ -172,44 +173,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int chunks = (cols + 15) / 16;
   float* red = reinterpret_cast<float*>(smem);  // pipeline smem is free now
   if constexpr (PUSH) {
-    const int S = a.splits;
-    const int per = (cols + S - 1) / S;
-    const int cb0 = split * per;
-    const int cb1 = min(cols, cb0 + per);
-    const int n_me = cb1 > cb0 ? cb1 - cb0 : 0;
-    if (threadIdx.x == 0 && n_me > 0) mbar_expect_tx(recv_bar, (uint32_t)((S - 1) * 128 * n_me * 4));
+    // Fixed slices of kPer = BN / kPushS token columns per rank (compile-time:
+    // fully unrolled, vector stores); a rank whose slice holds no live column
+    // receives nothing. Which rank sums a column does not change its sum order.
+    constexpr int S = kPushS, kPer = BN / kPushS;
+    const int cb0 = split * kPer;
+    const int n_me = min(kPer, cols - cb0);  // live columns of my slice (<= 0: none)
+    if (threadIdx.x == 0 && n_me > 0) mbar_expect_tx(recv_bar, (uint32_t)((S - 1) * 128 * kPer * 4));
     cluster_wait();  // every peer's recv_bar is initialised
-    const uint32_t recv_s = smem_addr(recv), bar_s = smem_addr(recv_bar);
-    for (int c = 0; c < chunks; ++c) {
-      float v[16];
-      tmem_ld16(trow + c * 16, v);
+    const uint32_t recv_s = smem_addr(recv) + (uint32_t)((split * 128 + row) * kPer * 4), bar_s = smem_addr(recv_bar);
+    float v[BN];
 #pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const int col = c * 16 + j;
-        if (col >= cols) break;
-        const int r0 = col / per;
-        const bool pair = col + 1 < cols && (col + 1) / per == r0 && ((col - r0 * per) & 1) == 0 && (per & 1) == 0;
-        if (pair) {
-          if (r0 == split) {
-            red[(col - cb0) * 128 + row] = v[j];
-            red[(col + 1 - cb0) * 128 + row] = v[j + 1];
-          } else {
-            const uint32_t off = (uint32_t)(((split * 128 + row) * per + (col - r0 * per)) * 4);
-            st_async_f32x2(dsmem_map(recv_s + off, r0), v[j], v[j + 1], dsmem_map(bar_s, r0));
-          }
+    for (int c = 0; c < BN / 16; ++c)
+      if (c < chunks) tmem_ld16(trow + c * 16, *reinterpret_cast<float(*)[16]>(v + c * 16));
+#pragma unroll
+    for (int r = 0; r < S; ++r) {
+      if (r * kPer >= cols) break;  // no live column from here on (uniform)
+      if (r == split) {
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) red[k * 128 + row] = v[r * kPer + k];
+      } else {
+        const uint32_t dst = dsmem_map(recv_s, r), bar = dsmem_map(bar_s, r);
+        if constexpr (kPer == 2) {
+          st_async_f32x2(dst, v[r * 2], v[r * 2 + 1], bar);
         } else {
+          static_assert(kPer % 4 == 0, "push slices of 2 or 4k columns");
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cc = col + h;
-            if (cc >= cols) break;
-            const int r = cc / per;
-            if (r == split) {
-              red[(cc - cb0) * 128 + row] = v[j + h];
-            } else {
-              const uint32_t off = (uint32_t)(((split * 128 + row) * per + (cc - r * per)) * 4);
-              st_async_f32(dsmem_map(recv_s + off, r), v[j + h], dsmem_map(bar_s, r));
-            }
-          }
+          for (int k = 0; k < kPer; k += 4)
+            st_async_f32x4(dst + k * 4, v[r * kPer + k], v[r * kPer + k + 1], v[r * kPer + k + 2],
+                           v[r * kPer + k + 3], bar);
         }
       }
     }
@@ -217,10 +209,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (n_me > 0) {
       mbar_wait(recv_bar, 0);
       // fixed rank order, own partial in place: identical sums to the pull variant
-      for (int k = 0; k < n_me; ++k) {
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
         float acc = 0.f;
+#pragma unroll
         for (int z = 0; z < S; ++z) {
-          const float x = z == split ? red[k * 128 + row] : recv[(z * 128 + row) * per + k];
+          const float x = z == split ? red[k * 128 + row] : recv[(z * 128 + row) * kPer + k];
           acc = z == 0 ? x : acc + x;
         }
         red[k * 128 + row] = acc;
@@ -306,11 +300,11 @@ constexpr size_t smem_for() {
 static_assert(smem_for<16, 5, true>() <= 113 * 1024, "BN16 push tile must fit twice per SM");
 static_assert(smem_for<32, 4, true>() <= 113 * 1024, "BN32 push tile must fit twice per SM");
 
-template <int BN, int EPI, int STAGES = stages_for<BN>(), bool PUSH = false>
+template <int BN, int EPI, int STAGES = stages_for<BN>(), int kPushS = 0>
 cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                       cudaStream_t st) {
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI, PUSH>;
-  constexpr size_t smem = smem_for<BN, STAGES, PUSH>();
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, kPushS>;
+  constexpr size_t smem = smem_for<BN, STAGES, (kPushS > 0)>();
   static std::atomic<uint64_t> configured{0};  // per instantiation, per device
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
   if (a.splits > 8) {  // 16-CTA clusters are non-portable (opt-in)
@@ -353,9 +347,9 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
   }();
   switch (bn_for(w, a.M)) {
     case 16:
-      return push && a.splits > 1 ? launch_bn<16, EPI, 5, true>(w, x, a, st) : launch_bn<16, EPI>(w, x, a, st);
+      return push && a.splits == 8 ? launch_bn<16, EPI, 5, 8>(w, x, a, st) : launch_bn<16, EPI>(w, x, a, st);
     case 32:
-      return push && a.splits > 1 ? launch_bn<32, EPI, 4, true>(w, x, a, st) : launch_bn<32, EPI>(w, x, a, st);
+      return push && a.splits == 8 ? launch_bn<32, EPI, 4, 8>(w, x, a, st) : launch_bn<32, EPI>(w, x, a, st);
     case 64: return launch_bn<64, EPI>(w, x, a, st);
     case 128: return launch_bn<128, EPI>(w, x, a, st);
     default: return launch_bn<256, EPI>(w, x, a, st);

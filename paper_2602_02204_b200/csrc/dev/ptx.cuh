@@ -200,6 +200,13 @@ __device__ __forceinline__ void st_async_f32x2(uint32_t cluster_saddr, float v0,
                "f"(v0), "f"(v1), "r"(cluster_bar)
                : "memory");
 }
+__device__ __forceinline__ void st_async_f32x4(uint32_t cluster_saddr, float v0, float v1, float v2, float v3,
+                                               uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   cluster_saddr),
+               "f"(v0), "f"(v1), "f"(v2), "f"(v3), "r"(cluster_bar)
+               : "memory");
+}
 // Address of the same smem variable in CTA `rank` of this cluster.
 __device__ __forceinline__ uint32_t dsmem_map(uint32_t local_saddr, uint32_t rank) {
   uint32_t r;
