@@ -353,7 +353,14 @@ void ensure_pages(omni_stage* st, SeqSlot& s, int upto) {
 
 size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 
-constexpr int kGraphAfterHits = 3;  // eager launches of a geometry before it is captured
+// eager launches of a geometry before it is captured (OMNI_GRAPH_HITS)
+int graph_after_hits() {
+  static const int n = [] {
+    const char* e = std::getenv("OMNI_GRAPH_HITS");
+    return e ? std::max(1, std::atoi(e)) : 12;
+  }();
+  return n;
+}
 
 // OMNI_GRAPHS=0 launches every step eagerly (A/B measurements).
 bool graphs_enabled() {
@@ -371,6 +378,32 @@ bool graphs_enabled() {
 // is captured (PDL launch attributes become programmatic graph edges) and
 // instantiated; later steps replay it with one cudaGraphLaunch.
 template <typename F>
+StepGraph& capture_graph(omni_stage* st, uint64_t key, F&& body) {
+  cudaStream_t s = st->stream;
+  if (st->graphs.size() >= 4096) drop_graphs(st);
+  const uint64_t l0 = counters().launches;
+  OMNI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+  cudaGraph_t g = nullptr;
+  try {
+    body();
+  } catch (...) {
+    cudaStreamEndCapture(s, &g);
+    if (g) cudaGraphDestroy(g);
+    counters().launches = l0;
+    throw;
+  }
+  OMNI_CUDA(cudaStreamEndCapture(s, &g));
+  StepGraph sg;
+  sg.nodes = (int)(counters().launches - l0);
+  counters().launches = l0;  // counted per replay
+  const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
+  cudaGraphDestroy(g);
+  OMNI_CUDA(e);
+  ++counters().graph_captures;
+  return st->graphs.emplace(key, sg).first->second;
+}
+
+template <class F>
 void run_graph(omni_stage* st, uint64_t key, F&& body) {
   cudaStream_t s = st->stream;
   if (!graphs_enabled()) {
@@ -378,40 +411,22 @@ void run_graph(omni_stage* st, uint64_t key, F&& body) {
     return;
   }
   auto it = st->graphs.find(key);
-  if (it == st->graphs.end()) {
+  StepGraph* sg = it == st->graphs.end() ? nullptr : &it->second;
+  if (!sg) {
     // Capture + instantiate costs ~1 ms of host time: a launch geometry is
     // only graphed once it has recurred (timing-dependent batches produce a
     // long tail of one-off geometries); until then the step runs eagerly
-    // (still PDL-chained).
-    if (++st->key_hits[key] < kGraphAfterHits) {
+    // (still PDL-chained). Decode-only geometries are captured up front
+    // (prewarm_decode_graphs).
+    if (++st->key_hits[key] < graph_after_hits()) {
       body();
       return;
     }
-    if (st->graphs.size() >= 4096) drop_graphs(st);
-    const uint64_t l0 = counters().launches;
-    OMNI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
-    cudaGraph_t g = nullptr;
-    try {
-      body();
-    } catch (...) {
-      cudaStreamEndCapture(s, &g);
-      if (g) cudaGraphDestroy(g);
-      counters().launches = l0;
-      throw;
-    }
-    OMNI_CUDA(cudaStreamEndCapture(s, &g));
-    StepGraph sg;
-    sg.nodes = (int)(counters().launches - l0);
-    counters().launches = l0;  // counted per replay below
-    const cudaError_t e = cudaGraphInstantiate(&sg.exec, g, 0);
-    cudaGraphDestroy(g);
-    OMNI_CUDA(e);
-    it = st->graphs.emplace(key, sg).first;
-    ++counters().graph_captures;
+    sg = &capture_graph(st, key, body);
   }
   ++counters().graph_replays;
-  OMNI_CUDA(cudaGraphLaunch(it->second.exec, s));
-  counters().launches += it->second.nodes;
+  OMNI_CUDA(cudaGraphLaunch(sg->exec, s));
+  counters().launches += sg->nodes;
 }
 
 // The whole AR step as one launch (chain.cu): the same ops, epilogues and
@@ -551,6 +566,160 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   OMNI_KERNEL(chain_launch(P, total, st->stream));
 }
 
+// The per-kernel AR step (PDL chain) for one launch geometry; everything
+// step-specific is read from the fixed-offset descriptor blob, so the launch
+// sequence depends on (n_rows, n_blocks, n_dec, cond_prefill) only -- the
+// step-graph key.
+void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_blocks, int n_dec,
+                       bool cond_prefill) {
+  const auto& m = st->m;
+  const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
+  const bool talker = m.kind == OMNI_MODEL_TALKER;
+  cudaStream_t s = st->stream;
+  if (cond_prefill) {
+    OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
+    GemmEpilogue e;
+    e.out = st->hproj;
+    e.ldo = d;
+    OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
+  }
+  // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
+  // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
+  const int ss_ld = d / 128;
+  // Cross-kernel weight pipelining (OMNI_PF_MB, default off): each decode
+  // GEMM (>= 128 CTAs, so the prefetch is spread over every SM's memory
+  // pipe) pulls the first OMNI_PF_MB of the NEXT GEMM's weights into L2
+  // after issuing its own stream. Small-grid kernels (embed, attention)
+  // never prefetch: a few SMs cannot pull MBs fast (measured: 4 attention
+  // CTAs prefetching 32 MB took 43 us).
+  static const uint64_t kPf = [] {
+    const char* e = std::getenv("OMNI_PF_MB");
+    return (uint64_t)(e ? std::atoi(e) : 0) << 20;
+  }();
+  auto wbytes = [](const GemmWeight& g) { return (uint64_t)g.N_pad * g.K * 2; };
+  auto part = [&](const GemmWeight& g, uint64_t off) -> std::pair<const void*, uint64_t> {
+    const uint64_t n = wbytes(g);
+    if (off >= n || kPf == 0) return {nullptr, 0};
+    return {reinterpret_cast<const char*>(g.ptr) + off, std::min(kPf, n - off)};
+  };
+  OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
+                         st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld,
+                         nullptr, 0, s));
+  GemmEpilogue norm_in;  // fused RMSNorm of the GEMM input
+  norm_in.ss_in = st->ss;
+  norm_in.ss_ld = ss_ld;
+  norm_in.ss_n = ss_ld;
+  norm_in.norm_d = (float)d;
+  norm_in.norm_eps = kNormEps;
+  for (int l = 0; l < L; ++l) {
+    const auto& ly = st->layers[l];
+    GemmEpilogue e = norm_in;  // QKV: norm scale -> RoPE -> q rows / paged KV
+    e.out = st->q;
+    e.ldo = H * kHeadDim;
+    e.rope.rows = sd.rows;
+    e.rope.page_table = sd.page_table;
+    e.rope.max_pages = sd.max_pages;
+    e.rope.table = st->rope;
+    e.rope.q_out = st->q;
+    e.rope.kv = st->kv;
+    e.rope.n_heads = H;
+    e.rope.n_kv = KVH;
+    e.rope.layer = l;
+    e.rope.n_layers = L;
+    std::tie(e.pf_ptr, e.pf_bytes) = part(ly.go, 0);
+    OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
+    static const bool skip_attn = [] {  // OMNI_SKIP_ATTN=1: timing attribution only (wrong outputs)
+      const char* e = std::getenv("OMNI_SKIP_ATTN");
+      return e && e[0] == '1';
+    }();
+    if (!skip_attn)
+      OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
+    GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
+    r.out = st->x;
+    r.ldo = d;
+    r.xb = st->xn;
+    r.ss_out = st->ss;
+    r.ss_ld = ss_ld;
+    std::tie(r.pf_ptr, r.pf_bytes) = part(ly.ggu, 0);
+    OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, r, s));
+    e = norm_in;
+    e.out = st->act;
+    e.ldo = m.d_ff;
+    std::tie(e.pf_ptr, e.pf_bytes) = part(ly.gd, 0);
+    OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
+    std::tie(r.pf_ptr, r.pf_bytes) = l + 1 < L ? part(st->layers[l + 1].gqkv, 0) : part(st->glm, 0);
+    OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, r, s));
+  }
+  if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
+    // one kernel: final norm (+ hidden ring) -> LM head -> argmax
+    OMNI_KERNEL(launch_head(sd, n_dec, st->x, d, kNormEps, st->hbuf, talker ? nullptr : st->ring,
+                            st->ring_rows, st->lm.p, m.vocab, st->logits, st->vocab_pad, st->argmax_lo,
+                            st->argmax_hi, st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec),
+                            st->head_cnt, s));
+  } else if (n_dec > 0) {
+    OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
+                                    talker ? nullptr : st->ring, st->ring_rows, s));
+    GemmEpilogue e;
+    e.out = st->logits;
+    e.ldo = st->vocab_pad;
+    OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
+    OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
+                              st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
+  }
+}
+
+// Descriptor blob at FIXED offsets (capacity-sized regions, so the device
+// pointers baked into a captured step graph never change):
+//   entries | decode entry list | attention blocks | rows | page table
+struct ArDescLayout {
+  size_t off_dec, off_blk, off_rows, off_pt, reserve;
+};
+ArDescLayout ar_desc_layout(const omni_stage* st) {
+  const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
+  ArDescLayout l;
+  l.off_dec = align16(cap_e * sizeof(ArEntryDesc));
+  l.off_blk = l.off_dec + align16(cap_e * sizeof(int32_t));
+  l.off_rows = l.off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
+  l.off_pt = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
+  l.reserve = l.off_pt + cap_e * st->max_pages * sizeof(int32_t);
+  return l;
+}
+ArStepDev ar_step_dev(const omni_stage* st, const ArDescLayout& lay) {
+  ArStepDev sd;
+  sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
+  sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + lay.off_rows);
+  sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_pt);
+  sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_dec);
+  sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + lay.off_blk);
+  sd.max_pages = st->max_pages;
+  return sd;
+}
+uint64_t ar_graph_key(int n_rows, int n_blocks, int n_dec, bool cond_prefill) {
+  return ((uint64_t)n_rows << 40) | ((uint64_t)n_blocks << 20) | ((uint64_t)n_dec << 1) | (cond_prefill ? 1u : 0u);
+}
+
+// Decode-only steps (every entry feeds one token: n_rows = n_blocks = n_dec)
+// are the steady state of both AR stages; capture their step graphs at stage
+// creation (~1 ms host time each) instead of stalling the serving loop the
+// third time a batch size shows up. OMNI_PREWARM=<max decode rows> (0 = off).
+void prewarm_decode_graphs(omni_stage* st) {
+  if (!graphs_enabled() || st->chain_on) return;
+  static const int cap_env = [] {
+    const char* e = std::getenv("OMNI_PREWARM");
+    return e ? std::atoi(e) : -1;
+  }();
+  int upto = std::min(st->lim.max_resident, st->rows_cap);
+  if (cap_env >= 0) upto = std::min(upto, cap_env);
+  if (upto <= 0) return;
+  const ArDescLayout lay = ar_desc_layout(st);
+  if (staging_reserve(st->desc, lay.reserve)) drop_graphs(st);
+  const ArStepDev sd = ar_step_dev(st, lay);
+  for (int n = 1; n <= upto; ++n) {
+    const uint64_t key = ar_graph_key(n, n, n, false);
+    if (!st->graphs.count(key)) capture_graph(st, key, [&] { launch_ar_kernels(st, sd, n, n, n, false); });
+  }
+}
+
 void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* margin_out) {
   ensure_idle(st);
   const int ne = b->n_entries;
@@ -568,16 +737,10 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   if (talker) OMNI_REQUIRE(b->cond_row != nullptr, OMNI_E_BADARG, "talker step needs cond_row");
 
   OMNI_REQUIRE(ne <= st->lim.max_resident, OMNI_E_BADARG, "more entries than max_resident_requests");
-  // descriptor blob at FIXED offsets (capacity-sized regions, so the device
-  // pointers baked into a captured step graph never change):
-  //   entries | decode entry list | attention blocks | rows | page table
-  const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
-  const size_t off_dec = align16(cap_e * sizeof(ArEntryDesc));
-  const size_t off_blk = off_dec + align16(cap_e * sizeof(int32_t));
-  const size_t off_rows = off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
-  const size_t off_pt = off_rows + align16(cap_r * sizeof(ArRowDesc));
+  const ArDescLayout lay = ar_desc_layout(st);
+  const size_t off_dec = lay.off_dec, off_blk = lay.off_blk, off_rows = lay.off_rows, off_pt = lay.off_pt;
   const size_t total = off_pt + align16((size_t)ne * st->max_pages * sizeof(int32_t));
-  if (staging_reserve(st->desc, off_pt + cap_e * st->max_pages * sizeof(int32_t))) drop_graphs(st);
+  if (staging_reserve(st->desc, lay.reserve)) drop_graphs(st);
   auto* ents = reinterpret_cast<ArEntryDesc*>(st->desc.host);
   auto* rows = reinterpret_cast<ArRowDesc*>(st->desc.host + off_rows);
   auto* pt = reinterpret_cast<int32_t*>(st->desc.host + off_pt);
@@ -635,112 +798,16 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, total, cudaMemcpyHostToDevice, s));
   counters().h2d_bytes += total;
   OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
-  ArStepDev sd;
-  sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
-  sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + off_rows);
-  sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + off_pt);
-  sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + off_dec);
-  sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + off_blk);
-  sd.max_pages = st->max_pages;
+  const ArStepDev sd = ar_step_dev(st, lay);
 
   const auto& m = st->m;
   const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   if (n_rows > 0) {
-    const uint64_t key = ((uint64_t)n_rows << 40) | ((uint64_t)n_blocks << 20) | ((uint64_t)n_dec << 1) |
-                         (talker && n_prefill_rows > 0 ? 1u : 0u);
+    const uint64_t key = ar_graph_key(n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0);
     if (st->chain_on && !talker && n_rows <= chain_max_rows()) {
       run_graph(st, key, [&] { launch_step_chain(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0); });
     } else run_graph(st, key, [&] {
-      if (talker && n_prefill_rows > 0) {
-        OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
-        GemmEpilogue e;
-        e.out = st->hproj;
-        e.ldo = d;
-        OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
-      }
-      // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
-      // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
-      const int ss_ld = d / 128;
-      // Cross-kernel weight pipelining (OMNI_PF_MB, default off): each decode
-      // GEMM (>= 128 CTAs, so the prefetch is spread over every SM's memory
-      // pipe) pulls the first OMNI_PF_MB of the NEXT GEMM's weights into L2
-      // after issuing its own stream. Small-grid kernels (embed, attention)
-      // never prefetch: a few SMs cannot pull MBs fast (measured: 4 attention
-      // CTAs prefetching 32 MB took 43 us).
-      static const uint64_t kPf = [] {
-        const char* e = std::getenv("OMNI_PF_MB");
-        return (uint64_t)(e ? std::atoi(e) : 0) << 20;
-      }();
-      auto wbytes = [](const GemmWeight& g) { return (uint64_t)g.N_pad * g.K * 2; };
-      auto part = [&](const GemmWeight& g, uint64_t off) -> std::pair<const void*, uint64_t> {
-        const uint64_t n = wbytes(g);
-        if (off >= n || kPf == 0) return {nullptr, 0};
-        return {reinterpret_cast<const char*>(g.ptr) + off, std::min(kPf, n - off)};
-      };
-      OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
-                             st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld,
-                             nullptr, 0, s));
-      GemmEpilogue norm_in;  // fused RMSNorm of the GEMM input
-      norm_in.ss_in = st->ss;
-      norm_in.ss_ld = ss_ld;
-      norm_in.ss_n = ss_ld;
-      norm_in.norm_d = (float)d;
-      norm_in.norm_eps = kNormEps;
-      for (int l = 0; l < L; ++l) {
-        const auto& ly = st->layers[l];
-        GemmEpilogue e = norm_in;  // QKV: norm scale -> RoPE -> q rows / paged KV
-        e.out = st->q;
-        e.ldo = H * kHeadDim;
-        e.rope.rows = sd.rows;
-        e.rope.page_table = sd.page_table;
-        e.rope.max_pages = sd.max_pages;
-        e.rope.table = st->rope;
-        e.rope.q_out = st->q;
-        e.rope.kv = st->kv;
-        e.rope.n_heads = H;
-        e.rope.n_kv = KVH;
-        e.rope.layer = l;
-        e.rope.n_layers = L;
-        std::tie(e.pf_ptr, e.pf_bytes) = part(ly.go, 0);
-        OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
-        static const bool skip_attn = [] {  // OMNI_SKIP_ATTN=1: timing attribution only (wrong outputs)
-          const char* e = std::getenv("OMNI_SKIP_ATTN");
-          return e && e[0] == '1';
-        }();
-        if (!skip_attn)
-          OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
-        GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
-        r.out = st->x;
-        r.ldo = d;
-        r.xb = st->xn;
-        r.ss_out = st->ss;
-        r.ss_ld = ss_ld;
-        std::tie(r.pf_ptr, r.pf_bytes) = part(ly.ggu, 0);
-        OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, r, s));
-        e = norm_in;
-        e.out = st->act;
-        e.ldo = m.d_ff;
-        std::tie(e.pf_ptr, e.pf_bytes) = part(ly.gd, 0);
-        OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
-        std::tie(r.pf_ptr, r.pf_bytes) = l + 1 < L ? part(st->layers[l + 1].gqkv, 0) : part(st->glm, 0);
-        OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, r, s));
-      }
-      if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
-        // one kernel: final norm (+ hidden ring) -> LM head -> argmax
-        OMNI_KERNEL(launch_head(sd, n_dec, st->x, d, kNormEps, st->hbuf, talker ? nullptr : st->ring,
-                                st->ring_rows, st->lm.p, m.vocab, st->logits, st->vocab_pad, st->argmax_lo,
-                                st->argmax_hi, st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec),
-                                st->head_cnt, s));
-      } else if (n_dec > 0) {
-        OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
-                                        talker ? nullptr : st->ring, st->ring_rows, s));
-        GemmEpilogue e;
-        e.out = st->logits;
-        e.ldo = st->vocab_pad;
-        OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
-        OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
-                                  st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
-      }
+      launch_ar_kernels(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0);
     });
     if (n_dec > 0) {
       // tokens and margins in one copy: [n_dec x i32 | n_dec x f32]
@@ -819,6 +886,28 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
   }
 }
 
+constexpr int kDitPadTok = 8;  // DiT batches are padded to whole 128-row token tiles
+uint64_t dit_graph_key(int nt, int64_t t0) { return (uint64_t)nt << 20 | (uint64_t)t0; }
+
+// Capture the DiT step graph of every padded batch size up front
+// (OMNI_PREWARM caps the token count too; 0 = off).
+void prewarm_dit_graphs(omni_stage* st) {
+  if (!graphs_enabled()) return;
+  static const int cap_env = [] {
+    const char* e = std::getenv("OMNI_PREWARM");
+    return e ? std::atoi(e) * kDitPadTok : -1;
+  }();
+  int upto = st->tok_cap;
+  if (cap_env >= 0) upto = std::min(upto, cap_env);
+  if (upto < kDitPadTok) return;
+  if (staging_reserve(st->desc, align16((size_t)st->tok_cap * sizeof(DitTokDesc)))) drop_graphs(st);
+  const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
+  for (int nt = kDitPadTok; nt <= upto; nt += kDitPadTok) {
+    const uint64_t key = dit_graph_key(nt, 0);
+    if (!st->graphs.count(key)) capture_graph(st, key, [&] { dit_chunk(st, toks_dev, nt, st->dsamples); });
+  }
+}
+
 void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
   ensure_idle(st);
   OMNI_REQUIRE(st->m.kind == OMNI_MODEL_DIT, OMNI_E_BADARG, "not a DiT stage");
@@ -827,7 +916,13 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
     OMNI_REQUIRE(b->n_tokens[j] >= 0 && b->token_offset[j] >= 0, OMNI_E_BADARG, "bad DiT job");
     n_tok += b->n_tokens[j];
   }
-  const size_t bytes = align16((size_t)n_tok * sizeof(DitTokDesc));
+  // Pad the batch to a multiple of kDitPadTok tokens (= 128 rows, a whole
+  // GEMM token tile: no extra MMA work) with dummy tokens whose rows are
+  // computed and dropped. Rows never interact (token-local DiT), so real
+  // outputs are unchanged, and the step-graph geometries shrink 8x (all
+  // prewarmed at stage creation).
+  const int64_t n_pad = n_tok == 0 ? 0 : (n_tok + kDitPadTok - 1) / kDitPadTok * kDitPadTok;
+  const size_t bytes = align16((size_t)n_pad * sizeof(DitTokDesc));
   if (staging_reserve(st->desc, std::max(bytes, align16((size_t)st->tok_cap * sizeof(DitTokDesc)))))
     drop_graphs(st);
   auto* toks = reinterpret_cast<DitTokDesc*>(st->desc.host);
@@ -840,6 +935,7 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
                    "diffusion_engine.hpp:29-30)");
       toks[k] = DitTokDesc{b->request_id[j], b->token_offset[j] + i, id};
     }
+  for (; k < n_pad; ++k) toks[k] = DitTokDesc{0, 0, 0};
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
   if (n_tok > 0) {
@@ -848,9 +944,9 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
     OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
     const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
     for (int64_t t0 = 0; t0 < n_tok; t0 += st->tok_cap) {
-      const int nt = (int)std::min<int64_t>(st->tok_cap, n_tok - t0);
-      run_graph(st, (uint64_t)nt << 20 | (uint64_t)t0, [&] { dit_chunk(st, toks_dev + t0, nt, st->dsamples); });
-      const int64_t nsamp = (int64_t)nt * kDitSamples;
+      const int nt = (int)std::min<int64_t>(st->tok_cap, n_pad - t0);
+      run_graph(st, dit_graph_key(nt, t0), [&] { dit_chunk(st, toks_dev + t0, nt, st->dsamples); });
+      const int64_t nsamp = std::min<int64_t>(nt, n_tok - t0) * kDitSamples;  // real tokens only
       OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
       counters().d2h_bytes += nsamp * sizeof(int32_t);
@@ -1057,8 +1153,14 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     OMNI_CUDA(cudaEventCreate(&st->ev_start));
     OMNI_CUDA(cudaEventCreate(&st->ev_done));
     OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_link, cudaEventDisableTiming));
-    if (model->kind == OMNI_MODEL_DIT) build_dit(st);
-    else if (model->kind == OMNI_MODEL_THINKER || model->kind == OMNI_MODEL_TALKER) build_ar(st);
+    if (model->kind == OMNI_MODEL_DIT) {
+      build_dit(st);
+      prewarm_dit_graphs(st);
+    }
+    else if (model->kind == OMNI_MODEL_THINKER || model->kind == OMNI_MODEL_TALKER) {
+      build_ar(st);
+      prewarm_decode_graphs(st);
+    }
     else throw DevError(OMNI_E_BADARG, "unknown model kind");
     *out = st;
   });
