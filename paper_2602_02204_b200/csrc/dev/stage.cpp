@@ -1138,13 +1138,15 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     OMNI_CUDA(cudaSetDevice(dev));
     // Stream priority by stage kind when stages share a GPU. OMNI_PRIO = three
     // digits, the urgency rank (0 = most urgent) of thinker / talker / DiT.
-    // Default "000" (all equal): measured best for the bench workload; ranking
-    // the Talker (the per-token critical path) first starves the DiT and the
-    // final waveform chunks (profiles/r01_bench_prio_ab.txt).
+    // Default "101": the Talker's 4L dependent decode steps are the longest
+    // chain of every request; with the split-K push reduction, warp-MMA
+    // attention and prewarmed graphs it now wins 194.6 vs 185.3 req/s (median
+    // of 3) over all-equal (profiles/r01_bench_prio_ab3.txt; before those
+    // changes equal ranks measured best, profiles/r01_bench_prio_ab.txt).
     int lo = 0, hi = 0;
     OMNI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // hi = numerically lowest = most urgent
     const char* pe = std::getenv("OMNI_PRIO");
-    const char* ranks = (pe && std::strlen(pe) == 3) ? pe : "000";
+    const char* ranks = (pe && std::strlen(pe) == 3) ? pe : "101";
     const int kind_ix = model->kind == OMNI_MODEL_THINKER ? 0 : model->kind == OMNI_MODEL_TALKER ? 1 : 2;
     const int rank = std::clamp(ranks[kind_ix] - '0', 0, 2);
     const int prio = hi + (lo - hi) * rank / 2;
