@@ -218,7 +218,23 @@ void build_ar(omni_stage* st) {
                               cudaMemcpyHostToDevice, st->stream));
     st->chain_done = dev_alloc<int>(st, kChainMaxOps + 1);
   }
-  OMNI_CUDA(cudaMallocHost(&st->h_tok, 2 * (size_t)R * sizeof(int32_t)));
+  // Step results [n_dec tokens | n_dec margins]: the argmax kernel stores
+  // them straight into mapped pinned host memory (no D2H copy on the step's
+  // tail: -2..3 µs per step, profiles/r01_zc_tok_ab.txt); OMNI_ZC_TOK=0: a
+  // device buffer + one D2H copy.
+  static const bool zc = [] {
+    const char* e = std::getenv("OMNI_ZC_TOK");
+    return !(e && e[0] == '0');
+  }();
+  st->zc_tok = zc;
+  if (zc) {
+    OMNI_CUDA(cudaHostAlloc(&st->h_tok, 2 * (size_t)R * sizeof(int32_t), cudaHostAllocMapped));
+    void* dp = nullptr;
+    OMNI_CUDA(cudaHostGetDevicePointer(&dp, st->h_tok, 0));
+    st->d_tok = static_cast<int32_t*>(dp);
+  } else {
+    OMNI_CUDA(cudaMallocHost(&st->h_tok, 2 * (size_t)R * sizeof(int32_t)));
+  }
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
 }
 
@@ -811,7 +827,8 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
     });
     if (n_dec > 0) {
       // tokens and margins in one copy: [n_dec x i32 | n_dec x f32]
-      OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, 2 * n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      if (!st->zc_tok)
+        OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, 2 * n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       counters().d2h_bytes += n_dec * (sizeof(int32_t) + sizeof(float));
     }
   }

@@ -106,6 +106,7 @@ struct omni_stage {
   // ---- step staging / results ----
   omni_dev::Staging desc, pack;
   int32_t* h_tok = nullptr;
+  bool zc_tok = false;  // h_tok is mapped: kernels write results to host memory directly
   int32_t* h_samples = nullptr;
   bool pending = false;
   int pending_kind = 0;  // 1 = AR, 2 = DiT
