@@ -63,9 +63,12 @@ __device__ __forceinline__ void input_scales(const GemmArgs& a, int tok0, int nc
 // owns 8 consecutive output features of one token, so every global access
 // is a 16-byte vector (bf16) or 2x16-byte (fp32); SWIGLU pairs gate row f
 // with up row f + 64 of the same tile, ROPE_KV rotates feature f with f + 64.
+// `pre` (optional, push path): smem staged during the mainloop -- RESID_NORM:
+// the residual rows pre[c * 128 + feature] = x[tok0 + c][tile]; ROPE_KV: the
+// tokens' positions, KV pages and RoPE (cos, sin) rows.
 template <int EPI>
 __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0, int ncols,
-                                         const float* acc, const float* inv) {
+                                         const float* acc, const float* inv, const float* pre = nullptr) {
   __syncthreads();
   const int t = threadIdx.x;
   if constexpr (EPI == EPI_SWIGLU) {
@@ -90,10 +93,17 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
       ld8(acc + c * 128 + f0, lo);
       ld8(acc + c * 128 + 64 + f0, hi);
       const float sc = inv[c];
-      const ArRowDesc rd = rows[tok];
+      // `pre` (push path): pos[16] | page[16] | (cos, sin)[c][64], staged
+      // during the mainloop; else straight from the descriptors / table
+      const int* pre_i = reinterpret_cast<const int*>(pre);
+      const float2* pre_cs = reinterpret_cast<const float2*>(pre + 32);
+      ArRowDesc rd;
+      if (pre) rd.pos = pre_i[c], rd.entry = 0;
+      else rd = rows[tok];
       float o0[8], o1[8];
       if (head < rp.n_heads + rp.n_kv) {
-        const float4* cs4 = reinterpret_cast<const float4*>(rp.table + (size_t)rd.pos * 64 + f0);
+        const float4* cs4 = reinterpret_cast<const float4*>(pre ? pre_cs + c * 64 + f0
+                                                                : rp.table + (size_t)rd.pos * 64 + f0);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const float4 w = cs4[i];  // (cos, sin) of pairs 2i, 2i+1
@@ -114,7 +124,7 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
       } else {
         const int is_v = head >= rp.n_heads + rp.n_kv;
         const int kh = head - rp.n_heads - (is_v ? rp.n_kv : 0);
-        const int page = rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens];
+        const int page = pre ? pre_i[16 + c] : rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens];
         const int pt = rd.pos % kPageTokens;
         dst = rp.kv +
               ((((size_t)page * rp.n_layers + rp.layer) * 2 + is_v) * rp.n_kv + kh) * kPageTokens * 128 +
@@ -139,7 +149,8 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
         float v[8], x[8];
         ld8(acc + c * 128 + r0, v);
         float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
-        ld8(r, x);
+        if (pre) ld8(pre + c * 128 + r0, x);
+        else ld8(r, x);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           x[i] += v[i];
@@ -189,7 +200,8 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
         const int grow = a.gate_index ? a.gate_index[(size_t)grp * a.gate_index_stride] : grp;
         ld8(a.gate + (size_t)grow * a.ldg + a.gate_off + n0, g);
         float* r = static_cast<float*>(a.out) + (size_t)tok * a.ldo + n0;
-        ld8(r, x);
+        if (pre) ld8(pre + c * 128 + r0, x);
+        else ld8(r, x);
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] += g[i] * v[i];
         st8(r, x);

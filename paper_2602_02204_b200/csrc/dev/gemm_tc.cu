@@ -66,8 +66,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr size_t kEpi = (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
   constexpr size_t kMain = kPipe > kEpi ? kPipe : kEpi;
   constexpr size_t kRecv = PUSH ? (size_t)BN * 128 * 4 : 0;  // [S][128][per] fp32, S * per <= BN
+  // own-slice residual (RESID_NORM) / positions, pages, RoPE rows (ROPE_KV)
+  constexpr size_t kPre = PUSH ? (size_t)(BN / (kPushS > 0 ? kPushS : 1)) * 128 * 4 + 128 : 0;
   float* recv = reinterpret_cast<float*>(smem + kMain);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMain + kRecv);
+  float* pre = reinterpret_cast<float*>(smem + kMain + kRecv);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kMain + kRecv + kPre);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
@@ -136,9 +139,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 2) {
     // idle warps: input-RMS scales of this token tile, overlapped with the mainloop
+    if constexpr (PUSH && EPI == EPI_ROPE_KV) {
+      // positions / KV pages / RoPE rows of this rank's token slice: step
+      // descriptors and static tables, readable before the PDL wait
+      constexpr int kPer = BN / kPushS;
+      const int cb0 = m_tile * BN + split * kPer;
+      const int n_me = min(kPer, a.M - cb0);
+      const RopeKvArgs& rp = a.rope;
+      int* pre_i = reinterpret_cast<int*>(pre);
+      float2* pre_cs = reinterpret_cast<float2*>(pre + 32);
+      const int q = threadIdx.x - 64;
+      if (q < n_me) {
+        const ArRowDesc rd = static_cast<const ArRowDesc*>(rp.rows)[cb0 + q];
+        pre_i[q] = rd.pos;
+        pre_i[16 + q] = n_tile >= rp.n_heads ? rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens] : 0;
+      }
+      asm volatile("bar.sync 1, 64;" ::: "memory");  // warps 2-3 only
+      if (n_tile < rp.n_heads + rp.n_kv)
+        for (int i = q; i < n_me * 64; i += kThreads - 64)
+          pre_cs[i] = rp.table[(size_t)pre_i[i >> 6] * 64 + (i & 63)];
+    }
     pdl_wait();
     const int m0 = m_tile * BN;
     input_scales(a, m0, min(BN, a.M - m0), inv_s, threadIdx.x - 64, kThreads - 64);
+    if constexpr (PUSH && EPI == EPI_RESID_NORM) {
+      // stage this rank's residual slice while the MMAs run (the epilogue
+      // would otherwise start with a dependent L2 round trip)
+      constexpr int kPer = BN / kPushS;
+      const int cb0 = m0 + split * kPer;
+      const int n_me = min(kPer, a.M - cb0);
+      const int n0 = n_tile * kBlockM;
+      for (int q = threadIdx.x - 64; q < n_me * 32; q += kThreads - 64) {
+        const int c = q >> 5, f = (q & 31) * 4;
+        *reinterpret_cast<float4*>(pre + c * 128 + f) =
+            *reinterpret_cast<const float4*>(static_cast<const float*>(a.out) + (size_t)(cb0 + c) * a.ldo + n0 + f);
+      }
+    }
   } else if (warp == 1) {
     if (elect_one()) {
       for (int i = 0; i < kb_per; ++i) {
@@ -219,7 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         red[k * 128 + row] = acc;
       }
-      epi_cols<EPI>(a, n_tile, m0 + cb0, n_me, red, inv_s + cb0);  // syncs before reading the slice
+      // syncs before reading the slice (and the staged residual)
+      epi_cols<EPI>(a, n_tile, m0 + cb0, n_me, red, inv_s + cb0,
+                    (EPI == EPI_RESID_NORM || EPI == EPI_ROPE_KV) ? pre : nullptr);
     }
   } else {
   for (int c = 0; c < chunks; ++c) {
@@ -293,8 +331,8 @@ constexpr size_t smem_for() {
   constexpr size_t pipe = STAGES * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
   // + [push receive buffer] + barriers / tmem slot (256 B) + per-column
   // input-RMS scales (4 B x BN) + flag / receive barrier
-  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + (PUSH ? (size_t)BN * 128 * 4 : 0) + 256 +
-         4 * BN + 16;
+  return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + (PUSH ? (size_t)BN * 128 * 4 : 0) +
+         (PUSH ? (size_t)BN / 2 * 128 * 4 + 128 : 0) + 256 + 4 * BN + 16;  // + staged epilogue inputs (kPushS >= 2)
 }
 // push split-K variants keep two CTAs per SM (<= ~113 KB): one stage less
 static_assert(smem_for<16, 5, true>() <= 113 * 1024, "BN16 push tile must fit twice per SM");
@@ -347,9 +385,13 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
   }();
   switch (bn_for(w, a.M)) {
     case 16:
-      return push && a.splits == 8 ? launch_bn<16, EPI, 5, 8>(w, x, a, st) : launch_bn<16, EPI>(w, x, a, st);
+      if (push && a.splits == 8) return launch_bn<16, EPI, 5, 8>(w, x, a, st);
+      if (push && a.splits == 2) return launch_bn<16, EPI, 5, 2>(w, x, a, st);
+      return launch_bn<16, EPI>(w, x, a, st);
     case 32:
-      return push && a.splits == 8 ? launch_bn<32, EPI, 4, 8>(w, x, a, st) : launch_bn<32, EPI>(w, x, a, st);
+      if (push && a.splits == 8) return launch_bn<32, EPI, 4, 8>(w, x, a, st);
+      if (push && a.splits == 2) return launch_bn<32, EPI, 4, 2>(w, x, a, st);
+      return launch_bn<32, EPI>(w, x, a, st);
     case 64: return launch_bn<64, EPI>(w, x, a, st);
     case 128: return launch_bn<128, EPI>(w, x, a, st);
     default: return launch_bn<256, EPI>(w, x, a, st);

@@ -146,7 +146,11 @@ void build_ar(omni_stage* st) {
     ly.wd = make_weight(st, p + "wd", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
     ly.gqkv = gemm_of(ly.wqkv, 8);
     ly.go = gemm_of(ly.wo, 8);
-    ly.ggu = gemm_of(ly.wgu, 8);
+    static const int gu_split = [] {  // OMNI_GU_SPLIT: split cap of the gate-up GEMM (CTA target 256 if > 1)
+      const char* e = std::getenv("OMNI_GU_SPLIT");
+      return e ? std::atoi(e) : 1;
+    }();
+    ly.ggu = gemm_of(ly.wgu, gu_split, gu_split > 1 ? 256 : 192);
     static const int down_split = [] {  // OMNI_DOWN_SPLIT (experiments): split cap / CTA target of the down proj
       const char* e = std::getenv("OMNI_DOWN_SPLIT");
       return e ? std::atoi(e) : 8;
@@ -217,6 +221,12 @@ void build_ar(omni_stage* st) {
     OMNI_CUDA(cudaMemcpyAsync(st->chain_maps, maps.data(), maps.size() * sizeof(CUtensorMap),
                               cudaMemcpyHostToDevice, st->stream));
     st->chain_done = dev_alloc<int>(st, kChainMaxOps + 1);
+  }
+  // OMNI_STEP_TRACE=1 (tools/step_trace.py): every GEMM launch of a step
+  // records its per-CTA phase stamps in its own slot (baked into the graphs).
+  if (const char* e = std::getenv("OMNI_STEP_TRACE"); e && e[0] == '1') {
+    st->step_trace = dev_alloc<unsigned long long>(st, (size_t)kStepTraceLaunches * kStepTraceCtas * 8);
+    OMNI_CUDA(cudaMemsetAsync(st->step_trace, 0, (size_t)kStepTraceLaunches * kStepTraceCtas * 8 * 8, st->stream));
   }
   // Step results [n_dec tokens | n_dec margins]: the argmax kernel stores
   // them straight into mapped pinned host memory (no D2H copy on the step's
@@ -592,12 +602,18 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   const bool talker = m.kind == OMNI_MODEL_TALKER;
   cudaStream_t s = st->stream;
+  int trace_slot = 0;  // OMNI_STEP_TRACE: one slot per GEMM launch, in launch order
+  auto traced = [&](GemmEpilogue e) {
+    if (st->step_trace && trace_slot < kStepTraceLaunches)
+      e.trace = st->step_trace + (size_t)(trace_slot++) * kStepTraceCtas * 8;
+    return e;
+  };
   if (cond_prefill) {
     OMNI_KERNEL(launch_gather_cond(sd, n_rows, m.cond_dim, st->condin, s));
     GemmEpilogue e;
     e.out = st->hproj;
     e.ldo = d;
-    OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, e, s));
+    OMNI_KERNEL(gemm_run(st->ghid, st->in_cond, n_rows, EPI_F32, traced(e), s));
   }
   // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
   // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
@@ -642,8 +658,15 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     e.rope.n_kv = KVH;
     e.rope.layer = l;
     e.rope.n_layers = L;
-    std::tie(e.pf_ptr, e.pf_bytes) = part(ly.go, 0);
-    OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, e, s));
+    // OMNI_PF_MODE=2: "two ahead" -- the QKV GEMM pulls the WHOLE gate-up
+    // weight and the O GEMM the whole down weight into L2 while the
+    // latency-bound QKV -> attention -> O segment leaves HBM idle.
+    static const int pf_mode = [] {
+      const char* e = std::getenv("OMNI_PF_MODE");
+      return e ? std::atoi(e) : 1;
+    }();
+    std::tie(e.pf_ptr, e.pf_bytes) = pf_mode == 2 ? part(ly.ggu, 0) : part(ly.go, 0);
+    OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, traced(e), s));
     static const bool skip_attn = [] {  // OMNI_SKIP_ATTN=1: timing attribution only (wrong outputs)
       const char* e = std::getenv("OMNI_SKIP_ATTN");
       return e && e[0] == '1';
@@ -656,15 +679,17 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     r.xb = st->xn;
     r.ss_out = st->ss;
     r.ss_ld = ss_ld;
-    std::tie(r.pf_ptr, r.pf_bytes) = part(ly.ggu, 0);
-    OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, r, s));
+    std::tie(r.pf_ptr, r.pf_bytes) = pf_mode == 2 ? part(ly.gd, 0) : part(ly.ggu, 0);
+    OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, traced(r), s));
     e = norm_in;
     e.out = st->act;
     e.ldo = m.d_ff;
-    std::tie(e.pf_ptr, e.pf_bytes) = part(ly.gd, 0);
-    OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, e, s));
-    std::tie(r.pf_ptr, r.pf_bytes) = l + 1 < L ? part(st->layers[l + 1].gqkv, 0) : part(st->glm, 0);
-    OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, r, s));
+    std::tie(e.pf_ptr, e.pf_bytes) = pf_mode == 2 ? std::pair<const void*, uint64_t>{nullptr, 0} : part(ly.gd, 0);
+    OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, traced(e), s));
+    std::tie(r.pf_ptr, r.pf_bytes) = pf_mode == 2 ? std::pair<const void*, uint64_t>{nullptr, 0}
+                                     : l + 1 < L  ? part(st->layers[l + 1].gqkv, 0)
+                                                  : part(st->glm, 0);
+    OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, traced(r), s));
   }
   if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
     // one kernel: final norm (+ hidden ring) -> LM head -> argmax
@@ -678,7 +703,7 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     GemmEpilogue e;
     e.out = st->logits;
     e.ldo = st->vocab_pad;
-    OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, e, s));
+    OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, traced(e), s));
     OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
                               st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
   }
@@ -1245,6 +1270,12 @@ omni_status omni_stage_tensor(const omni_stage* st, const char* name, uint64_t* 
       *dev_ptr = reinterpret_cast<uint64_t>(st->hproj);
       if (rows) *rows = st->rows_cap;
       if (cols) *cols = st->m.d_model;
+      return;
+    }
+    if (n == "buf.step_trace" && st->step_trace) {  // OMNI_STEP_TRACE=1: [launch][cta][8] u64
+      *dev_ptr = reinterpret_cast<uint64_t>(st->step_trace);
+      if (rows) *rows = kStepTraceLaunches * kStepTraceCtas;
+      if (cols) *cols = 8;
       return;
     }
     if (n == "buf.x") {

@@ -17,6 +17,9 @@
 
 namespace omni_dev {
 
+constexpr int kStepTraceLaunches = 64;  // OMNI_STEP_TRACE: GEMM launches per step traced
+constexpr int kStepTraceCtas = 512;     // CTA slots per traced launch
+
 struct DevTensor {
   __nv_bfloat16* p = nullptr;
   int64_t rows = 0, rows_pad = 0, cols = 0;
@@ -106,7 +109,8 @@ struct omni_stage {
   // ---- step staging / results ----
   omni_dev::Staging desc, pack;
   int32_t* h_tok = nullptr;
-  bool zc_tok = false;  // h_tok is mapped: kernels write results to host memory directly
+  bool zc_tok = false;
+  unsigned long long* step_trace = nullptr;  // OMNI_STEP_TRACE debug stamps  // h_tok is mapped: kernels write results to host memory directly
   int32_t* h_samples = nullptr;
   bool pending = false;
   int pending_kind = 0;  // 1 = AR, 2 = DiT
