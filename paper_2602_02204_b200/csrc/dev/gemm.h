@@ -116,6 +116,9 @@ struct GemmArgs {
 };
 
 int gemm_block_n(int M);
+// Split-K reduction by st.async push (decode tiles BN <= 32, 2- or 8-way
+// splits); OMNI_SPLITK_PUSH=0 selects the cluster-barrier pull variant.
+bool gemm_push_enabled();
 int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas = 192);
 // max_splits / target_ctas: 8 / 192 for decode-path (weight-streaming)
 // matrices (measured in-chain optimum: qkv 24x8, wo 16x8, down 16x8,

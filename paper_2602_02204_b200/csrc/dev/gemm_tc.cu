@@ -35,6 +35,7 @@ __device__ unsigned long long* g_gemm_marks = nullptr;
 cudaError_t gemm_marks_set(void* p) { return cudaMemcpyToSymbol(g_gemm_marks, &p, sizeof(p)); }
 
 static int bn_for(const GemmWeight& w, int M);  // token-tile width for (weight, batch)
+bool gemm_push_enabled();
 
 namespace {
 
@@ -379,10 +380,7 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
       }
     }
   }
-  static const bool push = [] {  // OMNI_SPLITK_PUSH=0: cluster-barrier + DSMEM-pull reduction
-    const char* e = std::getenv("OMNI_SPLITK_PUSH");
-    return !(e && e[0] == '0');
-  }();
+  const bool push = gemm_push_enabled();
   switch (bn_for(w, a.M)) {
     case 16:
       if (push && a.splits == 8) return launch_bn<16, EPI, 5, 8>(w, x, a, st);
@@ -399,6 +397,14 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
 }
 
 }  // namespace
+
+bool gemm_push_enabled() {  // OMNI_SPLITK_PUSH=0: cluster-barrier + DSMEM-pull reduction
+  static const bool push = [] {
+    const char* e = std::getenv("OMNI_SPLITK_PUSH");
+    return !(e && e[0] == '0');
+  }();
+  return push;
+}
 
 static int bn_for(const GemmWeight& w, int M) {
   int bn = gemm_block_n(M);

@@ -63,8 +63,12 @@ for slot in range(tr.shape[0]):
     if t0 is None:
         t0 = ent.min()
     events.append((nm, ent.min(), np.median(wait), wait.max(), np.median(done), ext.max(), len(c)))
+    if os.environ.get("TRACE_PHASES") and nm.startswith("qkv"):
+        ph = {k: np.round(np.percentile((ent + c[:, i] / GHZ - t0) / 1e3, [50, 100]), 2).tolist()
+              for k, i in (("s1", 1), ("s3", 3), ("s5", 5), ("end6", 6))}
+        print(nm, ph)
 ncta = (at[:, 0] > 0).sum() // L
-for l in range(L):
+for l in range(L if ncta else 0):
     a = at[l * ncta:(l + 1) * ncta]
     a = a[a[:, 0] > 0]
     events.append(("attn" + str(l), a[:, 0].min(), np.median(a[:, 1]), a[:, 1].max(), np.median(a[:, 4]), a[:, 5].max(), len(a)))
