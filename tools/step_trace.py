@@ -63,6 +63,9 @@ for slot in range(tr.shape[0]):
     if t0 is None:
         t0 = ent.min()
     events.append((nm, ent.min(), np.median(wait), wait.max(), np.median(done), ext.max(), len(c)))
+    if os.environ.get("TRACE_SKEW"):
+        pc = lambda v: np.round((np.percentile(v, [0, 10, 50, 90, 100]) - t0) / 1e3, 2).tolist()
+        print(nm, "entry", pc(ent), "done", pc(done), "exit", pc(ext))
     if os.environ.get("TRACE_PHASES") and nm.startswith("qkv"):
         ph = {k: np.round(np.percentile((ent + c[:, i] / GHZ - t0) / 1e3, [50, 100]), 2).tolist()
               for k, i in (("s1", 1), ("s3", 3), ("s5", 5), ("end6", 6))}
