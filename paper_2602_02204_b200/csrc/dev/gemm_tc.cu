@@ -19,6 +19,8 @@
 // projections; reused by the DiT (diffusion_engine.hpp:28-43 replacement).
 #include <cuda.h>
 #include <cstdlib>
+#include <cstring>
+#include <utility>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -414,6 +416,17 @@ static int bn_for(const GemmWeight& w, int M) {
       return e ? std::atoi(e) : 0;
     }();
     if (forced == 64 || forced == 128 || forced == 256) return forced;
+    // OMNI_DIT_DEEP_BN=<16|32|64>[:max_rows]: narrower token tiles for the
+    // deep-K DiT weight (MLP down, K = 4d) at small batches, where 8 fat-tile
+    // CTAs each stream 2 MB (per-element results do not depend on BN)
+    static const std::pair<int, int> deep = [] {
+      const char* e = std::getenv("OMNI_DIT_DEEP_BN");
+      if (!e) return std::pair<int, int>{0, 0};
+      int bn = std::atoi(e), mx = 256;
+      if (const char* c = std::strchr(e, ':')) mx = std::atoi(c + 1);
+      return std::pair<int, int>{bn, mx};
+    }();
+    if (deep.first && w.K >= 4096 && M <= deep.second) return deep.first;
     // Widest token tile (fewest CTAs), not the isolated-latency optimum: the
     // DiT shares the GPU with two latency-bound AR chains, and fat tiles leave
     // them SMs -- measured +6.5 % pipeline req/s over a fill-the-SMs cost
