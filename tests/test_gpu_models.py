@@ -174,6 +174,39 @@ def test_talker_parity_small(small_thinker):
     ta.close()
 
 
+def test_talker_parity_default_dims():
+    """Full-size Talker (d 2048, 4 layers, V 64, conditioning projection
+    2048x2048) against the oracle: 3 conditioning rows (synthetic bf16
+    hidden rows in HBM), prefill + 12 teacher-forced decode steps."""
+    tm = D.model_default(D.TALKER)
+    d = tm.cond_dim
+    rng = np.random.default_rng(6)
+    hid = (rng.standard_normal((3, d)).astype(np.float32) * 0.8)
+    hid_bits = (hid.view(np.uint32) >> 16).astype(np.uint16)
+    buf = D.mem_alloc(2 * d * 3)
+    D.h2d(buf, hid_bits.reshape(-1))
+    rows = [buf + 2 * d * j for j in range(3)]
+    ta = D.Stage(tm, D.StageLimits(256, 8, 256, 0, 64), seed=23)
+    om = oracle.Model(tm, 23)
+    text = [17, 203, 9]
+    ta.ar_step([2], [0], [3], [0], [-1], text, cond_src=rows, cond_row=[0, 1, 2])
+    os_ = om.new_seq(64)
+    os_.feed(text, decode=False, cond_rows=[0, 1, 2], hid_rows=hid_bits)
+    codec = []
+    for m_ in range(12):
+        tin = -1 if m_ == 0 else codec[-1]
+        t, mg = ta.ar_step([2], [1], [1], [3 + m_], [m_], [tin], cond_src=[0], cond_row=[m_ // 4])
+        ot, _, _, omg = os_.feed([tin], decode=True, cond_rows=[m_ // 4])
+        if omg > MARGIN_TOL:
+            assert t[0] == ot, (m_, t[0], ot, omg)
+            assert abs(mg[0] - omg) < 2 * LOGIT_ATOL
+        assert 0 <= t[0] < 64
+        codec.append(int(t[0]))
+    print("talker default codec", codec)
+    ta.close()
+    D.mem_free(buf)
+
+
 def test_pack_hidden_bit_exact(small_thinker):
     th, _ = small_thinker
     d = th.model.d_model
