@@ -141,6 +141,36 @@ def test_thinker_parity_default_dims():
     st.close()
 
 
+def test_thinker_batch_invariance_default_dims():
+    """Full-size Thinker: one sequence's decode row is bit-identical whether
+    it runs alone (M=1: 16-token tile, push split-K), among 20 decoders
+    (32-token tile, push) or among 40 decoders (64-token tile, cluster-pull
+    reduction) -- split factors are per weight, sum order per rank fixed."""
+    m = D.model_default(D.THINKER)
+    st = D.Stage(m, D.StageLimits(256, 48, 256, 0, 64), seed=9)
+    d = m.d_model
+    rng = np.random.default_rng(12)
+    p = list(rng.integers(1, 256, size=30))
+    others = {o: list(rng.integers(1, 256, size=5 + o % 7)) for o in range(100, 139)}
+    res = []
+    for n_other in (0, 19, 39):
+        seq = 1 + n_other
+        st.ar_step([seq], [0], [30], [0], [-1], p)
+        batch = sorted(others)[:n_other]
+        for o in batch:
+            st.ar_step([o], [0], [len(others[o])], [0], [-1], others[o])
+        ids = sorted([seq] + batch)
+        pos = [30 if s == seq else len(others[s]) for s in ids]
+        t, _ = st.ar_step(ids, [1] * len(ids), [1] * len(ids), pos, [0] * len(ids), [-1] * len(ids))
+        res.append((int(t[ids.index(seq)]), hidden_bits(st, seq, 0, d)))
+        for s in ids:
+            st.release(s)
+    for tok, h in res[1:]:
+        assert tok == res[0][0]
+        assert np.array_equal(h, res[0][1]), "decode row depends on the batch"
+    st.close()
+
+
 def test_talker_parity_small(small_thinker):
     th, _ = small_thinker
     d = th.model.d_model
