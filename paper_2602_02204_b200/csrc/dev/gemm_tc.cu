@@ -329,23 +329,24 @@ template <int BN>
 constexpr size_t epi_smem_for() {
   return (size_t)BN * 128 * 4 * 3 / 2;  // own partial + reduced slice (S >= 2)
 }
-template <int BN, int STAGES = stages_for<BN>(), bool PUSH = false>
+template <int BN, int STAGES = stages_for<BN>(), int kPushS = 0>
 constexpr size_t smem_for() {
+  constexpr bool PUSH = kPushS > 0;
   constexpr size_t pipe = STAGES * (kBlockM * kBlockK * 2 + BN * kBlockK * 2);
   // + [push receive buffer] + barriers / tmem slot (256 B) + per-column
   // input-RMS scales (4 B x BN) + flag / receive barrier
   return 1024 + (pipe > epi_smem_for<BN>() ? pipe : epi_smem_for<BN>()) + (PUSH ? (size_t)BN * 128 * 4 : 0) +
-         (PUSH ? (size_t)BN / 2 * 128 * 4 + 128 : 0) + 256 + 4 * BN + 16;  // + staged epilogue inputs (kPushS >= 2)
+         (PUSH ? (size_t)BN / (PUSH ? kPushS : 1) * 128 * 4 + 128 : 0) + 256 + 4 * BN + 16;  // + staged epilogue inputs
 }
 // push split-K variants keep two CTAs per SM (<= ~113 KB): one stage less
-static_assert(smem_for<16, 5, true>() <= 113 * 1024, "BN16 push tile must fit twice per SM");
-static_assert(smem_for<32, 4, true>() <= 113 * 1024, "BN32 push tile must fit twice per SM");
+static_assert(smem_for<16, 5, 2>() <= 113 * 1024, "BN16 push tile must fit twice per SM");
+static_assert(smem_for<32, 4, 2>() <= 113 * 1024, "BN32 push tile must fit twice per SM");
 
 template <int BN, int EPI, int STAGES = stages_for<BN>(), int kPushS = 0>
 cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                       cudaStream_t st) {
   auto kern = gemm_tc_kernel<BN, STAGES, EPI, kPushS>;
-  constexpr size_t smem = smem_for<BN, STAGES, (kPushS > 0)>();
+  constexpr size_t smem = smem_for<BN, STAGES, kPushS>();
   static std::atomic<uint64_t> configured{0};  // per instantiation, per device
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
   if (a.splits > 8) {  // 16-CTA clusters are non-portable (opt-in)
@@ -392,7 +393,7 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
       if (push && a.splits == 8) return launch_bn<32, EPI, 4, 8>(w, x, a, st);
       if (push && a.splits == 2) return launch_bn<32, EPI, 4, 2>(w, x, a, st);
       return launch_bn<32, EPI>(w, x, a, st);
-    case 64: return launch_bn<64, EPI>(w, x, a, st);
+    case 64: return launch_bn<64, EPI>(w, x, a, st);  // push needs a 3-stage ring here: measured slower
     case 128: return launch_bn<128, EPI>(w, x, a, st);
     default: return launch_bn<256, EPI>(w, x, a, st);
   }
