@@ -13,6 +13,7 @@
 // All per-row work depends only on that row's own inputs (batch invariance,
 // SURVEY §0.7a). Replaces StageModel::prefill/decode (registry.hpp:79-89;
 // mock semantics reference_pipeline.hpp:96-154).
+#include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -31,6 +32,21 @@ __global__ void embed_kernel(const ArStepDev s, const __nv_bfloat16* __restrict_
                              uint64_t pf_bytes) {
   prefetch_l2_share(pf_ptr, pf_bytes, blockIdx.x, gridDim.x, threadIdx.x, blockDim.x);
   embed_row(blockIdx.x, s, emb, emb2, hproj, cond_table, cond_rows, d, start_id, x, xb, ss_out, ss_ld, PdlDep{});
+}
+
+// Step descriptor blob pinned host -> device by the step's first kernel
+// (UVA load of the pinned staging buffer) instead of a copy-engine H2D.
+__global__ void desc_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int n16) {
+  pdl_wait();  // the previous step's kernels may still read the blob
+  pdl_trigger();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
+}
+
+cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  const int n16 = (int)((bytes + 15) / 16);
+  const int blocks = std::min(16, (n16 + 255) / 256);
+  return launch_k(desc_copy_kernel, dim3(blocks), dim3(256), 0, st, 1, static_cast<uint4*>(dst),
+                  static_cast<const uint4*>(src), n16);
 }
 
 __global__ void gather_cond_kernel(const ArStepDev s, int d, __nv_bfloat16* __restrict__ out) {

@@ -61,7 +61,8 @@ cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, i
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
                                 cudaStream_t st);
 // Fused final RMSNorm + LM head (CUDA cores) + greedy argmax, vocab <= 256.
-cudaError_t attn_trace_set(void* p);  // debug: per-CTA phase stamps of attention launches
+cudaError_t attn_trace_set(void* p);
+cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);  // debug: per-CTA phase stamps of attention launches
 // Grid (vocab / kHeadIdsPerCta, n_dec); cnt = n_dec zeroed tickets (self-resetting).
 constexpr int kHeadMaxVocab = 256;
 constexpr int kHeadIdsPerCta = 16;

@@ -592,6 +592,32 @@ void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   OMNI_KERNEL(chain_launch(P, total, st->stream));
 }
 
+// Descriptor blob at FIXED offsets (capacity-sized regions, so the device
+// pointers baked into a captured step graph never change):
+//   entries | decode entry list | attention blocks | rows | page table
+struct ArDescLayout {
+  size_t off_dec, off_blk, off_rows, off_pt, reserve;
+};
+ArDescLayout ar_desc_layout(const omni_stage* st) {
+  const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
+  ArDescLayout l;
+  l.off_dec = align16(cap_e * sizeof(ArEntryDesc));
+  l.off_blk = l.off_dec + align16(cap_e * sizeof(int32_t));
+  l.off_rows = l.off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
+  l.off_pt = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
+  l.reserve = l.off_pt + cap_e * st->max_pages * sizeof(int32_t);
+  return l;
+}
+ArStepDev ar_step_dev(const omni_stage* st, const ArDescLayout& lay) {
+  ArStepDev sd;
+  sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
+  sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + lay.off_rows);
+  sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_pt);
+  sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_dec);
+  sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + lay.off_blk);
+  sd.max_pages = st->max_pages;
+  return sd;
+}
 // The per-kernel AR step (PDL chain) for one launch geometry; everything
 // step-specific is read from the fixed-offset descriptor blob, so the launch
 // sequence depends on (n_rows, n_blocks, n_dec, cond_prefill) only -- the
@@ -602,6 +628,10 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   const bool talker = m.kind == OMNI_MODEL_TALKER;
   cudaStream_t s = st->stream;
+  if (st->desc_kernel) {  // the whole (capacity-sized) blob: the size is baked into step graphs
+    const ArDescLayout lay = ar_desc_layout(st);
+    OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, lay.reserve, s));
+  }
   int trace_slot = 0;  // OMNI_STEP_TRACE: one slot per GEMM launch, in launch order
   auto traced = [&](GemmEpilogue e) {
     if (st->step_trace && trace_slot < kStepTraceLaunches)
@@ -709,32 +739,6 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   }
 }
 
-// Descriptor blob at FIXED offsets (capacity-sized regions, so the device
-// pointers baked into a captured step graph never change):
-//   entries | decode entry list | attention blocks | rows | page table
-struct ArDescLayout {
-  size_t off_dec, off_blk, off_rows, off_pt, reserve;
-};
-ArDescLayout ar_desc_layout(const omni_stage* st) {
-  const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
-  ArDescLayout l;
-  l.off_dec = align16(cap_e * sizeof(ArEntryDesc));
-  l.off_blk = l.off_dec + align16(cap_e * sizeof(int32_t));
-  l.off_rows = l.off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
-  l.off_pt = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
-  l.reserve = l.off_pt + cap_e * st->max_pages * sizeof(int32_t);
-  return l;
-}
-ArStepDev ar_step_dev(const omni_stage* st, const ArDescLayout& lay) {
-  ArStepDev sd;
-  sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
-  sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + lay.off_rows);
-  sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_pt);
-  sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_dec);
-  sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + lay.off_blk);
-  sd.max_pages = st->max_pages;
-  return sd;
-}
 uint64_t ar_graph_key(int n_rows, int n_blocks, int n_dec, bool cond_prefill) {
   return ((uint64_t)n_rows << 40) | ((uint64_t)n_blocks << 20) | ((uint64_t)n_dec << 1) | (cond_prefill ? 1u : 0u);
 }
@@ -836,9 +840,14 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   const int n_dec = (int)dec_list.size();
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
-  OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, total, cudaMemcpyHostToDevice, s));
-  counters().h2d_bytes += total;
-  OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
+  const bool kcopy = st->desc_kernel && n_rows > 0 && !(st->chain_on && !talker && n_rows <= chain_max_rows());
+  if (!kcopy) {
+    OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, total, cudaMemcpyHostToDevice, s));
+    counters().h2d_bytes += total;
+    OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
+  } else {
+    counters().h2d_bytes += lay.reserve;
+  }
   const ArStepDev sd = ar_step_dev(st, lay);
 
   const auto& m = st->m;
@@ -850,6 +859,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
     } else run_graph(st, key, [&] {
       launch_ar_kernels(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0);
     });
+    if (kcopy) OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));  // staging read by the step's first kernel
     if (n_dec > 0) {
       // tokens and margins in one copy: [n_dec x i32 | n_dec x f32]
       if (!st->zc_tok)
@@ -946,7 +956,12 @@ void prewarm_dit_graphs(omni_stage* st) {
   const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
   for (int nt = kDitPadTok; nt <= upto; nt += kDitPadTok) {
     const uint64_t key = dit_graph_key(nt, 0);
-    if (!st->graphs.count(key)) capture_graph(st, key, [&] { dit_chunk(st, toks_dev, nt, st->dsamples); });
+    if (!st->graphs.count(key))
+      capture_graph(st, key, [&] {
+        if (st->desc_kernel)
+          OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, (size_t)nt * sizeof(DitTokDesc), st->stream));
+        dit_chunk(st, toks_dev, nt, st->dsamples);
+      });
   }
 }
 
@@ -981,13 +996,23 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
   if (n_tok > 0) {
-    OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, bytes, cudaMemcpyHostToDevice, s));
+    // descriptors: copied by the chunk graph's first kernel (desc_kernel) or by
+    // one H2D; either way the graph reads them from the device blob
+    if (!st->desc_kernel) {
+      OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, bytes, cudaMemcpyHostToDevice, s));
+      OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
+    }
     counters().h2d_bytes += bytes;
-    OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
     const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
     for (int64_t t0 = 0; t0 < n_tok; t0 += st->tok_cap) {
       const int nt = (int)std::min<int64_t>(st->tok_cap, n_pad - t0);
-      run_graph(st, dit_graph_key(nt, t0), [&] { dit_chunk(st, toks_dev + t0, nt, st->dsamples); });
+      run_graph(st, dit_graph_key(nt, t0), [&] {
+        if (st->desc_kernel)
+          OMNI_KERNEL(launch_desc_copy(st->desc.dev + t0 * sizeof(DitTokDesc), st->desc.host + t0 * sizeof(DitTokDesc),
+                                       (size_t)nt * sizeof(DitTokDesc), s));
+        dit_chunk(st, toks_dev + t0, nt, st->dsamples);
+      });
+      if (st->desc_kernel && t0 + st->tok_cap >= n_tok) OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
       const int64_t nsamp = std::min<int64_t>(nt, n_tok - t0) * kDitSamples;  // real tokens only
       OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
                                 cudaMemcpyDeviceToHost, s));
@@ -1173,6 +1198,11 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     // OMNI_FUSED_HEAD=1: one-kernel head (measured flat at 1 row, slower at 16; default off)
     const char* fh = std::getenv("OMNI_FUSED_HEAD");
     st->fused_head = fh && fh[0] == '1';
+    // Step descriptors copied from pinned staging by the step's first kernel
+    // (UVA loads) instead of a copy-engine H2D: -9..10 µs per AR step
+    // (profiles/r01_desc_kernel_ab.txt). OMNI_DESC_KERNEL=0: cudaMemcpyAsync.
+    const char* dk = std::getenv("OMNI_DESC_KERNEL");
+    st->desc_kernel = !(dk && dk[0] == '0');
     if (st->lim.max_batch_tokens <= 0) st->lim.max_batch_tokens = 256;
     if (st->lim.max_resident <= 0) st->lim.max_resident = 64;
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;

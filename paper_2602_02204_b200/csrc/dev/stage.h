@@ -110,6 +110,7 @@ struct omni_stage {
   omni_dev::Staging desc, pack;
   int32_t* h_tok = nullptr;
   bool zc_tok = false;
+  bool desc_kernel = false;  // step descriptors copied by the step's first kernel (OMNI_DESC_KERNEL)
   unsigned long long* step_trace = nullptr;  // OMNI_STEP_TRACE debug stamps  // h_tok is mapped: kernels write results to host memory directly
   int32_t* h_samples = nullptr;
   bool pending = false;
