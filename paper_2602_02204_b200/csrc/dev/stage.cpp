@@ -331,6 +331,9 @@ void build_dit(omni_stage* st) {
     }
   }
   OMNI_CUDA(cudaMallocHost(&st->h_samples, (size_t)R * sizeof(int32_t)));
+  // Zero-copy waveform samples (OMNI_ZC_TOK, default on): the Euler epilogue
+  // of the last step stores them straight into the pinned host buffer (UVA).
+  if (const char* e = std::getenv("OMNI_ZC_TOK"); !(e && e[0] == '0')) st->dsamples = st->h_samples;
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
 }
 
@@ -1014,8 +1017,9 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
       });
       if (st->desc_kernel && t0 + st->tok_cap >= n_tok) OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
       const int64_t nsamp = std::min<int64_t>(nt, n_tok - t0) * kDitSamples;  // real tokens only
-      OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
-                                cudaMemcpyDeviceToHost, s));
+      if (st->dsamples != st->h_samples)
+        OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
+                                  cudaMemcpyDeviceToHost, s));
       counters().d2h_bytes += nsamp * sizeof(int32_t);
       if (n_tok > st->tok_cap) {  // multi-chunk: land each chunk before reusing h_samples
         OMNI_CUDA(cudaStreamSynchronize(s));
