@@ -341,6 +341,7 @@ constexpr size_t smem_for() {
 // push split-K variants keep two CTAs per SM (<= ~113 KB): one stage less
 static_assert(smem_for<16, 5, 2>() <= 113 * 1024, "BN16 push tile must fit twice per SM");
 static_assert(smem_for<32, 4, 2>() <= 113 * 1024, "BN32 push tile must fit twice per SM");
+static_assert(smem_for<128, 3>() <= 113 * 1024, "BN128 3-stage tile must fit twice per SM");
 
 template <int BN, int EPI, int STAGES = stages_for<BN>(), int kPushS = 0>
 cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
@@ -394,7 +395,18 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
       if (push && a.splits == 2) return launch_bn<32, EPI, 4, 2>(w, x, a, st);
       return launch_bn<32, EPI>(w, x, a, st);
     case 64: return launch_bn<64, EPI>(w, x, a, st);  // push needs a 3-stage ring here: measured slower
-    case 128: return launch_bn<128, EPI>(w, x, a, st);
+    case 128: {
+      // decode weights (prefill / mixed steps): a 6-stage 128-token tile holds
+      // a whole SM, so grids over 148 CTAs (QKV: 192) would run in two waves;
+      // a 3-stage ring fits two CTAs per SM (OMNI_BN128_2CTA=0: off)
+      static const bool two = [] {
+        const char* e = std::getenv("OMNI_BN128_2CTA");
+        return !(e && e[0] == '0');
+      }();
+      const int ctas = (w.N_pad / kBlockM) * ((a.M + 127) / 128) * a.splits;
+      if (two && !w.fill_sms && ctas > 148) return launch_bn<128, EPI, 3>(w, x, a, st);
+      return launch_bn<128, EPI>(w, x, a, st);
+    }
     default: return launch_bn<256, EPI>(w, x, a, st);
   }
 }
