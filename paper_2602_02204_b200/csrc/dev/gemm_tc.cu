@@ -397,14 +397,16 @@ cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& 
     case 64: return launch_bn<64, EPI>(w, x, a, st);  // push needs a 3-stage ring here: measured slower
     case 128: {
       // decode weights (prefill / mixed steps): a 6-stage 128-token tile holds
-      // a whole SM, so grids over 148 CTAs (QKV: 192) would run in two waves;
-      // a 3-stage ring fits two CTAs per SM (OMNI_BN128_2CTA=0: off)
-      static const bool two = [] {
+      // a whole SM -- grids over 148 CTAs (QKV: 192) run in two waves and the
+      // next kernel's CTAs cannot co-reside to prefetch (PDL). A 3-stage ring
+      // (96 KB in flight, as much as the 16-token 6-stage tile) fits two CTAs
+      // per SM. OMNI_BN128_2CTA=0: 6 stages; =2: only for grids > 148 CTAs.
+      static const int two = [] {
         const char* e = std::getenv("OMNI_BN128_2CTA");
-        return !(e && e[0] == '0');
+        return e ? std::atoi(e) : 1;
       }();
       const int ctas = (w.N_pad / kBlockM) * ((a.M + 127) / 128) * a.splits;
-      if (two && !w.fill_sms && ctas > 148) return launch_bn<128, EPI, 3>(w, x, a, st);
+      if (!w.fill_sms && (two == 1 || (two == 2 && ctas > 148))) return launch_bn<128, EPI, 3>(w, x, a, st);
       return launch_bn<128, EPI>(w, x, a, st);
     }
     default: return launch_bn<256, EPI>(w, x, a, st);

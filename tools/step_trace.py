@@ -33,12 +33,20 @@ for i in range(0, B, 4):
     st.ar_step(grp, [D.PREFILL] * len(grp), [P] * len(grp), [0] * len(grp), [-1] * len(grp), toks, cs, cr)
 AT = D.mem_alloc(8 * 8 * 8192)
 prev = [-1] * B
+PF = int(os.environ.get("TRACE_PREFILL", "0"))  # add a PF-token prefill chunk to every traced step
 for k in range(8):
     D.mem_set(AT, 0, 8 * 8 * 8192)
     lib.omni_k_debug_traces(C.c_uint64(AT), C.c_uint64(0))
     cs = [0] * B if cond else None
     cr = [0] * B if cond else None
-    tok, _ = st.ar_step(ids, [D.DECODE] * B, [1] * B, [P + k] * B, [k] * B, prev, cs, cr)
+    if PF and not cond:
+        new = 5000 + k
+        tok, _ = st.ar_step(ids + [new], [D.DECODE] * B + [D.PREFILL], [1] * B + [PF], [P + k] * B + [0],
+                            [k] * B + [-1], prev + [(5 * j + k) % 250 + 1 for j in range(PF)])
+        st.release(new)
+        tok = tok[:B]
+    else:
+        tok, _ = st.ar_step(ids, [D.DECODE] * B, [1] * B, [P + k] * B, [k] * B, prev, cs, cr)
     prev = [int(t) for t in tok]
     lib.omni_k_debug_traces(C.c_uint64(0), C.c_uint64(0))
 step_us = st.last_step_us()
