@@ -425,6 +425,16 @@ bool gemm_push_enabled() {  // OMNI_SPLITK_PUSH=0: cluster-barrier + DSMEM-pull 
 
 static int bn_for(const GemmWeight& w, int M) {
   int bn = gemm_block_n(M);
+  if (!w.fill_sms && bn > 128) {
+    // decode weights in big prefill steps: two 128-token tiles (3-stage,
+    // two CTAs per SM) instead of one 256-token tile that holds a whole SM
+    // (OMNI_BN256_SPLIT=0: keep 256)
+    static const bool split = [] {
+      const char* e = std::getenv("OMNI_BN256_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    if (split) return 128;
+  }
   if (w.fill_sms && bn > 64) {
     static const int forced = [] {  // OMNI_DIT_BN: experiments only
       const char* e = std::getenv("OMNI_DIT_BN");
