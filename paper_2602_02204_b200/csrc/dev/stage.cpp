@@ -1461,7 +1461,11 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
     staging_reserve(src->pack, total);
     auto* cd = reinterpret_cast<PackChunkDesc*>(src->pack.host);
     auto* tk = reinterpret_cast<int32_t*>(src->pack.host + off_tok);
-    const auto* tk_dev = reinterpret_cast<const int32_t*>(src->pack.dev + off_tok);
+    // desc_kernel: the pack kernel reads its descriptors straight from the
+    // pinned staging buffer (UVA) -- no copy-engine H2D ahead of it on the
+    // thinker stream, where the next Thinker step queues behind it
+    const uint8_t* desc_base = src->desc_kernel ? src->pack.host : src->pack.dev;
+    const auto* tk_dev = reinterpret_cast<const int32_t*>(desc_base + off_tok);
     int at = 0;
     for (int c = 0; c < n_chunks; ++c) {
       auto it = src->seqs.find(seq_id[c]);
@@ -1470,12 +1474,15 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
       for (int r = begin[c]; r < end[c]; ++r, ++at) tk[at] = tokens[at];
     }
     cudaStream_t s = src->stream;
-    OMNI_CUDA(cudaMemcpyAsync(src->pack.dev, src->pack.host, total, cudaMemcpyHostToDevice, s));
+    if (!src->desc_kernel) {
+      OMNI_CUDA(cudaMemcpyAsync(src->pack.dev, src->pack.host, total, cudaMemcpyHostToDevice, s));
+      OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));
+    }
     counters().h2d_bytes += total;
-    OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));
-    OMNI_KERNEL(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(src->pack.dev), n_chunks,
-                                 max_rows, src->ring, src->m.d_model, src->ring_rows,
-                                 reinterpret_cast<uint8_t*>(dst_base), s));
+    OMNI_KERNEL(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(desc_base), n_chunks, max_rows,
+                                 src->ring, src->m.d_model, src->ring_rows, reinterpret_cast<uint8_t*>(dst_base),
+                                 s));
+    if (src->desc_kernel) OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));  // staging read by the kernel
   });
 }
 
