@@ -33,19 +33,22 @@ def ar_probe(kind: int, batches, prompt: int = 64, steps: int = 12):
     out = []
     for B in batches:
         ids = list(range(1000 * (B + 1), 1000 * (B + 1) + B))
-        # prefill in chunks of <= 256 tokens (4 x 64)
-        for i in range(0, B, 4):
-            grp = ids[i:i + 4]
-            toks = [(7 * j + 3) % 250 + 1 for j in range(prompt)] * len(grp)
-            cs = [cond + 2 * m.cond_dim * (j % 256) for j in range(len(toks))] if kind == D.TALKER else None
-            cr = [j for _ in grp for j in range(prompt)] if kind == D.TALKER else None
-            st.ar_step(grp, [D.PREFILL] * len(grp), [prompt] * len(grp), [0] * len(grp), [-1] * len(grp),
-                       toks, cs, cr)
+        # prefill in steps of <= 256 tokens (groups of whole prompts, long prompts chunked)
+        per = max(1, 256 // prompt)
+        for i in range(0, B, per):
+            grp = ids[i:i + per]
+            for at in range(0, prompt, 256):
+                sp = min(256, prompt - at)
+                toks = [(7 * j + 3) % 250 + 1 for j in range(at, at + sp)] * len(grp)
+                cs = [cond + 2 * m.cond_dim * (j % 256) for j in range(len(toks))] if kind == D.TALKER else None
+                cr = [j % 64 for _ in grp for j in range(at, at + sp)] if kind == D.TALKER else None
+                st.ar_step(grp, [D.PREFILL] * len(grp), [sp] * len(grp), [at] * len(grp), [-1] * len(grp),
+                           toks, cs, cr)
         prev = [-1] * B
         ts = []
         for k in range(steps):
             cs = [0] * B if kind == D.TALKER else None
-            cr = [min(k // 4, prompt - 1)] * B if kind == D.TALKER else None
+            cr = [min(k // 4, prompt - 1, 63)] * B if kind == D.TALKER else None
             tok, _ = st.ar_step(ids, [D.DECODE] * B, [1] * B, [prompt + k] * B, [k] * B, prev, cs, cr)
             prev = [int(t) for t in tok]
             if k >= 2:
@@ -86,10 +89,17 @@ def dit_probe(ntoks):
 
 if __name__ == "__main__":
     quick = "--quick" in sys.argv
-    if "--dit-only" not in sys.argv:
+    ctxs = [int(a.split("=")[1]) for a in sys.argv if a.startswith("--ctx=")]
+    if ctxs:  # step time vs context length (attention scaling), 16 decode rows
+        for c in ctxs:
+            ar_probe(D.TALKER, [16], prompt=c)
+            ar_probe(D.THINKER, [4], prompt=c)
+    elif "--dit-only" not in sys.argv:
         ar_probe(D.THINKER, [1, 4, 16] if quick else [1, 2, 4, 8, 16, 32, 64])
         ar_probe(D.TALKER, [1, 16] if quick else [1, 4, 16, 32, 64])
-    if "--dit64" in sys.argv:
+    if ctxs:
+        pass
+    elif "--dit64" in sys.argv:
         dit_probe([64])
     elif "--ar-only" not in sys.argv:
         dit_probe([8, 64] if quick else [8, 32, 64, 128, 256, 512])
