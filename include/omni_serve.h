@@ -44,8 +44,9 @@ typedef struct omni_bench_spec {
   uint32_t prompt_min, prompt_max;
   const char* clock;     /* "virtual" (parity), "device" (performance), "wall" */
   int32_t trace;         /* 1 = record the reference-harness trace */
-  int32_t talker_chunk;  /* >0 overrides edge 0 chunk size */
-  int32_t vocoder_chunk; /* >0 overrides edge 1 chunk size */
+  int32_t talker_chunk;  /* >0 overrides the Thinker2Talker edge chunk size */
+  int32_t vocoder_chunk; /* >0 overrides the Talker2Vocoder edge chunk size */
+  int32_t capture;       /* 1 = keep per-request outputs + thinker hidden rows (parity tests) */
 } omni_bench_spec;
 
 typedef struct omni_bench_result {
@@ -69,6 +70,19 @@ typedef struct omni_bench_result {
 omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* spec, omni_bench_result* out);
 /* Text of the last bench: what 0 = CSV v1, 1 = trace. Returns the full length. */
 size_t omni_pipeline_text(omni_pipeline* p, int32_t what, char* buf, size_t cap);
+
+/* Per-request outputs of the last bench run with spec->capture = 1 (parity
+ * tests replay them teacher-forced through the CPU oracle). Copies up to
+ * `cap` bytes into buf (may be NULL) and returns the full byte length; 0 for
+ * an unknown request. */
+enum {
+  OMNI_OUT_PROMPT = 0, /* u8 prompt tokens                         */
+  OMNI_OUT_TEXT = 1,   /* i32 thinker tokens                        */
+  OMNI_OUT_CODEC = 2,  /* i32 talker codec tokens                   */
+  OMNI_OUT_WAVE = 3,   /* i32 waveform samples (first diffusion exit) */
+  OMNI_OUT_HIDDEN = 4  /* u16 bf16 bits of the thinker hidden rows, [text index][d] */
+};
+size_t omni_pipeline_output(omni_pipeline* p, uint64_t request_id, int32_t what, void* buf, size_t cap);
 
 const char* omni_serve_last_error(void);
 

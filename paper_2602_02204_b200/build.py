@@ -64,6 +64,7 @@ def _build_lib(name: str, srcdir: Path, out: Path, link: list[str], jobs: int) -
     srcs = sorted([*srcdir.glob("*.cu"), *srcdir.glob("*.cpp")])
     headers = sorted([*(CSRC / "dev").glob("*.h"), *(CSRC / "dev").glob("*.cuh"),
                       *(CSRC / "serve").glob("*.h"), *(CSRC / "serve").glob("*.hpp"),
+                      *(CSRC / "serve" / "omni").glob("*.hpp"),
                       *(ROOT / "include").glob("*.h")])
     objs_dir = BUILD / name
     with cf.ThreadPoolExecutor(max_workers=jobs) as ex:

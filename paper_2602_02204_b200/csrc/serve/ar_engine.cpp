@@ -270,6 +270,27 @@ void ArEngine::run_entries_batched() {
       fail(e.request_id, err.what());
     }
   }
+  // device admission per entry: one sequence that cannot get KV pages fails
+  // alone, before anything is launched
+  if (model_.reserve) {
+    for (const auto& t : todo) {
+      Resident* r = find(t.rid);
+      if (!r) continue;
+      BatchSlot b;
+      b.request_id = t.rid;
+      b.phase = t.phase;
+      b.span = t.span;
+      b.pos0 = t.pos0;
+      b.out_index = t.out_index;
+      b.seq = &r->seq;
+      b.ctx = r->ctx.get();
+      try {
+        model_.reserve(b);
+      } catch (const OmniError& err) {
+        fail(t.rid, err.what());
+      }
+    }
+  }
   prune_failed();
   slots_.clear();
   for (const auto& t : todo) {

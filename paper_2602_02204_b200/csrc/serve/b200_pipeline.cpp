@@ -118,6 +118,8 @@ struct ArStage {
   std::unique_ptr<Arena> arena;
   ArStage* upstream = nullptr;  // talker: the stage whose arena it reads
   Tracer* tracer = nullptr;
+  // parity capture (tests): thinker hidden rows per request, [index][d] bf16 bits
+  std::map<uint64_t, std::vector<uint16_t>>* capture = nullptr;
   // step arrays (kept alive until the step completes)
   std::vector<uint64_t> seq_id, cond_src;
   std::vector<int32_t> phase, span, pos0, out_index, tokens, cond_row, tok_out;
@@ -220,6 +222,20 @@ struct ArStage {
     for (size_t i = 0; i < slots.size(); ++i) {
       out[i] = tok_out[i];
       if (slots[i].phase == Phase::DECODE && tok_out[i] < 0) throw ForwardError("device step returned no token");
+    }
+    if (capture && kind == OMNI_MODEL_THINKER) capture_rows(slots);
+  }
+
+  // Copies the hidden-ring rows the step just wrote to the host (parity tests only).
+  void capture_rows(const std::vector<BatchSlot>& slots) {
+    const size_t d = static_cast<size_t>(model.d_model);
+    for (const BatchSlot& b : slots) {
+      if (b.phase != Phase::DECODE) continue;
+      uint64_t row = 0;
+      dev_ok(omni_seq_hidden_row(st, b.request_id, b.out_index, &row), "omni_seq_hidden_row");
+      auto& v = (*capture)[b.request_id];
+      if (v.size() < (static_cast<size_t>(b.out_index) + 1) * d) v.resize((static_cast<size_t>(b.out_index) + 1) * d);
+      dev_ok(omni_mem_d2h(v.data() + static_cast<size_t>(b.out_index) * d, row, d * 2), "omni_mem_d2h");
     }
   }
 
@@ -382,6 +398,7 @@ omni_model_desc model_for(int kind, bool small) {
 
 struct B200Pipeline::Impl {
   B200Options opt;
+  std::map<uint64_t, std::vector<uint16_t>> captured;
   std::map<std::string, std::unique_ptr<ArStage>> ar;
   std::map<std::string, std::unique_ptr<DitStage>> dit;
   Tracer* tracer = nullptr;
@@ -465,6 +482,15 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
 }
 
 B200Pipeline::~B200Pipeline() = default;
+
+void B200Pipeline::set_capture(bool on) {
+  impl_->captured.clear();
+  for (auto& [_, s] : impl_->ar) s->capture = on ? &impl_->captured : nullptr;
+}
+const std::vector<uint16_t>* B200Pipeline::captured_hidden(uint64_t rid) const {
+  auto it = impl_->captured.find(rid);
+  return it == impl_->captured.end() ? nullptr : &it->second;
+}
 
 void B200Pipeline::set_tracer(Tracer* t) {
   impl_->tracer = t;

@@ -1,7 +1,9 @@
 // C ABI of libomni_serve (include/omni_serve.h).
 #include <chrono>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <vector>
 #include <set>
 #include <string>
 
@@ -54,6 +56,11 @@ struct omni_pipeline {
   std::unique_ptr<omni::B200Pipeline> dev;
   omni::FunctionRegistry reg;
   std::string csv, trace;
+  struct Captured {
+    std::vector<uint8_t> prompt;
+    std::vector<int32_t> text, codec, wave;
+  };
+  std::map<uint64_t, Captured> outputs;  // spec->capture: per-request outputs of the last bench
 };
 
 extern "C" {
@@ -91,10 +98,13 @@ omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* s, omni
   return guard([&] {
     omni::DeploymentPlan plan = p->plan;
     plan.clock_kind = s->clock ? s->clock : "device";
-    if (s->talker_chunk > 0 && !plan.graph.edges.empty())
-      plan.graph.edges[0].streaming_chunk_size = static_cast<uint32_t>(s->talker_chunk);
-    if (s->vocoder_chunk > 0 && plan.graph.edges.size() > 1)
-      plan.graph.edges[1].streaming_chunk_size = static_cast<uint32_t>(s->vocoder_chunk);
+    // chunk overrides by edge role (transfer function), not edge position
+    for (auto& e : plan.graph.edges) {
+      if (s->talker_chunk > 0 && e.transfer_ref == "Thinker2Talker")
+        e.streaming_chunk_size = static_cast<uint32_t>(s->talker_chunk);
+      if (s->vocoder_chunk > 0 && e.transfer_ref == "Talker2Vocoder")
+        e.streaming_chunk_size = static_cast<uint32_t>(s->vocoder_chunk);
+    }
     omni::bench::WorkloadSpec spec;
     spec.n = s->n;
     spec.seed = s->seed;
@@ -109,6 +119,10 @@ omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* s, omni
     const std::string th = plan.graph.entry;
     bo.thinker_stage = th;
     bo.talker_stage = "talker";
+    for (const auto& n : plan.graph.nodes)
+      if (n.kind == omni::StageKind::AR && n.forward_ref == "talker_forward") bo.talker_stage = n.id;
+    p->outputs.clear();
+    p->dev->set_capture(s->capture != 0);
     omni::Tracer tracer;
     p->dev->set_tracer(s->trace ? &tracer : nullptr);
     p->dev->reset_counters();
@@ -156,9 +170,13 @@ omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* s, omni
         digest = fnv_i32(out.text_tokens, digest);
         digest = fnv_i32(out.codec_tokens, digest);
         digest = fnv_i32(out.waveform, digest);
-        if (out.status == "DONE") {
-          ++rep.completed;
-          r->text_tokens += 0;
+        if (out.status == "DONE") ++rep.completed;
+        if (s->capture) {
+          auto& c = p->outputs[workload[i].request_id];
+          c.prompt = workload[i].prompt_tokens;
+          c.text = out.text_tokens;
+          c.codec = out.codec_tokens;
+          c.wave = out.waveform;
         }
         const auto& m = out.metrics;
         if (m.submitted_at != omni::kTimeUnset) first = std::min(first, m.submitted_at);
@@ -224,6 +242,28 @@ omni_status omni_pipeline_bench(omni_pipeline* p, const omni_bench_spec* s, omni
     p->csv = rep.csv;
     p->trace = std::move(tracer.out);
   });
+}
+
+size_t omni_pipeline_output(omni_pipeline* p, uint64_t request_id, int32_t what, void* buf, size_t cap) {
+  auto it = p->outputs.find(request_id);
+  if (it == p->outputs.end()) return 0;
+  const auto& c = it->second;
+  const void* src = nullptr;
+  size_t n = 0;
+  switch (what) {
+    case OMNI_OUT_PROMPT: src = c.prompt.data(), n = c.prompt.size(); break;
+    case OMNI_OUT_TEXT: src = c.text.data(), n = c.text.size() * 4; break;
+    case OMNI_OUT_CODEC: src = c.codec.data(), n = c.codec.size() * 4; break;
+    case OMNI_OUT_WAVE: src = c.wave.data(), n = c.wave.size() * 4; break;
+    case OMNI_OUT_HIDDEN: {
+      const auto* h = p->dev->captured_hidden(request_id);
+      if (h) src = h->data(), n = h->size() * 2;
+      break;
+    }
+    default: return 0;
+  }
+  if (buf && src) std::memcpy(buf, src, std::min(cap, n));
+  return n;
 }
 
 size_t omni_pipeline_text(omni_pipeline* p, int32_t what, char* buf, size_t cap) {

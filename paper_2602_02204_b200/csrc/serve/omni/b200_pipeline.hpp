@@ -44,6 +44,10 @@ class B200Pipeline {
   // Thinker2Talker / Talker2Vocoder / denoise (+ dit_image) into `reg`.
   void register_into(FunctionRegistry& reg);
   void set_tracer(Tracer* t);
+  // Parity capture (tests): keep every thinker hidden row a step writes
+  // (bf16 bits, [index][d]) per request id, read back after the run.
+  void set_capture(bool on);
+  const std::vector<uint16_t>* captured_hidden(uint64_t rid) const;
   // Device milliseconds spent in steps, per stage kind (diagnostics).
   std::map<std::string, double> device_ms() const;
   std::map<std::string, uint64_t> step_counts() const;

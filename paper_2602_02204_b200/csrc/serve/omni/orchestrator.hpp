@@ -42,11 +42,19 @@ struct DeploymentPlan {
   StageGraph graph;
   std::map<StageId, EngineConfig> engines;
   std::map<std::string, TransportConfig> transports;  // keyed "from->to"
-  std::map<StageId, std::string> placement;           // stage -> "cuda:N" (B200 placement)
+  // B200 placement: stage -> "cuda:N" or a comma list "cuda:1,cuda:2" of
+  // replica devices. The reference declares this map and never
+  // reads it (orchestrator.hpp:37); here R devices = R engine replicas of the
+  // stage, requests routed by replica_for(rid, R).
+  std::map<StageId, std::string> placement;
   std::string clock_kind = "virtual";                 // virtual | wall | device
   ServerOptions server;
   std::string server_id = "0";
 };
+
+// Parsed placement of one stage: CUDA ordinals of its replicas, or
+// {default_dev} when the plan does not place it.
+std::vector<int> placement_devices(const DeploymentPlan& plan, const StageId& stage, int default_dev = 0);
 
 struct FinalOutput {
   std::vector<int32_t> text_tokens;
@@ -107,6 +115,9 @@ class Orchestrator {
   // introspection (bench / tests)
   uint64_t iterations(const StageId& s) const;
   uint64_t preemptions(const StageId& s) const;
+  size_t replicas(const StageId& s) const;
+  // per-replica iteration counts (router balance)
+  std::vector<uint64_t> replica_iterations(const StageId& s) const;
 
  private:
   struct Pending {
@@ -148,7 +159,7 @@ class Orchestrator {
   void admit_request(Pending s, uint64_t now);
   void apply_transfer(InFlight& f, const TransferEdge& e, std::optional<Payload> upstream_final);
   void pump_diffusion_inflows();
-  void handle_ar_report(const StageId& stage, const StepReport& rep, uint64_t now);
+  void handle_ar_report(const StageId& stage, ArEngine& eng, const StepReport& rep, uint64_t now);
   void on_diffusion_output(const StageId& stage, const DiffusionOutput& out, uint64_t now);
   bool is_exit(const StageId& s) const;
   InFlight* find_inflight(uint64_t rid);
@@ -156,16 +167,19 @@ class Orchestrator {
   void fail_request(uint64_t rid, const StageId& stage, const std::string& why);
   void fail_all_locked(const std::string& why);
   void cleanup_request(uint64_t rid);
-  void complete_engine(const StageId& id, bool diffusion, uint64_t t);
+  void complete_engine(const StageId& id, size_t replica, bool diffusion, uint64_t t);
+  ArEngine& ar_for(const StageId& id, uint64_t rid);
+  DiffusionEngine& diff_for(const StageId& id, uint64_t rid);
 
   DeploymentPlan plan_;
   const FunctionRegistry* registry_;
   std::unique_ptr<Clock> clock_;
   MetricsCollector metrics_;
   std::map<std::string, std::unique_ptr<Connector>> connectors_;
-  std::map<StageId, std::unique_ptr<ArEngine>> ar_;
-  std::map<StageId, std::unique_ptr<DiffusionEngine>> diff_;
-  std::map<StageId, StageModel> models_;  // for cleanup hooks
+  // one engine per replica; replica r of a request = replica_for(rid, R)
+  std::map<StageId, std::vector<std::unique_ptr<ArEngine>>> ar_;
+  std::map<StageId, std::vector<std::unique_ptr<DiffusionEngine>>> diff_;
+  std::vector<StageModel> models_;  // for cleanup hooks
   std::vector<StageId> topo_;
   StageId text_stage_, codec_stage_, wave_stage_;
 

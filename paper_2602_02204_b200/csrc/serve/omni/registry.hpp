@@ -96,6 +96,10 @@ struct StageModel {
   std::function<void(std::vector<BatchSlot>&)> launch_batch;         // enqueue, return
   std::function<bool()> batch_ready;                                   // non-blocking
   std::function<void(std::vector<BatchSlot>&, std::vector<int32_t>&)> collect_batch;  // tokens per slot
+  // Per-entry device admission before the batched launch (KV pages for
+  // [pos0, pos0+span)); throwing fails that request alone (ar_engine.hpp:
+  // 332-334 semantics) instead of the whole step.
+  std::function<void(const BatchSlot&)> reserve;
   std::function<void(uint64_t)> release;  // drop device state (finish / preempt / fail)
   std::function<void()> flush;            // after an iteration's chunks are packed
   std::function<void(uint64_t)> cleanup;  // request left the pipeline
@@ -150,6 +154,18 @@ struct DiffusionModel {
   bool batched() const { return static_cast<bool>(launch_batch); }
 };
 
+// Replica router of a stage placed on several devices: request
+// ids are dense from 1 (bench.hpp:31-56), so (rid - 1) mod R spreads a closed
+// loop evenly and is decided once, at admission to the stage.
+inline size_t replica_for(uint64_t request_id, size_t replicas) {
+  return replicas <= 1 || request_id == 0 ? 0 : static_cast<size_t>((request_id - 1) % replicas);
+}
+// Name a stage replica's model is registered under: replica 0 keeps the
+// reference name (registry.hpp:127-129), replica r > 0 is "name#r".
+inline std::string replica_name(const std::string& n, size_t r) {
+  return r == 0 ? n : n + "#" + std::to_string(r);
+}
+
 class FunctionRegistry final : public FunctionResolver {
  public:
   void register_forward(const std::string& n, StageModel m) { fwd_[n] = std::move(m); }
@@ -167,6 +183,16 @@ class FunctionRegistry final : public FunctionResolver {
   const PreprocessFn& preprocess(const std::string& n) const { return find(pre_, n, "preprocess"); }
   const TransferFn& transfer(const std::string& n) const { return find(xfer_, n, "transfer"); }
   const DiffusionModel& denoiser(const std::string& n) const { return find(den_, n, "denoiser"); }
+  // Replica r's model: its own registration when present (device plugins
+  // register one per replica), else the shared one (stateless host plugins).
+  const StageModel& forward_for(const std::string& n, size_t r) const {
+    auto it = fwd_.find(replica_name(n, r));
+    return it != fwd_.end() ? it->second : forward(n);
+  }
+  const DiffusionModel& denoiser_for(const std::string& n, size_t r) const {
+    auto it = den_.find(replica_name(n, r));
+    return it != den_.end() ? it->second : denoiser(n);
+  }
 
  private:
   template <typename M>

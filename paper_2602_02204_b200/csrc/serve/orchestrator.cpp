@@ -40,6 +40,27 @@ void ResultHandle::finish(FinalOutput out) {
 }
 
 // ---- lifecycle ------------------------------------------------------------------
+std::vector<int> placement_devices(const DeploymentPlan& plan, const StageId& stage, int default_dev) {
+  auto it = plan.placement.find(stage);
+  if (it == plan.placement.end() || it->second.empty()) return {default_dev};
+  std::vector<int> devs;
+  size_t at = 0;
+  const std::string& v = it->second;
+  while (at <= v.size()) {
+    size_t end = v.find(',', at);
+    if (end == std::string::npos) end = v.size();
+    std::string tok = v.substr(at, end - at);
+    while (!tok.empty() && tok.front() == ' ') tok.erase(tok.begin());
+    while (!tok.empty() && tok.back() == ' ') tok.pop_back();
+    if (tok.rfind("cuda:", 0) == 0) tok = tok.substr(5);
+    if (tok.empty() || tok.find_first_not_of("0123456789") != std::string::npos)
+      throw ConfigInvalid("placement." + stage + ": expected \"cuda:N[,cuda:M...]\", got \"" + v + "\"");
+    devs.push_back(std::stoi(tok));
+    at = end + 1;
+  }
+  return devs;
+}
+
 namespace {
 std::unique_ptr<Clock> clock_for(const std::string& kind) {
   if (kind == "virtual") return std::make_unique<VirtualClock>();
@@ -91,19 +112,22 @@ void Orchestrator::start() {
   }
   for (const auto& n : plan_.graph.nodes) {
     const EngineConfig& cfg = plan_.engines.at(n.id);
+    const size_t R = placement_devices(plan_, n.id).size();
     try {
-      if (n.kind == StageKind::AR) {
-        PreprocessFn pre = n.preprocess_ref.empty() ? nullptr : registry_->preprocess(n.preprocess_ref);
-        const StageModel& m = registry_->forward(n.forward_ref);
-        models_[n.id] = m;
-        ar_[n.id] = std::make_unique<ArEngine>(n.id, cfg, m, pre, &metrics_);
-      } else {
-        const std::string den = n.forward_ref.empty() ? "denoise" : n.forward_ref;
-        auto eng = std::make_unique<DiffusionEngine>(n.id, cfg, registry_->denoiser(den), &metrics_);
-        eng->set_output_sink([this, id = n.id](const DiffusionOutput& o, uint64_t now) {
-          on_diffusion_output(id, o, now);
-        });
-        diff_[n.id] = std::move(eng);
+      for (size_t r = 0; r < R; ++r) {
+        if (n.kind == StageKind::AR) {
+          PreprocessFn pre = n.preprocess_ref.empty() ? nullptr : registry_->preprocess(n.preprocess_ref);
+          const StageModel& m = registry_->forward_for(n.forward_ref, r);
+          models_.push_back(m);
+          ar_[n.id].push_back(std::make_unique<ArEngine>(n.id, cfg, m, pre, &metrics_));
+        } else {
+          const std::string den = n.forward_ref.empty() ? "denoise" : n.forward_ref;
+          auto eng = std::make_unique<DiffusionEngine>(n.id, cfg, registry_->denoiser_for(den, r), &metrics_);
+          eng->set_output_sink([this, id = n.id](const DiffusionOutput& o, uint64_t now) {
+            on_diffusion_output(id, o, now);
+          });
+          diff_[n.id].push_back(std::move(eng));
+        }
       }
     } catch (const ConfigInvalid&) {
       throw;
@@ -196,12 +220,16 @@ ShutdownReport Orchestrator::shutdown(bool drain) {
   }
   stop_loop();
   // let in-flight device work of every engine settle before tearing down
-  for (auto& [_, e] : ar_)
-    if (e->computing()) e->complete_iteration(clock_->now_us());
-  for (auto& [_, e] : diff_)
-    if (e->computing()) e->complete_iteration(clock_->now_us());
-  for (auto& [_, e] : ar_) e->abort_all();
-  for (auto& [_, e] : diff_) e->abort_all();
+  for (auto& [_, v] : ar_)
+    for (auto& e : v)
+      if (e->computing()) e->complete_iteration(clock_->now_us());
+  for (auto& [_, v] : diff_)
+    for (auto& e : v)
+      if (e->computing()) e->complete_iteration(clock_->now_us());
+  for (auto& [_, v] : ar_)
+    for (auto& e : v) e->abort_all();
+  for (auto& [_, v] : diff_)
+    for (auto& e : v) e->abort_all();
   ar_.clear();
   diff_.clear();
   connectors_.clear();
@@ -210,14 +238,37 @@ ShutdownReport Orchestrator::shutdown(bool drain) {
   return rep;
 }
 
+std::vector<uint64_t> Orchestrator::replica_iterations(const StageId& s) const {
+  std::vector<uint64_t> v;
+  if (auto it = ar_.find(s); it != ar_.end())
+    for (const auto& e : it->second) v.push_back(e->iterations());
+  if (auto it = diff_.find(s); it != diff_.end())
+    for (const auto& e : it->second) v.push_back(e->iterations());
+  return v;
+}
 uint64_t Orchestrator::iterations(const StageId& s) const {
-  if (auto it = ar_.find(s); it != ar_.end()) return it->second->iterations();
-  if (auto it = diff_.find(s); it != diff_.end()) return it->second->iterations();
-  return 0;
+  uint64_t n = 0;
+  for (uint64_t x : replica_iterations(s)) n += x;
+  return n;
 }
 uint64_t Orchestrator::preemptions(const StageId& s) const {
-  auto it = ar_.find(s);
-  return it == ar_.end() ? 0 : it->second->preemptions();
+  uint64_t n = 0;
+  if (auto it = ar_.find(s); it != ar_.end())
+    for (const auto& e : it->second) n += e->preemptions();
+  return n;
+}
+size_t Orchestrator::replicas(const StageId& s) const {
+  if (auto it = ar_.find(s); it != ar_.end()) return it->second.size();
+  if (auto it = diff_.find(s); it != diff_.end()) return it->second.size();
+  return 0;
+}
+ArEngine& Orchestrator::ar_for(const StageId& id, uint64_t rid) {
+  auto& v = ar_.at(id);
+  return *v[replica_for(rid, v.size())];
+}
+DiffusionEngine& Orchestrator::diff_for(const StageId& id, uint64_t rid) {
+  auto& v = diff_.at(id);
+  return *v[replica_for(rid, v.size())];
 }
 
 void Orchestrator::loop() {
@@ -245,12 +296,13 @@ void Orchestrator::stop_loop() {
 }
 
 // ---- event loop -------------------------------------------------------------------
-void Orchestrator::complete_engine(const StageId& id, bool diffusion, uint64_t t) {
+void Orchestrator::complete_engine(const StageId& id, size_t replica, bool diffusion, uint64_t t) {
   if (diffusion) {
-    diff_[id]->complete_iteration(t);
+    diff_[id][replica]->complete_iteration(t);
   } else {
-    StepReport rep = ar_[id]->complete_iteration(t);
-    handle_ar_report(id, rep, t);
+    ArEngine& eng = *ar_[id][replica];
+    StepReport rep = eng.complete_iteration(t);
+    handle_ar_report(id, eng, rep, t);
   }
   pump_diffusion_inflows();
 }
@@ -261,10 +313,12 @@ bool Orchestrator::tick() {
   pump_diffusion_inflows();
 
   for (const auto& id : topo_) {
-    if (auto a = ar_.find(id); a != ar_.end() && !a->second->computing() && a->second->has_work())
-      a->second->begin_iteration(now);
-    if (auto d = diff_.find(id); d != diff_.end() && !d->second->computing() && d->second->has_work())
-      d->second->begin_iteration(now);
+    if (auto a = ar_.find(id); a != ar_.end())
+      for (auto& e : a->second)
+        if (!e->computing() && e->has_work()) e->begin_iteration(now);
+    if (auto d = diff_.find(id); d != diff_.end())
+      for (auto& e : d->second)
+        if (!e->computing() && e->has_work()) e->begin_iteration(now);
   }
 
   uint64_t next_arrival = kTimeUnset;
@@ -286,26 +340,29 @@ bool Orchestrator::tick() {
     }();
     bool busy = false;
     for (const auto& id : topo_) {
-      if (auto a = ar_.find(id); a != ar_.end() && a->second->computing()) {
-        busy = true;
-        if (a->second->ready()) {
-          complete_engine(id, false, clock_->now_us());
-          if (eager && !a->second->computing() && a->second->has_work()) {
+      if (auto a = ar_.find(id); a != ar_.end())
+        for (size_t r = 0; r < a->second.size(); ++r) {
+          ArEngine& e = *a->second[r];
+          if (!e.computing()) continue;
+          busy = true;
+          if (!e.ready()) continue;
+          complete_engine(id, r, false, clock_->now_us());
+          if (eager && !e.computing() && e.has_work()) {
             pump_diffusion_inflows();
-            a->second->begin_iteration(clock_->now_us());
+            e.begin_iteration(clock_->now_us());
           }
           return true;
         }
-      }
-      if (auto d = diff_.find(id); d != diff_.end() && d->second->computing()) {
-        busy = true;
-        if (d->second->ready()) {
-          complete_engine(id, true, clock_->now_us());
-          if (eager && !d->second->computing() && d->second->has_work())
-            d->second->begin_iteration(clock_->now_us());
+      if (auto d = diff_.find(id); d != diff_.end())
+        for (size_t r = 0; r < d->second.size(); ++r) {
+          DiffusionEngine& e = *d->second[r];
+          if (!e.computing()) continue;
+          busy = true;
+          if (!e.ready()) continue;
+          complete_engine(id, r, true, clock_->now_us());
+          if (eager && !e.computing() && e.has_work()) e.begin_iteration(clock_->now_us());
           return true;
         }
-      }
     }
     if (busy) {
       std::this_thread::yield();
@@ -321,18 +378,25 @@ bool Orchestrator::tick() {
 
   uint64_t best = kTimeUnset;
   StageId best_stage;
+  size_t best_rep = 0;
   bool best_diff = false;
   for (const auto& id : topo_) {
-    if (auto a = ar_.find(id); a != ar_.end() && a->second->computing() && a->second->end_time() < best) {
-      best = a->second->end_time();
-      best_stage = id;
-      best_diff = false;
-    }
-    if (auto d = diff_.find(id); d != diff_.end() && d->second->computing() && d->second->end_time() < best) {
-      best = d->second->end_time();
-      best_stage = id;
-      best_diff = true;
-    }
+    if (auto a = ar_.find(id); a != ar_.end())
+      for (size_t r = 0; r < a->second.size(); ++r)
+        if (a->second[r]->computing() && a->second[r]->end_time() < best) {
+          best = a->second[r]->end_time();
+          best_stage = id;
+          best_rep = r;
+          best_diff = false;
+        }
+    if (auto d = diff_.find(id); d != diff_.end())
+      for (size_t r = 0; r < d->second.size(); ++r)
+        if (d->second[r]->computing() && d->second[r]->end_time() < best) {
+          best = d->second[r]->end_time();
+          best_stage = id;
+          best_rep = r;
+          best_diff = true;
+        }
   }
   if (next_arrival < best) {
     clock_->advance_to_us(next_arrival);
@@ -341,7 +405,7 @@ bool Orchestrator::tick() {
   }
   if (best == kTimeUnset) return false;
   clock_->advance_to_us(best);
-  complete_engine(best_stage, best_diff, clock_->now_us());
+  complete_engine(best_stage, best_rep, best_diff, clock_->now_us());
   return true;
 }
 
@@ -412,7 +476,7 @@ void Orchestrator::admit_request(Pending s, uint64_t now) {
     adm.sub.seed = f->req.seed;
     adm.ctx = f->ctx;
     adm.emits = std::move(f->stage_plans[plan_.graph.entry]);
-    ar_.at(plan_.graph.entry)->admit(std::move(adm));
+    ar_for(plan_.graph.entry, rid).admit(std::move(adm));
   } catch (const OmniError& e) {
     fail_request(rid, plan_.graph.entry, e.what());
   }
@@ -434,7 +498,7 @@ void Orchestrator::apply_transfer(InFlight& f, const TransferEdge& e, std::optio
       f.pending_receivers.erase(pr);
     }
     adm.emits = std::move(f.stage_plans[e.to]);
-    ar_.at(e.to)->admit(std::move(adm));
+    ar_for(e.to, rid).admit(std::move(adm));
   };
   env.wire_diffusion = [this, &f, &e, rid](DiffusionWiring w) {
     f.diff_wirings.push_back({w, e.to, e.key(), false, 0});
@@ -473,7 +537,7 @@ void Orchestrator::pump_diffusion_inflows() {
           job.eos = c->eos;
           job.token_offset = w.tokens_seen;
           w.tokens_seen += static_cast<uint32_t>(job.input.element_count() * (job.input.shape.empty() ? 0 : 1));
-          diff_.at(w.to_stage)->submit(std::move(job));
+          diff_for(w.to_stage, rid).submit(std::move(job));
           if (c->eos) {
             w.eos_seen = true;
             break;
@@ -486,11 +550,10 @@ void Orchestrator::pump_diffusion_inflows() {
   }
 }
 
-void Orchestrator::handle_ar_report(const StageId& stage, const StepReport& rep, uint64_t now) {
+void Orchestrator::handle_ar_report(const StageId& stage, ArEngine& eng, const StepReport& rep, uint64_t now) {
   for (const auto& [rid, why] : rep.failed) fail_request(rid, stage, why);
   for (uint64_t rid : rep.finished) {
     InFlight* f = find_inflight(rid);
-    ArEngine& eng = *ar_.at(stage);
     if (!f) {
       eng.drop_finished(rid);
       continue;
@@ -628,7 +691,7 @@ void Orchestrator::fail_all_locked(const std::string& why) {
 
 void Orchestrator::cleanup_request(uint64_t rid) {
   for (auto& [_, c] : connectors_) c->cleanup(rid);
-  for (auto& [_, m] : models_)
+  for (auto& m : models_)
     if (m.cleanup) m.cleanup(rid);
 }
 

@@ -15,7 +15,8 @@ class BenchSpec(C.Structure):
     _fields_ = [("n", C.c_uint64), ("seed", C.c_uint64), ("concurrency", C.c_uint64),
                 ("stream", C.c_int32), ("poisson", C.c_int32), ("rate", C.c_double),
                 ("prompt_min", C.c_uint32), ("prompt_max", C.c_uint32), ("clock", C.c_char_p),
-                ("trace", C.c_int32), ("talker_chunk", C.c_int32), ("vocoder_chunk", C.c_int32)]
+                ("trace", C.c_int32), ("talker_chunk", C.c_int32), ("vocoder_chunk", C.c_int32),
+                ("capture", C.c_int32)]
 
 
 class BenchResult(C.Structure):
@@ -56,12 +57,25 @@ class Pipeline:
             pass
 
     def bench(self, n=100, seed=7, concurrency=16, stream=True, clock="device", trace=False,
-              poisson=False, rate=1.0, talker_chunk=0, vocoder_chunk=0) -> dict:
+              poisson=False, rate=1.0, talker_chunk=0, vocoder_chunk=0, capture=False) -> dict:
         spec = BenchSpec(n, seed, concurrency, 1 if stream else 0, 1 if poisson else 0, rate, 0, 0,
-                         clock.encode(), 1 if trace else 0, talker_chunk, vocoder_chunk)
+                         clock.encode(), 1 if trace else 0, talker_chunk, vocoder_chunk, 1 if capture else 0)
         res = BenchResult()
         check(self.lib.omni_pipeline_bench(self.h, C.byref(spec), C.byref(res)), self.lib)
         return res.as_dict()
+
+    def output(self, request_id: int, what: int):
+        """Per-request output of the last bench(capture=True) run (OMNI_OUT_*)."""
+        import numpy as np
+        f = self.lib.omni_pipeline_output
+        f.restype = C.c_size_t
+        f.argtypes = [C.c_void_p, C.c_uint64, C.c_int32, C.c_void_p, C.c_size_t]
+        n = f(self.h, request_id, what, None, 0)
+        dt = {0: np.uint8, 1: np.int32, 2: np.int32, 3: np.int32, 4: np.uint16}[what]
+        out = np.empty(n // np.dtype(dt).itemsize, dtype=dt)
+        if n:
+            f(self.h, request_id, what, out.ctypes.data, n)
+        return out
 
     def text(self, what: int) -> str:
         self.lib.omni_pipeline_text.restype = C.c_size_t

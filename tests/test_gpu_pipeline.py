@@ -39,20 +39,47 @@ def keyed(trace: str):
 
 
 @pytest.fixture(scope="module")
-def small_omni3():
-    p = Pipeline((ROOT / "configs" / "omni3.json").read_text(), weight_seed=99, small_models=True)
-    yield p
-    p.close()
+def pipelines():
+    """One small-model pipeline per config file, shared by the trace cases."""
+    cache = {}
+
+    def get(cfg):
+        if cfg not in cache:
+            cache[cfg] = Pipeline((ROOT / "configs" / cfg).read_text(), weight_seed=99, small_models=True)
+        return cache[cfg]
+
+    yield get
+    for p in cache.values():
+        p.close()
 
 
-@pytest.mark.parametrize("case", [("omni3_chunk1", 30, 3, 16, 1, 1, 1), ("omni3_full", 40, 11, 64, 0, 0, 0)],
-                         ids=lambda c: c[0])
-def test_virtual_clock_trace_matches_reference(small_omni3, case):
-    name, n, seed, conc, stream, c0, c1 = case
-    r = small_omni3.bench(n=n, seed=seed, concurrency=conc, stream=bool(stream), clock="virtual", trace=True,
-                          talker_chunk=c0, vocoder_chunk=c1)
+@pytest.fixture(scope="module")
+def small_omni3(pipelines):
+    return pipelines("omni3.json")
+
+
+def trace_cases():
+    out = []
+    for line in (GOLD / "traces.index").read_text().splitlines():
+        f = line.split()
+        if f:
+            out.append((f[0], f[1], int(f[2]), int(f[3]), int(f[4]), int(f[5]),
+                        int(f[6]) if len(f) > 6 else 0, int(f[7]) if len(f) > 7 else 0))
+    return out
+
+
+@pytest.mark.parametrize("case", trace_cases(), ids=lambda c: c[0])
+def test_virtual_clock_trace_matches_reference(pipelines, case):
+    """Every golden trace of the unmodified reference (8 configs: the bench's
+    n=100 run, concurrency 64, FULL edges, chunk 1, tight KV budgets with
+    recompute preemption, single-stage, two-stage and AR->DiT graphs) replayed
+    with the B200 device models in the loop on the virtual clock."""
+    name, cfg, n, seed, conc, stream, c0, c1 = case
+    p = pipelines(cfg)
+    r = p.bench(n=n, seed=seed, concurrency=conc, stream=bool(stream), clock="virtual", trace=True,
+                talker_chunk=c0, vocoder_chunk=c1)
     assert r["completed"] == n and r["failed"] == 0
-    got = keyed(small_omni3.trace())
+    got = keyed(p.trace())
     want = keyed(gzip.decompress((GOLD / f"trace_{name}.txt.gz").read_bytes()).decode())
     assert set(got) == set(want)
     for k in want:
