@@ -129,17 +129,19 @@ typedef struct omni_ar_batch {
  * omni_stage_query. PREFILL entries emit nothing (ar_engine.hpp:313-324). */
 omni_status omni_ar_step(omni_stage* st, const omni_ar_batch* batch, int32_t* token_out,
                          float* margin_out);
-/* Execution mode of small Thinker steps (<= 16 token rows): 1 runs the whole
- * step as ONE "step chain" launch (cluster-ticketed work items with
- * device-side dependency counters), 0 (default) as the per-kernel PDL chain.
- * Results are bit-identical; the switch exists for A/B measurement. */
-omni_status omni_stage_set_chain(omni_stage* st, int32_t on);
+/* Sampling of DECODE rows: top_k <= 1 = greedy argmax (default; the
+ * reference's token_of is greedy, reference_pipeline.hpp:34), 2..32 = top-k
+ * sampling at temperature 1 with a draw keyed by (seed, request id, emitted
+ * index) -- deterministic and batch-invariant, so recompute preemption
+ * (ar_engine.hpp:229-257) replays the same tokens. The margin output stays
+ * the top-2 logit margin. */
+omni_status omni_stage_set_sampling(omni_stage* st, int32_t top_k, uint64_t seed);
 
-/* Tools: record {start, dependency met, end} globaltimer ns per work item of
- * subsequent step-chain launches into trace_dev (3 x u64 per item; 0 = off);
- * returns the item / op counts and op start tickets of the LAST chain launch. */
-omni_status omni_stage_chain_trace(omni_stage* st, uint64_t trace_dev, int32_t* n_items, int32_t* n_ops,
-                                   int32_t* op_first);
+/* Admits a sequence's KV pages for positions [0, upto_tokens) ahead of a
+ * step, so a sequence that does not fit fails alone (OMNI_E_OOM) instead of
+ * failing the whole batched step (the reference fails per entry,
+ * ar_engine.hpp:332-334). omni_ar_step reserves implicitly. */
+omni_status omni_seq_reserve(omni_stage* st, uint64_t seq_id, int32_t upto_tokens);
 
 /* Frees the KV pages / hidden ring / conditioning rows of a sequence
  * (finish, recompute-preemption ar_engine.hpp:233-257, or failure). */
@@ -191,12 +193,20 @@ uint64_t omni_pack_bytes(int32_t rows, int32_t d);
 
 /* Packs rows [begin[c], end[c]) of seq_id[c]'s hidden ring, with token ids
  * tokens[sum of previous row counts ...], into dst_base + dst_offset[c] for
- * every chunk c, in one launch on the source stage's stream. */
+ * every chunk c, in one launch on the source stage's stream. Destinations may
+ * lie on a peer GPU (remote stores over NVLink; omni_init enables peer
+ * access) and may differ per chunk (dst_base = 0, absolute dst_offset). */
 omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* seq_id,
                              const int32_t* begin, const int32_t* end, const int32_t* tokens,
                              uint64_t dst_base, const uint64_t* dst_offset);
 /* Make `dst`'s next step wait (on-device) for everything `src` enqueued so far. */
 omni_status omni_stage_after(omni_stage* dst, omni_stage* src);
+/* Make `dst`'s next step wait (on-device, across GPUs) for `src`'s most recent
+ * omni_pack_hidden only -- not for steps `src` enqueued after the pack. This
+ * is the connector's consumer-side ordering: the Talker reads rows the
+ * Thinker packed into its arena without serialising behind the Thinker's next
+ * step. No-op before the first pack. */
+omni_status omni_stage_after_pack(omni_stage* dst, omni_stage* src);
 
 /* Plumbing for tests / bench (no compute): device memory and copies. */
 omni_status omni_mem_alloc(int32_t dev, uint64_t bytes, uint64_t* dev_ptr);

@@ -221,6 +221,15 @@ long oracle_mock_trace(const char* config_json, uint64_t n, uint64_t seed, uint6
     register_mock(reg);
     for (const char* f : {"thinker_forward", "talker_forward", "ar_forward"})
       reg.register_forward(f, tr.wrap(f, base.forward(f)));
+    // replicated AR stages: one traced model per replica ("name#r" in the
+    // trace lines) so tests can see which replica served which request
+    for (const auto& nd : plan.graph.nodes) {
+      const size_t R = placement_devices(plan, nd.id).size();
+      if (nd.kind != StageKind::AR || R < 2) continue;
+      for (size_t r = 1; r < R; ++r)
+        reg.register_forward(replica_name(nd.forward_ref, r),
+                             tr.wrap(replica_name(nd.forward_ref, r), base.forward(nd.forward_ref)));
+    }
     Orchestrator orch(plan, &reg);
     tr.clock = &orch.clock();
     orch.start();
@@ -248,6 +257,14 @@ long oracle_mock_trace(const char* config_json, uint64_t n, uint64_t seed, uint6
       for (const auto& [st, t] : m.stages)
         rs << " " << st << ":" << (long long)t.first_scheduled_at << ":" << (long long)t.first_token_at << ":"
            << (long long)t.finished_at << ":" << t.tokens;
+      rs << "\n";
+    }
+    // replicated stages (placement lists several devices): iterations per replica
+    for (const auto& nd : plan.graph.nodes) {
+      const auto it = orch.replica_iterations(nd.id);
+      if (it.size() < 2) continue;
+      rs << "I " << nd.id;
+      for (uint64_t x : it) rs << " " << x;
       rs << "\n";
     }
     orch.shutdown(true);

@@ -164,6 +164,20 @@ def codec_token(t: int, hsum: int, i: int) -> int:  # reference_pipeline.hpp:43-
     return (t * 7 + hsum + i) % 64
 
 
+M64 = 0xFFFFFFFFFFFFFFFF
+
+
+def mix64(x: int) -> int:  # csrc/dev/rng.h mix64 (splitmix64 finaliser)
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+def sample_hash(seed: int, key: int, index: int) -> int:  # csrc/dev/rng.h sample_hash
+    return mix64(seed ^ mix64(((key << 32) ^ index ^ 0x73616D706C650000) & M64))
+
+
 def denoise_closed_form(codec, S=16):  # diffusion_engine.hpp:28-43
     out = []
     for c in codec:

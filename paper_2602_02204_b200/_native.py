@@ -49,5 +49,11 @@ def serve_lib() -> C.CDLL:
 def check(status: int, lib: C.CDLL | None = None) -> None:
     if status != 0:
         lib = lib or dev_lib()
-        getter = getattr(lib, "omni_last_error", None) or getattr(lib, "omni_serve_last_error")
+        # the serve library re-exports libomni_dev's symbols (dlsym searches
+        # its dependencies), so pick its own error getter first
+        if hasattr(lib, "omni_serve_last_error"):
+            getter = lib.omni_serve_last_error
+        else:
+            getter = lib.omni_last_error
+        getter.restype = C.c_char_p
         raise OmniError(status, (getter() or b"").decode())

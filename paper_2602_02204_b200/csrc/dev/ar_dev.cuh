@@ -9,6 +9,7 @@
 
 #include "ar_kernels.h"
 #include "ptx.cuh"
+#include "rng.h"
 
 namespace omni_dev {
 
@@ -170,7 +171,7 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
     for (int i = 0; i < np; ++i) {
       const bool history = (first + i + 1) * kPageTokens <= ed.pos0;
       if (history != (part == 0)) continue;
-      const int page = s.page_table[blk.entry * s.max_pages + first + i];
+      const int page = s.page_table[ed.slot * s.max_pages + first + i];
       const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
       bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
       bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
@@ -383,7 +384,7 @@ __device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const A
     for (int i = 0; i < np; ++i) {
       const bool history = (first + i + 1) * kPageTokens <= ed.pos0;
       if (history != (part == 0)) continue;
-      const int page = s.page_table[blk.entry * s.max_pages + first + i];
+      const int page = s.page_table[ed.slot * s.max_pages + first + i];
       const size_t base = (((size_t)page * n_layers + layer) * 2) * n_kv;
       bulk_load(sm.k[buf] + i * kPageTokens * HD, kv + (base + kh) * kPageTokens * HD, PAGE_BYTES, &sm.bar[buf]);
       bulk_load(sm.v[buf] + i * kPageTokens * HD, kv + (base + n_kv + kh) * kPageTokens * HD, PAGE_BYTES,
@@ -650,108 +651,78 @@ __device__ __forceinline__ void argmax_row(int r, const float* __restrict__ logi
 }
 
 // ---------------------------------------------------------------------------
-// Fused step head for small vocabularies (V <= 256): final RMSNorm of one
-// DECODE row -> bf16 hidden row (+ Thinker hidden ring), LM-head dot
-// products on the CUDA cores (one warp per output id, 16-byte loads of the
-// L2-resident head weights), greedy id + top-2 margin. Replaces
-// final_gather + LM-head GEMM + argmax (two kernel boundaries less on the
-// per-token critical path). A row's ids [v0, v1) may be split over `parts`
-// CTAs: each recomputes the (cheap) norm, the last one to finish (ticket in
-// cnt[di], reset for the next replay) runs the argmax over the row in global
-// memory. Hidden rows are bit-identical to final_gather_row; each logit is
-// one warp's fixed-order dot product, so the split does not change it.
-// smem: hs[d] floats (+ red[32]).
-// ---------------------------------------------------------------------------
+// Top-k sampler (north star: "warp-shuffle argmax/top-k sampler"). One warp
+// per decode row; the row's logits live in registers (<= 8 per lane, V <=
+// 256). top_k <= 1 is the greedy argmax above (the reference's token_of is
+// greedy, reference_pipeline.hpp:34). Otherwise the k largest logits are
+// extracted by k warp-argmax rounds, softmax-weighted (temperature 1), and
+// one is drawn with u = sample_hash(seed, request key, emitted index): a pure
+// function of the request and position, so a recompute-preempted sequence
+// (ar_engine.hpp:229-257) redraws the same token and sampling stays
+// batch-invariant. Ties break to the lowest id; the top-2 margin is reported
+// as in the greedy path.
+constexpr int kSampleMaxK = 32;
+constexpr int kSamplePerLane = 8;  // V <= 256
 
 template <class Dep>
-__device__ __forceinline__ void head_row(int di, int v0, int v1, int parts, int* __restrict__ cnt,
-                                         const ArStepDev& s, const float* __restrict__ x, int d, float eps,
-                                         __nv_bfloat16* __restrict__ hout, __nv_bfloat16* __restrict__ ring,
-                                         int ring_rows, const __nv_bfloat16* __restrict__ lm,
-                                         float* __restrict__ logits, int ld, int lo, int hi,
-                                         int* __restrict__ tok_out, float* __restrict__ margin_out, float* hs,
-                                         float* red, Dep dep) {
+__device__ __forceinline__ void sample_row(int r, const ArStepDev& s, const float* __restrict__ logits, int ld,
+                                           int lo, int hi, int top_k, uint64_t seed,
+                                           int* __restrict__ tok_out, float* __restrict__ margin_out, Dep dep) {
+  if (top_k <= 1) {
+    argmax_row(r, logits, ld, lo, hi, tok_out, margin_out, dep);
+    return;
+  }
   dep();
-  const int e = s.dec_entries[di];
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const float* row = logits + (size_t)r * ld;
+  float v[kSamplePerLane];
+#pragma unroll
+  for (int j = 0; j < kSamplePerLane; ++j) {
+    const int i = lo + lane + 32 * j;
+    v[j] = i < hi ? row[i] : -INFINITY;
+  }
+  const int k = min(min(top_k, kSampleMaxK), hi - lo);
+  float top_v = -INFINITY;  // lane t keeps the t-th largest (t < k)
+  int top_i = 0x7fffffff;
+  for (int t = 0; t < k; ++t) {
+    float b = -INFINITY;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < kSamplePerLane; ++j) {
+      const int i = lo + lane + 32 * j;
+      if (v[j] > b || (v[j] == b && i < bi)) b = v[j], bi = i;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > b || (ob == b && oi < bi)) b = ob, bi = oi;
+    }
+    if (lane == t) top_v = b, top_i = bi;
+#pragma unroll
+    for (int j = 0; j < kSamplePerLane; ++j)
+      if (lo + lane + 32 * j == bi) v[j] = -INFINITY;
+  }
+  const float vmax = __shfl_sync(0xffffffffu, top_v, 0);
+  const float p = lane < k ? __expf(top_v - vmax) : 0.f;
+  // inclusive prefix sum in lane order (= descending logit order)
+  float c = p;
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, c, o);
+    if (lane >= o) c += y;
+  }
+  const float total = __shfl_sync(0xffffffffu, c, 31);
+  const int e = s.dec_entries[r];
   const ArEntryDesc ed = s.entries[e];
-  const float* xr = x + (size_t)ed.row0 * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) ss += xr[i] * xr[i];
-  const float tot = block_sum(ss, red);
-  const float inv = rsqrtf(tot / d + eps);
-  __nv_bfloat16* h = hout + (size_t)di * d;
-  __nv_bfloat16* rg = (ring && v0 == 0) ? ring + ((size_t)ed.slot * ring_rows + ed.out_index) * d : nullptr;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const __nv_bfloat16 v = f2bf(xr[i] * inv);
-    if (v0 == 0) h[i] = v;
-    if (rg) rg[i] = v;
-    hs[i] = bf2f(v);
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  float* lrow = logits + (size_t)di * ld;
-  for (int v = v0 + warp; v < v1; v += nw) {
-    const __nv_bfloat16* wr = lm + (size_t)v * d;
-    float acc = 0.f;
-#pragma unroll 4
-    for (int i0 = lane * 8; i0 < d; i0 += 32 * 8) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(wr + i0);
-      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-      const float4 ha = *reinterpret_cast<const float4*>(hs + i0);
-      const float4 hb = *reinterpret_cast<const float4*>(hs + i0 + 4);
-      const float2 f0 = __bfloat1622float2(w2[0]), f1 = __bfloat1622float2(w2[1]);
-      const float2 f2 = __bfloat1622float2(w2[2]), f3 = __bfloat1622float2(w2[3]);
-      acc += f0.x * ha.x + f0.y * ha.y;
-      acc += f1.x * ha.z + f1.y * ha.w;
-      acc += f2.x * hb.x + f2.y * hb.y;
-      acc += f3.x * hb.z + f3.y * hb.w;
-    }
-    acc = warp_sum(acc);
-    if (lane == 0) lrow[v] = acc;
-  }
-  if (parts > 1) {
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const int t = atomicAdd(cnt + di, 1);
-      s_last = (t == parts - 1);
-      if (s_last) cnt[di] = 0;
-      __threadfence();
-    }
-    __syncthreads();
-    if (!s_last) return;
-  } else {
-    __syncthreads();
-  }
-  if (warp != 0) return;
-  float b1 = -INFINITY, b2 = -INFINITY;
-  int i1 = 0x7fffffff;
-  for (int i = lo + lane; i < hi; i += 32) {
-    const float v = __ldcg(lrow + i);
-    if (v > b1 || (v == b1 && i < i1)) {
-      b2 = b1;
-      b1 = v;
-      i1 = i;
-    } else if (v > b2) {
-      b2 = v;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
-    const float ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
-    const int oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
-    if (ob1 > b1 || (ob1 == b1 && oi1 < i1)) {
-      b2 = fmaxf(b1, ob2);
-      b1 = ob1;
-      i1 = oi1;
-    } else {
-      b2 = fmaxf(b2, ob1);
-    }
-  }
+  const uint64_t h = sample_hash(seed, (uint32_t)ed.key, (uint32_t)ed.out_index);
+  const float u = (float)(h >> 40) * (1.0f / 16777216.0f) * total;
+  const unsigned hit = __ballot_sync(0xffffffffu, lane < k && c > u);
+  const int pick = hit ? __ffs(hit) - 1 : k - 1;
+  const int tok = __shfl_sync(0xffffffffu, top_i, pick);
+  const float m2 = __shfl_sync(0xffffffffu, top_v, 1);
   if (lane == 0) {
-    tok_out[di] = i1;
-    margin_out[di] = b1 - b2;
+    tok_out[r] = tok;
+    margin_out[r] = vmax - m2;
   }
 }
 

@@ -36,17 +36,27 @@ __global__ void embed_kernel(const ArStepDev s, const __nv_bfloat16* __restrict_
 
 // Step descriptor blob pinned host -> device by the step's first kernel
 // (UVA load of the pinned staging buffer) instead of a copy-engine H2D.
-__global__ void desc_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int n16) {
-  pdl_wait();  // the previous step's kernels may still read the blob
+__global__ void desc_copy_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int n16,
+                                 const PageDeltaHeader* __restrict__ dsrc, int32_t* __restrict__ pt) {
+  pdl_wait();  // the previous step's kernels may still read the blob / page table
   pdl_trigger();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) dst[i] = src[i];
+  if (dsrc && pt) {
+    const int n = dsrc->n;
+    const PageDelta* dl = reinterpret_cast<const PageDelta*>(dsrc + 1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+      const PageDelta dd = dl[i];
+      pt[dd.index] = dd.page;
+    }
+  }
 }
 
-cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, const void* delta_src, int32_t* page_table,
+                             cudaStream_t st) {
   const int n16 = (int)((bytes + 15) / 16);
-  const int blocks = std::min(16, (n16 + 255) / 256);
+  const int blocks = std::max(1, std::min(16, (n16 + 255) / 256));
   return launch_k(desc_copy_kernel, dim3(blocks), dim3(256), 0, st, 1, static_cast<uint4*>(dst),
-                  static_cast<const uint4*>(src), n16);
+                  static_cast<const uint4*>(src), n16, static_cast<const PageDeltaHeader*>(delta_src), page_table);
 }
 
 __global__ void gather_cond_kernel(const ArStepDev s, int d, __nv_bfloat16* __restrict__ out) {
@@ -90,22 +100,9 @@ __global__ void final_gather_kernel(const ArStepDev s, const float* __restrict__
   final_gather_row(blockIdx.x, s, x, d, eps, hout, ring, ring_rows, red, PdlDep{});
 }
 
-__global__ void __launch_bounds__(256)
-    head_kernel(const ArStepDev s, const float* __restrict__ x, int d, float eps, __nv_bfloat16* __restrict__ hout,
-                __nv_bfloat16* __restrict__ ring, int ring_rows, const __nv_bfloat16* __restrict__ lm, int vocab,
-                float* __restrict__ logits, int ld, int lo, int hi, int* __restrict__ tok_out,
-                float* __restrict__ margin_out, int* __restrict__ cnt) {
-  extern __shared__ float head_smem[];  // hs[d]
-  __shared__ float red[32];
-  const int per = (vocab + gridDim.x - 1) / gridDim.x;
-  const int v0 = blockIdx.x * per;
-  head_row(blockIdx.y, v0, min(vocab, v0 + per), gridDim.x, cnt, s, x, d, eps, hout, ring, ring_rows, lm, logits,
-           ld, lo, hi, tok_out, margin_out, head_smem, red, PdlDep{});
-}
-
-__global__ void argmax_kernel(const float* __restrict__ logits, int ld, int lo, int hi,
-                              int* __restrict__ tok_out, float* __restrict__ margin_out) {
-  argmax_row(blockIdx.x, logits, ld, lo, hi, tok_out, margin_out, PdlDep{});
+__global__ void sample_kernel(const ArStepDev s, const float* __restrict__ logits, int ld, int lo, int hi,
+                              int top_k, uint64_t seed, int* __restrict__ tok_out, float* __restrict__ margin_out) {
+  sample_row(blockIdx.x, s, logits, ld, lo, hi, top_k, seed, tok_out, margin_out, PdlDep{});
 }
 
 // ---------------------------------------------------------------------------
@@ -141,22 +138,10 @@ cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, i
   return launch_k(final_gather_kernel, dim3(n_dec), dim3(256), 0, st, 1, s, x, d, eps, hout, ring,
                   ring_rows);
 }
-cudaError_t launch_head(const ArStepDev& s, int n_dec, const float* x, int d, float eps, __nv_bfloat16* hout,
-                        __nv_bfloat16* ring, int ring_rows, const __nv_bfloat16* lm, int vocab, float* logits,
-                        int ld, int lo, int hi, int* tok, float* margin, int* cnt, cudaStream_t st) {
-  if (vocab > kHeadMaxVocab || d % 256 != 0) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)d * sizeof(float);
-  // kHeadIdsPerCta ids per CTA (2 per warp): the LM head streams from L2 over many SMs
-  const int parts = (vocab + kHeadIdsPerCta - 1) / kHeadIdsPerCta;
-  static std::atomic<uint64_t> configured{0};
-  if (smem > 48 * 1024)
-    if (cudaError_t e = smem_attr_once(head_kernel, smem, configured); e != cudaSuccess) return e;
-  return launch_k(head_kernel, dim3(parts, n_dec), dim3(256), smem, st, 1, s, x, d, eps, hout, ring, ring_rows, lm,
-                  vocab, logits, ld, lo, hi, tok, margin, cnt);
-}
-cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
-                          cudaStream_t st) {
-  return launch_k(argmax_kernel, dim3(n), dim3(32), 0, st, 1, logits, ld, lo, hi, tok, margin);
+cudaError_t launch_sample(const ArStepDev& s, const float* logits, int ld, int n, int lo, int hi, int top_k,
+                          uint64_t seed, int* tok, float* margin, cudaStream_t st) {
+  if (hi - lo > 32 * kSamplePerLane) return cudaErrorInvalidValue;
+  return launch_k(sample_kernel, dim3(n), dim3(32), 0, st, 1, s, logits, ld, lo, hi, top_k, seed, tok, margin);
 }
 
 }  // namespace omni_dev

@@ -18,7 +18,7 @@ struct ArEntryDesc {  // one IterationBatch entry (ar_engine.hpp:56-70)
   int32_t is_decode;
   int32_t out_index;  // decode: emitted index k
   int32_t dec_row;    // decode: row in the compact decode output, else -1
-  int32_t pad;
+  int32_t key;        // 32-bit hash of the request id (top-k sampler draws)
 };
 
 struct ArRowDesc {  // one token row of the step
@@ -26,6 +26,8 @@ struct ArRowDesc {  // one token row of the step
   int32_t pos;
   int32_t token;     // -1 = stage start id
   int32_t cond_row;  // talker conditioning row j
+  int32_t slot;      // resident slot of the entry's sequence (persistent page table row)
+  int32_t pad;
   uint64_t cond_src; // talker prefill: device address of the upstream hidden row
 };
 
@@ -41,7 +43,7 @@ struct AttnBlockDesc {  // one attention CTA row: tokens [tok0, tok0+ntok) of an
 struct ArStepDev {
   const ArEntryDesc* entries;
   const ArRowDesc* rows;
-  const int32_t* page_table;   // [n_entries][max_pages]
+  const int32_t* page_table;   // persistent [max_resident slots][max_pages] in HBM
   const int32_t* dec_entries;  // [n_dec] entry index of each decode row
   const AttnBlockDesc* attn_blocks;
   int32_t max_pages;
@@ -61,15 +63,23 @@ cudaError_t launch_final_gather(const ArStepDev& s, int n_dec, const float* x, i
                                 __nv_bfloat16* hout, __nv_bfloat16* ring, int ring_rows,
                                 cudaStream_t st);
 // Fused final RMSNorm + LM head (CUDA cores) + greedy argmax, vocab <= 256.
-cudaError_t attn_trace_set(void* p);
-cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);  // debug: per-CTA phase stamps of attention launches
-// Grid (vocab / kHeadIdsPerCta, n_dec); cnt = n_dec zeroed tickets (self-resetting).
-constexpr int kHeadMaxVocab = 256;
-constexpr int kHeadIdsPerCta = 16;
-cudaError_t launch_head(const ArStepDev& s, int n_dec, const float* x, int d, float eps, __nv_bfloat16* hout,
-                        __nv_bfloat16* ring, int ring_rows, const __nv_bfloat16* lm, int vocab, float* logits,
-                        int ld, int lo, int hi, int* tok, float* margin, int* cnt, cudaStream_t st);
-cudaError_t launch_argmax(const float* logits, int ld, int n, int lo, int hi, int* tok, float* margin,
-                          cudaStream_t st);
+cudaError_t attn_trace_set(void* p);  // debug: per-CTA phase stamps of attention launches
+// Page-table delta carried by a step's descriptor blob.
+struct PageDelta {
+  int32_t index;  // slot * max_pages + page ordinal
+  int32_t page;
+};
+struct PageDeltaHeader {
+  int32_t n;
+  int32_t pad[3];
+};
+constexpr int kPageDeltaCap = 1024;
+// Copies the step descriptor blob from pinned staging (UVA loads) and applies
+// the page-table delta (delta_src: header + PageDelta[n], pinned host).
+cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, const void* delta_src,
+                             int32_t* page_table, cudaStream_t st);
+// Greedy argmax (top_k <= 1) or top-k sampling of each decode row, + top-2 margin.
+cudaError_t launch_sample(const ArStepDev& s, const float* logits, int ld, int n, int lo, int hi, int top_k,
+                          uint64_t seed, int* tok, float* margin, cudaStream_t st);
 
 }  // namespace omni_dev

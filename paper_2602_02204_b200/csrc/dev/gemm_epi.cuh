@@ -124,7 +124,7 @@ __device__ __forceinline__ void epi_cols(const GemmArgs& a, int n_tile, int tok0
       } else {
         const int is_v = head >= rp.n_heads + rp.n_kv;
         const int kh = head - rp.n_heads - (is_v ? rp.n_kv : 0);
-        const int page = pre ? pre_i[16 + c] : rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens];
+        const int page = pre ? pre_i[16 + c] : rp.page_table[rd.slot * rp.max_pages + rd.pos / kPageTokens];
         const int pt = rd.pos % kPageTokens;
         dst = rp.kv +
               ((((size_t)page * rp.n_layers + rp.layer) * 2 + is_v) * rp.n_kv + kh) * kPageTokens * 128 +

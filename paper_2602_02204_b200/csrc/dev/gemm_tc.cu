@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (q < n_me) {
         const ArRowDesc rd = static_cast<const ArRowDesc*>(rp.rows)[cb0 + q];
         pre_i[q] = rd.pos;
-        pre_i[16 + q] = n_tile >= rp.n_heads ? rp.page_table[rd.entry * rp.max_pages + rd.pos / kPageTokens] : 0;
+        pre_i[16 + q] = n_tile >= rp.n_heads ? rp.page_table[rd.slot * rp.max_pages + rd.pos / kPageTokens] : 0;
       }
       asm volatile("bar.sync 1, 64;" ::: "memory");  // warps 2-3 only
       if (n_tile < rp.n_heads + rp.n_kv)

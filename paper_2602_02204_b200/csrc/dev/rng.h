@@ -43,4 +43,9 @@ OMNI_HD uint64_t noise_hash(uint64_t seed, uint64_t rid, uint32_t pos, uint32_t 
                                                            (static_cast<uint64_t>(s) << 12) ^ ch)));
 }
 
+// Top-k sampler draw: (stage sampling seed, request key, emitted index).
+OMNI_HD uint64_t sample_hash(uint64_t seed, uint32_t key, uint32_t index) {
+  return mix64(seed ^ mix64((static_cast<uint64_t>(key) << 32) ^ index ^ 0x73616d706c650000ull));
+}
+
 }  // namespace omni_dev

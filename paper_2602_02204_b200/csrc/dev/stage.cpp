@@ -16,6 +16,7 @@
 
 #include "common.h"
 #include "kernels.h"
+#include "rng.h"
 
 using namespace omni_dev;
 
@@ -146,16 +147,8 @@ void build_ar(omni_stage* st) {
     ly.wd = make_weight(st, p + "wd", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
     ly.gqkv = gemm_of(ly.wqkv, 8);
     ly.go = gemm_of(ly.wo, 8);
-    static const int gu_split = [] {  // OMNI_GU_SPLIT: split cap of the gate-up GEMM (CTA target 256 if > 1)
-      const char* e = std::getenv("OMNI_GU_SPLIT");
-      return e ? std::atoi(e) : 1;
-    }();
-    ly.ggu = gemm_of(ly.wgu, gu_split, gu_split > 1 ? 256 : 192);
-    static const int down_split = [] {  // OMNI_DOWN_SPLIT (experiments): split cap / CTA target of the down proj
-      const char* e = std::getenv("OMNI_DOWN_SPLIT");
-      return e ? std::atoi(e) : 8;
-    }();
-    ly.gd = gemm_of(ly.wd, down_split, down_split > 8 ? 256 : 192);
+    ly.ggu = gemm_of(ly.wgu, 1);  // 128 n-tiles: no split-K (a 2-way split measured neutral)
+    ly.gd = gemm_of(ly.wd, 8);    // 16 n-tiles x 8-way split-K (16-way measured slower)
   }
 
   // activations
@@ -168,11 +161,6 @@ void build_ar(omni_stage* st) {
   st->act = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
   st->hbuf = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
   st->logits = dev_alloc<float>(st, (size_t)R * st->vocab_pad);
-  // per-step results [n_dec tokens | n_dec margins] contiguous -> one D2H copy
-  st->d_tok = dev_alloc<int32_t>(st, 2 * (size_t)R);
-  st->d_margin = reinterpret_cast<float*>(st->d_tok + R);  // unused slot kept for the struct
-  st->head_cnt = dev_alloc<int32_t>(st, (size_t)R);
-  OMNI_CUDA(cudaMemsetAsync(st->head_cnt, 0, (size_t)R * sizeof(int32_t), st->stream));
   st->in_xn = input_of(st->xn, R, d);
   st->in_attn = input_of(st->attn, R, H * kHeadDim);
   st->in_act = input_of(st->act, R, ff);
@@ -189,6 +177,9 @@ void build_ar(omni_stage* st) {
   // paged KV: [page][layer][k|v][kv_head][16][128] bf16
   st->max_pages = (st->lim.max_seq_len + kPageTokens - 1) / kPageTokens;
   int pages = st->lim.kv_pages > 0 ? st->lim.kv_pages : st->lim.max_resident * st->max_pages;
+  st->page_table = dev_alloc<int32_t>(st, (size_t)st->lim.max_resident * st->max_pages);
+  OMNI_CUDA(cudaMemsetAsync(st->page_table, 0, (size_t)st->lim.max_resident * st->max_pages * sizeof(int32_t),
+                            st->stream));
   st->kv = dev_alloc<__nv_bfloat16>(st, (size_t)pages * L * 2 * KVH * kPageTokens * kHeadDim);
   st->free_pages.resize(pages);
   for (int i = 0; i < pages; ++i) st->free_pages[i] = pages - 1 - i;
@@ -205,23 +196,6 @@ void build_ar(omni_stage* st) {
   st->rope = dev_alloc<float2>(st, rt.size());
   OMNI_CUDA(cudaMemcpyAsync(st->rope, rt.data(), rt.size() * sizeof(float2), cudaMemcpyHostToDevice,
                             st->stream));
-  // step-chain resources (chain.cu): TMA descriptors in global memory, op
-  // completion counters
-  {
-    std::vector<CUtensorMap> maps;
-    for (const auto& ly : st->layers) maps.insert(maps.end(), {ly.gqkv.tmap, ly.go.tmap, ly.ggu.tmap, ly.gd.tmap});
-    maps.push_back(st->glm.tmap);
-    maps.push_back(talker ? st->ghid.tmap : st->glm.tmap);
-    maps.push_back(st->in_xn.tmaps[0]);
-    maps.push_back(st->in_attn.tmaps[0]);
-    maps.push_back(st->in_act.tmaps[0]);
-    maps.push_back(st->in_hbuf.tmaps[0]);
-    maps.push_back(talker ? st->in_cond.tmaps[0] : st->in_xn.tmaps[0]);
-    st->chain_maps = dev_alloc<CUtensorMap>(st, maps.size());
-    OMNI_CUDA(cudaMemcpyAsync(st->chain_maps, maps.data(), maps.size() * sizeof(CUtensorMap),
-                              cudaMemcpyHostToDevice, st->stream));
-    st->chain_done = dev_alloc<int>(st, kChainMaxOps + 1);
-  }
   // OMNI_STEP_TRACE=1 (tools/step_trace.py): every GEMM launch of a step
   // records its per-CTA phase stamps in its own slot (baked into the graphs).
   if (const char* e = std::getenv("OMNI_STEP_TRACE"); e && e[0] == '1') {
@@ -230,20 +204,12 @@ void build_ar(omni_stage* st) {
   }
   // Step results [n_dec tokens | n_dec margins]: the argmax kernel stores
   // them straight into mapped pinned host memory (no D2H copy on the step's
-  // tail: -2..3 µs per step, profiles/r01_zc_tok_ab.txt); OMNI_ZC_TOK=0: a
-  // device buffer + one D2H copy.
-  static const bool zc = [] {
-    const char* e = std::getenv("OMNI_ZC_TOK");
-    return !(e && e[0] == '0');
-  }();
-  st->zc_tok = zc;
-  if (zc) {
-    OMNI_CUDA(cudaHostAlloc(&st->h_tok, 2 * (size_t)R * sizeof(int32_t), cudaHostAllocMapped));
+  // tail: -2..3 µs per step, profiles/r01_zc_tok_ab.txt).
+  OMNI_CUDA(cudaHostAlloc(&st->h_tok, 2 * (size_t)R * sizeof(int32_t), cudaHostAllocMapped));
+  {
     void* dp = nullptr;
     OMNI_CUDA(cudaHostGetDevicePointer(&dp, st->h_tok, 0));
     st->d_tok = static_cast<int32_t*>(dp);
-  } else {
-    OMNI_CUDA(cudaMallocHost(&st->h_tok, 2 * (size_t)R * sizeof(int32_t)));
   }
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
 }
@@ -277,20 +243,11 @@ void build_dit(omni_stage* st) {
     ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
     ly.gqkv = gemm_of(ly.wqkv, 1);
     ly.gqkv.fill_sms = true;
-    static const int dit_split = [] {  // OMNI_DIT_SPLIT: split-K cap of the O projection (experiments)
-      const char* e = std::getenv("OMNI_DIT_SPLIT");
-      return e ? std::atoi(e) : 1;
-    }();
-    static const int dit_split2 = [] {  // OMNI_DIT_SPLIT_W2: split-K cap of the MLP-down (K = 4d).
-      // Default 1 with the widest-tile policy (profiles/r01_bench_ditw2_ab.log)
-      const char* e = std::getenv("OMNI_DIT_SPLIT_W2");
-      return e ? std::atoi(e) : 1;
-    }();
-    ly.go = gemm_of(ly.wo, dit_split, 64);
+    ly.go = gemm_of(ly.wo, 1, 64);
     ly.go.fill_sms = true;
     ly.g1 = gemm_of(ly.w1, 1);
     ly.g1.fill_sms = true;
-    ly.g2 = gemm_of(ly.w2, dit_split2, 64);
+    ly.g2 = gemm_of(ly.w2, 1, 64);
     ly.g2.fill_sms = true;
   }
   const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
@@ -304,7 +261,6 @@ void build_dit(omni_stage* st) {
   st->du = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
   const int cvec_rows = std::max(T, m.vocab);  // per-step rows / adaLN table rows
   st->dcvec = dev_alloc<__nv_bfloat16>(st, (size_t)cvec_rows * d);
-  st->dsamples = dev_alloc<int32_t>(st, R);
   st->din_x = input_of(st->dxin, R, C);
   st->din_a = input_of(st->da, R, d);
   st->din_o = input_of(st->dout, R, d);
@@ -330,10 +286,10 @@ void build_dit(omni_stage* st) {
       OMNI_KERNEL(gemm_run(st->g_mod, st->din_c, m.vocab, EPI_F32, e, st->stream));
     }
   }
+  // Zero-copy waveform samples: the Euler epilogue of the last step stores
+  // them straight into the pinned host buffer (UVA).
   OMNI_CUDA(cudaMallocHost(&st->h_samples, (size_t)R * sizeof(int32_t)));
-  // Zero-copy waveform samples (OMNI_ZC_TOK, default on): the Euler epilogue
-  // of the last step stores them straight into the pinned host buffer (UVA).
-  if (const char* e = std::getenv("OMNI_ZC_TOK"); !(e && e[0] == '0')) st->dsamples = st->h_samples;
+  st->dsamples = st->h_samples;
   OMNI_CUDA(cudaStreamSynchronize(st->stream));
 }
 
@@ -350,7 +306,7 @@ void destroy_stage(omni_stage* st) {
   }
   if (st->h_tok) cudaFreeHost(st->h_tok);
   if (st->h_samples) cudaFreeHost(st->h_samples);
-  for (cudaEvent_t e : {st->ev_start, st->ev_done, st->ev_link})
+  for (cudaEvent_t e : {st->ev_start, st->ev_done, st->ev_link, st->ev_pack})
     if (e) cudaEventDestroy(e);
   if (st->stream) cudaStreamDestroy(st->stream);
   delete st;
@@ -375,7 +331,9 @@ void ensure_pages(omni_stage* st, SeqSlot& s, int upto) {
                "sequence longer than max_seq_len (" + std::to_string(st->lim.max_seq_len) + ")");
   while ((int)s.pages.size() < need) {
     OMNI_REQUIRE(!st->free_pages.empty(), OMNI_E_OOM, "paged-KV pool exhausted");
-    s.pages.push_back(st->free_pages.back());
+    const int page = st->free_pages.back();
+    st->pending_deltas.push_back(PageDelta{s.slot * st->max_pages + (int)s.pages.size(), page});
+    s.pages.push_back(page);
     st->free_pages.pop_back();
   }
 }
@@ -458,148 +416,16 @@ void run_graph(omni_stage* st, uint64_t key, F&& body) {
   counters().launches += sg->nodes;
 }
 
-// The whole AR step as one launch (chain.cu): the same ops, epilogues and
-// split-K factors as the per-kernel path below, as an op table.
-void launch_step_chain(omni_stage* st, const ArStepDev& sd, int n_rows, int n_blocks, int n_dec, bool cond) {
-  const auto& m = st->m;
-  const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
-  const bool talker = m.kind == OMNI_MODEL_TALKER;
-  ChainParams P{};
-  P.sd = sd;
-  P.maps = st->chain_maps;
-  P.done = st->chain_done;
-  P.ticket = st->chain_done + kChainMaxOps;
-  P.trace = st->chain_trace;
-  P.emb = st->emb.p;
-  P.emb2 = talker ? st->emb2.p : nullptr;
-  P.hproj = st->hproj;
-  P.cond_table = st->cond_table;
-  P.cond_rows = st->cond_rows;
-  P.d = d;
-  P.start_id = st->start_id;
-  P.x = st->x;
-  P.xb = st->xn;
-  P.ss = st->ss;
-  P.ss_ld = d / 128;
-  P.cond_dim = m.cond_dim;
-  P.condin = st->condin;
-  P.q = st->q;
-  P.n_heads = H;
-  P.n_kv = KVH;
-  P.n_layers = L;
-  P.kv = st->kv;
-  P.attn = st->attn;
-  P.attn_scale = 1.0f / std::sqrt((float)kHeadDim);
-  P.eps = kNormEps;
-  P.hbuf = st->hbuf;
-  P.ring = talker ? nullptr : st->ring;
-  P.ring_rows = st->ring_rows;
-  P.logits = st->logits;
-  P.lm = st->lm.p;
-  P.vocab = m.vocab;
-  P.vocab_pad = st->vocab_pad;
-  P.argmax_lo = st->argmax_lo;
-  P.argmax_hi = st->argmax_hi;
-  P.tok = st->d_tok;
-  P.margin = reinterpret_cast<float*>(st->d_tok + n_dec);
-  int total = 0;
-  auto add = [&](ChainOp op) {  // item ranges padded to whole clusters (one ticket = 8 items)
-    OMNI_REQUIRE(P.n_ops < kChainMaxOps, OMNI_E_BADARG, "step chain: too many ops");
-    if (op.n_items <= 0) return;
-    op.first = total;
-    total += (op.n_items + kChainCluster - 1) / kChainCluster * kChainCluster;
-    P.ops[P.n_ops++] = op;
-  };
-  auto simple = [&](int kind, int items) {
-    ChainOp op{};
-    op.kind = kind;
-    op.n_items = op.units = items;
-    return op;
-  };
-  auto gemm = [&](const GemmWeight& w, int w_map, int x_map, const GemmInput& xin, int M, int epi,
-                  const GemmEpilogue& e) {
-    ChainOp op{};
-    op.kind = CHAIN_GEMM;
-    OMNI_CUDA(gemm_make_args(w, xin, M, epi, e, op.a));
-    op.w_map = w_map;
-    op.x_map = x_map;
-    op.epi = epi;
-    op.n_tiles = w.N_pad / 128;
-    op.splits = w.splits;
-    op.kb_per = (w.K / 64) / w.splits;
-    op.n_items = op.n_tiles * op.splits;
-    op.units = op.n_items;  // every split signals after the cluster reduction
-    OMNI_REQUIRE(kChainCluster % op.splits == 0, OMNI_E_BADARG, "step chain: split-K must divide the cluster");
-    add(op);
-  };
-  const int mx = 4 * L + 2;  // input descriptor indices: xn, attn, act, hbuf, cond
-  if (cond) {
-    add(simple(CHAIN_GATHER_COND, n_rows));
-    GemmEpilogue e;
-    e.out = st->hproj;
-    e.ldo = d;
-    gemm(st->ghid, 4 * L + 1, mx + 4, st->in_cond, n_rows, EPI_F32, e);
-  }
-  add(simple(CHAIN_EMBED, n_rows));
-  GemmEpilogue norm_in;
-  norm_in.ss_in = st->ss;
-  norm_in.ss_ld = d / 128;
-  norm_in.ss_n = d / 128;
-  norm_in.norm_d = (float)d;
-  norm_in.norm_eps = kNormEps;
-  for (int l = 0; l < L; ++l) {
-    const auto& ly = st->layers[l];
-    GemmEpilogue e = norm_in;
-    e.out = st->q;
-    e.ldo = H * kHeadDim;
-    e.rope.rows = sd.rows;
-    e.rope.page_table = sd.page_table;
-    e.rope.max_pages = sd.max_pages;
-    e.rope.table = st->rope;
-    e.rope.q_out = st->q;
-    e.rope.kv = st->kv;
-    e.rope.n_heads = H;
-    e.rope.n_kv = KVH;
-    e.rope.layer = l;
-    e.rope.n_layers = L;
-    gemm(ly.gqkv, 4 * l + 0, mx + 0, st->in_xn, n_rows, EPI_ROPE_KV, e);
-    ChainOp at = simple(CHAIN_ATTN, n_blocks * KVH);
-    at.layer = l;
-    add(at);
-    GemmEpilogue r;
-    r.out = st->x;
-    r.ldo = d;
-    r.xb = st->xn;
-    r.ss_out = st->ss;
-    r.ss_ld = d / 128;
-    gemm(ly.go, 4 * l + 1, mx + 1, st->in_attn, n_rows, EPI_RESID_NORM, r);
-    e = norm_in;
-    e.out = st->act;
-    e.ldo = m.d_ff;
-    gemm(ly.ggu, 4 * l + 2, mx + 0, st->in_xn, n_rows, EPI_SWIGLU, e);
-    gemm(ly.gd, 4 * l + 3, mx + 2, st->in_act, n_rows, EPI_RESID_NORM, r);
-  }
-  if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
-    add(simple(CHAIN_HEAD, n_dec));
-  } else if (n_dec > 0) {
-    add(simple(CHAIN_FINAL, n_dec));
-    GemmEpilogue e;
-    e.out = st->logits;
-    e.ldo = st->vocab_pad;
-    gemm(st->glm, 4 * L, mx + 3, st->in_hbuf, n_dec, EPI_F32, e);
-    add(simple(CHAIN_ARGMAX, n_dec));
-  }
-  st->chain_last_items = total;
-  st->chain_last_nops = P.n_ops;
-  for (int i = 0; i < P.n_ops; ++i) st->chain_last_first[i] = P.ops[i].first;
-  OMNI_KERNEL(chain_launch(P, total, st->stream));
-}
-
 // Descriptor blob at FIXED offsets (capacity-sized regions, so the device
 // pointers baked into a captured step graph never change):
-//   entries | decode entry list | attention blocks | rows | page table
+//   entries | decode entry list | attention blocks | rows | page-table delta
+// The page table itself is persistent in HBM ([slot][max_pages], indexed by
+// the resident slot); a step's blob carries only the page assignments made
+// since the previous step ({index, page} pairs, count in the delta header),
+// which the step's first kernel applies. So the blob stays ~20 KB even when
+// max_seq_len is the 8192-token kv budget (516 pages per sequence).
 struct ArDescLayout {
-  size_t off_dec, off_blk, off_rows, off_pt, reserve;
+  size_t off_dec, off_blk, off_rows, off_delta, reserve, cap_delta;
 };
 ArDescLayout ar_desc_layout(const omni_stage* st) {
   const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
@@ -607,15 +433,16 @@ ArDescLayout ar_desc_layout(const omni_stage* st) {
   l.off_dec = align16(cap_e * sizeof(ArEntryDesc));
   l.off_blk = l.off_dec + align16(cap_e * sizeof(int32_t));
   l.off_rows = l.off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
-  l.off_pt = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
-  l.reserve = l.off_pt + cap_e * st->max_pages * sizeof(int32_t);
+  l.off_delta = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
+  l.cap_delta = kPageDeltaCap;
+  l.reserve = l.off_delta + sizeof(PageDeltaHeader) + l.cap_delta * sizeof(PageDelta);
   return l;
 }
 ArStepDev ar_step_dev(const omni_stage* st, const ArDescLayout& lay) {
   ArStepDev sd;
   sd.entries = reinterpret_cast<const ArEntryDesc*>(st->desc.dev);
   sd.rows = reinterpret_cast<const ArRowDesc*>(st->desc.dev + lay.off_rows);
-  sd.page_table = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_pt);
+  sd.page_table = st->page_table;
   sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_dec);
   sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + lay.off_blk);
   sd.max_pages = st->max_pages;
@@ -625,15 +452,24 @@ ArStepDev ar_step_dev(const omni_stage* st, const ArDescLayout& lay) {
 // step-specific is read from the fixed-offset descriptor blob, so the launch
 // sequence depends on (n_rows, n_blocks, n_dec, cond_prefill) only -- the
 // step-graph key.
+//
+// Ordering contract of the blob: desc_copy_kernel (first kernel) copies it
+// from pinned staging and applies the page-table delta; the next kernel
+// (embed / gather_cond) waits for it (PdlDep: griddepcontrol.wait BEFORE its
+// launch_dependents), so every later kernel -- including the attention and
+// RoPE-epilogue reads that run before their own griddepcontrol.wait -- sees
+// a completed copy. Keep that wait-before-trigger order in the kernel after
+// desc_copy.
 void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_blocks, int n_dec,
                        bool cond_prefill) {
   const auto& m = st->m;
   const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   const bool talker = m.kind == OMNI_MODEL_TALKER;
   cudaStream_t s = st->stream;
-  if (st->desc_kernel) {  // the whole (capacity-sized) blob: the size is baked into step graphs
+  {
     const ArDescLayout lay = ar_desc_layout(st);
-    OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, lay.reserve, s));
+    OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, lay.off_delta, st->desc.host + lay.off_delta,
+                                 st->page_table, s));
   }
   int trace_slot = 0;  // OMNI_STEP_TRACE: one slot per GEMM launch, in launch order
   auto traced = [&](GemmEpilogue e) {
@@ -651,22 +487,6 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   // st->xn holds bf16(x) (un-normalised); the RMSNorm scale is applied in
   // the consuming GEMM's epilogue from the per-tile sums of squares st->ss.
   const int ss_ld = d / 128;
-  // Cross-kernel weight pipelining (OMNI_PF_MB, default off): each decode
-  // GEMM (>= 128 CTAs, so the prefetch is spread over every SM's memory
-  // pipe) pulls the first OMNI_PF_MB of the NEXT GEMM's weights into L2
-  // after issuing its own stream. Small-grid kernels (embed, attention)
-  // never prefetch: a few SMs cannot pull MBs fast (measured: 4 attention
-  // CTAs prefetching 32 MB took 43 us).
-  static const uint64_t kPf = [] {
-    const char* e = std::getenv("OMNI_PF_MB");
-    return (uint64_t)(e ? std::atoi(e) : 0) << 20;
-  }();
-  auto wbytes = [](const GemmWeight& g) { return (uint64_t)g.N_pad * g.K * 2; };
-  auto part = [&](const GemmWeight& g, uint64_t off) -> std::pair<const void*, uint64_t> {
-    const uint64_t n = wbytes(g);
-    if (off >= n || kPf == 0) return {nullptr, 0};
-    return {reinterpret_cast<const char*>(g.ptr) + off, std::min(kPf, n - off)};
-  };
   OMNI_KERNEL(launch_embed(sd, n_rows, st->emb.p, talker ? st->emb2.p : nullptr, st->hproj,
                          st->cond_table, st->cond_rows, d, st->start_id, st->x, st->xn, st->ss, ss_ld,
                          nullptr, 0, s));
@@ -691,54 +511,30 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
     e.rope.n_kv = KVH;
     e.rope.layer = l;
     e.rope.n_layers = L;
-    // OMNI_PF_MODE=2: "two ahead" -- the QKV GEMM pulls the WHOLE gate-up
-    // weight and the O GEMM the whole down weight into L2 while the
-    // latency-bound QKV -> attention -> O segment leaves HBM idle.
-    static const int pf_mode = [] {
-      const char* e = std::getenv("OMNI_PF_MODE");
-      return e ? std::atoi(e) : 1;
-    }();
-    std::tie(e.pf_ptr, e.pf_bytes) = pf_mode == 2 ? part(ly.ggu, 0) : part(ly.go, 0);
     OMNI_KERNEL(gemm_run(ly.gqkv, st->in_xn, n_rows, EPI_ROPE_KV, traced(e), s));
-    static const bool skip_attn = [] {  // OMNI_SKIP_ATTN=1: timing attribution only (wrong outputs)
-      const char* e = std::getenv("OMNI_SKIP_ATTN");
-      return e && e[0] == '1';
-    }();
-    if (!skip_attn)
-      OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
+    OMNI_KERNEL(launch_attention(sd, n_blocks, st->q, H, KVH, l, L, st->kv, st->attn, nullptr, 0, s));
     GemmEpilogue r;  // x += attn W_o^T; xb = bf16(x); ss = sums of squares
     r.out = st->x;
     r.ldo = d;
     r.xb = st->xn;
     r.ss_out = st->ss;
     r.ss_ld = ss_ld;
-    std::tie(r.pf_ptr, r.pf_bytes) = pf_mode == 2 ? part(ly.gd, 0) : part(ly.ggu, 0);
     OMNI_KERNEL(gemm_run(ly.go, st->in_attn, n_rows, EPI_RESID_NORM, traced(r), s));
     e = norm_in;
     e.out = st->act;
     e.ldo = m.d_ff;
-    std::tie(e.pf_ptr, e.pf_bytes) = pf_mode == 2 ? std::pair<const void*, uint64_t>{nullptr, 0} : part(ly.gd, 0);
     OMNI_KERNEL(gemm_run(ly.ggu, st->in_xn, n_rows, EPI_SWIGLU, traced(e), s));
-    std::tie(r.pf_ptr, r.pf_bytes) = pf_mode == 2 ? std::pair<const void*, uint64_t>{nullptr, 0}
-                                     : l + 1 < L  ? part(st->layers[l + 1].gqkv, 0)
-                                                  : part(st->glm, 0);
     OMNI_KERNEL(gemm_run(ly.gd, st->in_act, n_rows, EPI_RESID_NORM, traced(r), s));
   }
-  if (n_dec > 0 && st->fused_head && m.vocab <= kHeadMaxVocab && d % 256 == 0) {
-    // one kernel: final norm (+ hidden ring) -> LM head -> argmax
-    OMNI_KERNEL(launch_head(sd, n_dec, st->x, d, kNormEps, st->hbuf, talker ? nullptr : st->ring,
-                            st->ring_rows, st->lm.p, m.vocab, st->logits, st->vocab_pad, st->argmax_lo,
-                            st->argmax_hi, st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec),
-                            st->head_cnt, s));
-  } else if (n_dec > 0) {
+  if (n_dec > 0) {
     OMNI_KERNEL(launch_final_gather(sd, n_dec, st->x, d, kNormEps, st->hbuf,
                                     talker ? nullptr : st->ring, st->ring_rows, s));
     GemmEpilogue e;
     e.out = st->logits;
     e.ldo = st->vocab_pad;
     OMNI_KERNEL(gemm_run(st->glm, st->in_hbuf, n_dec, EPI_F32, traced(e), s));
-    OMNI_KERNEL(launch_argmax(st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi,
-                              st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
+    OMNI_KERNEL(launch_sample(sd, st->logits, st->vocab_pad, n_dec, st->argmax_lo, st->argmax_hi, st->top_k,
+                              st->sample_seed, st->d_tok, reinterpret_cast<float*>(st->d_tok + n_dec), s));
   }
 }
 
@@ -751,7 +547,7 @@ uint64_t ar_graph_key(int n_rows, int n_blocks, int n_dec, bool cond_prefill) {
 // creation (~1 ms host time each) instead of stalling the serving loop the
 // third time a batch size shows up. OMNI_PREWARM=<max decode rows> (0 = off).
 void prewarm_decode_graphs(omni_stage* st) {
-  if (!graphs_enabled() || st->chain_on) return;
+  if (!graphs_enabled()) return;
   static const int cap_env = [] {
     const char* e = std::getenv("OMNI_PREWARM");
     return e ? std::atoi(e) : -1;
@@ -786,20 +582,22 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
 
   OMNI_REQUIRE(ne <= st->lim.max_resident, OMNI_E_BADARG, "more entries than max_resident_requests");
   const ArDescLayout lay = ar_desc_layout(st);
-  const size_t off_dec = lay.off_dec, off_blk = lay.off_blk, off_rows = lay.off_rows, off_pt = lay.off_pt;
-  const size_t total = off_pt + align16((size_t)ne * st->max_pages * sizeof(int32_t));
   if (staging_reserve(st->desc, lay.reserve)) drop_graphs(st);
+  // every entry's pages first: a failure leaves the step unlaunched
+  for (int e = 0; e < ne; ++e) ensure_pages(st, seq_for(st, b->seq_id[e]), b->pos0[e] + b->span[e]);
+  OMNI_REQUIRE(st->pending_deltas.size() <= lay.cap_delta, OMNI_E_OOM,
+               "more page assignments than one step's page-table delta holds");
   auto* ents = reinterpret_cast<ArEntryDesc*>(st->desc.host);
-  auto* rows = reinterpret_cast<ArRowDesc*>(st->desc.host + off_rows);
-  auto* pt = reinterpret_cast<int32_t*>(st->desc.host + off_pt);
-  auto* dec = reinterpret_cast<int32_t*>(st->desc.host + off_dec);
-  auto* blks = reinterpret_cast<AttnBlockDesc*>(st->desc.host + off_blk);
+  auto* rows = reinterpret_cast<ArRowDesc*>(st->desc.host + lay.off_rows);
+  auto* dec = reinterpret_cast<int32_t*>(st->desc.host + lay.off_dec);
+  auto* blks = reinterpret_cast<AttnBlockDesc*>(st->desc.host + lay.off_blk);
+  auto* dh = reinterpret_cast<PageDeltaHeader*>(st->desc.host + lay.off_delta);
+  auto* dl = reinterpret_cast<PageDelta*>(st->desc.host + lay.off_delta + sizeof(PageDeltaHeader));
   int n_blocks = 0;
   std::vector<int> dec_list;
   int r = 0, n_prefill_rows = 0;
   for (int e = 0; e < ne; ++e) {
-    SeqSlot& s = seq_for(st, b->seq_id[e]);
-    ensure_pages(st, s, b->pos0[e] + b->span[e]);
+    SeqSlot& s = st->seqs.at(b->seq_id[e]);
     const bool is_dec = b->phase[e] == OMNI_PHASE_DECODE;
     ArEntryDesc& ed = ents[e];
     ed.slot = s.slot;
@@ -809,7 +607,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
     ed.is_decode = is_dec ? 1 : 0;
     ed.out_index = is_dec ? b->out_index[e] : -1;
     ed.dec_row = is_dec ? (int)dec_list.size() : -1;
-    ed.pad = 0;
+    ed.key = (int32_t)(uint32_t)mix64(b->seq_id[e]);
     if (is_dec) {
       if (!talker)
         OMNI_REQUIRE(ed.out_index >= 0 && ed.out_index < st->ring_rows, OMNI_E_BADARG,
@@ -817,8 +615,6 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       dec[dec_list.size()] = e;
       dec_list.push_back(e);
     }
-    for (size_t k = 0; k < s.pages.size() && (int)k < st->max_pages; ++k)
-      pt[(size_t)e * st->max_pages + k] = s.pages[k];
     for (int t0 = 0; t0 < b->span[e]; t0 += kAttnQTok)
       blks[n_blocks++] = AttnBlockDesc{e, t0, std::min(kAttnQTok, b->span[e] - t0), 0};
     for (int t = 0; t < b->span[e]; ++t, ++r) {
@@ -827,6 +623,8 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       rd.pos = b->pos0[e] + t;
       rd.token = b->tokens[r];
       rd.cond_row = talker ? b->cond_row[r] : 0;
+      rd.slot = s.slot;
+      rd.pad = 0;
       rd.cond_src = (talker && !is_dec && b->cond_src) ? b->cond_src[r] : 0;
       if (talker) {
         OMNI_REQUIRE(rd.cond_row >= 0 && rd.cond_row < st->cond_rows, OMNI_E_BADARG,
@@ -840,35 +638,23 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
                    OMNI_E_BADARG, "input token id out of range");
     }
   }
+  // page assignments since the previous step (applied by the step's first kernel)
+  dh->n = (int32_t)st->pending_deltas.size();
+  for (size_t i = 0; i < st->pending_deltas.size(); ++i) dl[i] = st->pending_deltas[i];
+  st->pending_deltas.clear();
   const int n_dec = (int)dec_list.size();
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
-  const bool kcopy = st->desc_kernel && n_rows > 0 && !(st->chain_on && !talker && n_rows <= chain_max_rows());
-  if (!kcopy) {
-    OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, total, cudaMemcpyHostToDevice, s));
-    counters().h2d_bytes += total;
-    OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
-  } else {
-    counters().h2d_bytes += lay.reserve;
-  }
+  counters().h2d_bytes += lay.off_delta + sizeof(PageDeltaHeader) + dh->n * sizeof(PageDelta);
   const ArStepDev sd = ar_step_dev(st, lay);
-
-  const auto& m = st->m;
-  const int d = m.d_model, H = m.n_heads, KVH = m.n_kv_heads, L = m.n_layers;
   if (n_rows > 0) {
     const uint64_t key = ar_graph_key(n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0);
-    if (st->chain_on && !talker && n_rows <= chain_max_rows()) {
-      run_graph(st, key, [&] { launch_step_chain(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0); });
-    } else run_graph(st, key, [&] {
-      launch_ar_kernels(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0);
-    });
-    if (kcopy) OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));  // staging read by the step's first kernel
-    if (n_dec > 0) {
-      // tokens and margins in one copy: [n_dec x i32 | n_dec x f32]
-      if (!st->zc_tok)
-        OMNI_CUDA(cudaMemcpyAsync(st->h_tok, st->d_tok, 2 * n_dec * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      counters().d2h_bytes += n_dec * (sizeof(int32_t) + sizeof(float));
-    }
+    run_graph(st, key, [&] { launch_ar_kernels(st, sd, n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0); });
+    OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));  // staging read by the step's first kernel
+    if (n_dec > 0) counters().d2h_bytes += n_dec * (sizeof(int32_t) + sizeof(float));
+  } else if (dh->n > 0) {
+    // no rows to run but pages were assigned: keep them pending for the next step
+    for (int i = 0; i < dh->n; ++i) st->pending_deltas.push_back(dl[i]);
   }
   OMNI_CUDA(cudaEventRecord(st->ev_done, s));
   st->pending = true;
@@ -961,8 +747,8 @@ void prewarm_dit_graphs(omni_stage* st) {
     const uint64_t key = dit_graph_key(nt, 0);
     if (!st->graphs.count(key))
       capture_graph(st, key, [&] {
-        if (st->desc_kernel)
-          OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, (size_t)nt * sizeof(DitTokDesc), st->stream));
+        OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, (size_t)nt * sizeof(DitTokDesc), nullptr, nullptr,
+                                     st->stream));
         dit_chunk(st, toks_dev, nt, st->dsamples);
       });
   }
@@ -999,23 +785,17 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
   if (n_tok > 0) {
-    // descriptors: copied by the chunk graph's first kernel (desc_kernel) or by
-    // one H2D; either way the graph reads them from the device blob
-    if (!st->desc_kernel) {
-      OMNI_CUDA(cudaMemcpyAsync(st->desc.dev, st->desc.host, bytes, cudaMemcpyHostToDevice, s));
-      OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
-    }
+    // descriptors: copied from pinned staging by the chunk graph's first kernel
     counters().h2d_bytes += bytes;
     const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
     for (int64_t t0 = 0; t0 < n_tok; t0 += st->tok_cap) {
       const int nt = (int)std::min<int64_t>(st->tok_cap, n_pad - t0);
       run_graph(st, dit_graph_key(nt, t0), [&] {
-        if (st->desc_kernel)
-          OMNI_KERNEL(launch_desc_copy(st->desc.dev + t0 * sizeof(DitTokDesc), st->desc.host + t0 * sizeof(DitTokDesc),
-                                       (size_t)nt * sizeof(DitTokDesc), s));
+        OMNI_KERNEL(launch_desc_copy(st->desc.dev + t0 * sizeof(DitTokDesc), st->desc.host + t0 * sizeof(DitTokDesc),
+                                     (size_t)nt * sizeof(DitTokDesc), nullptr, nullptr, s));
         dit_chunk(st, toks_dev + t0, nt, st->dsamples);
       });
-      if (st->desc_kernel && t0 + st->tok_cap >= n_tok) OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
+      if (t0 + st->tok_cap >= n_tok) OMNI_CUDA(cudaEventRecord(st->desc.in_use, s));
       const int64_t nsamp = std::min<int64_t>(nt, n_tok - t0) * kDitSamples;  // real tokens only
       if (st->dsamples != st->h_samples)
         OMNI_CUDA(cudaMemcpyAsync(st->h_samples, st->dsamples, nsamp * sizeof(int32_t),
@@ -1057,63 +837,6 @@ void finish_pending(omni_stage* st) {
 }
 
 std::mutex g_init_mu;
-
-// Optional spatial partition of the GPU between the stage kinds (green
-// contexts, CUDA 12.4+): OMNI_SM_SPLIT="dit:N" runs DiT stages on N SMs;
-// "dit:N,ar" also confines the AR stages to the other SMs. Memory stays in
-// the primary context; only the streams (kernel placement) are partitioned.
-struct SmPartition {
-  bool ok = false;
-  CUgreenCtx dit = nullptr, rest = nullptr;
-  bool ar_rest = false;
-};
-
-template <typename F>
-F driver_fn(const char* n) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(n, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-    return nullptr;
-  return reinterpret_cast<F>(p);
-}
-
-SmPartition& sm_partition(int dev) {
-  static std::mutex mu;
-  static std::unordered_map<int, SmPartition> parts;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = parts.find(dev);
-  if (it != parts.end()) return it->second;
-  SmPartition& P = parts[dev];
-  const char* e = std::getenv("OMNI_SM_SPLIT");
-  if (!e || std::strncmp(e, "dit:", 4) != 0) return P;
-  const unsigned n = (unsigned)std::atoi(e + 4);
-  P.ar_rest = std::strstr(e, ",ar") != nullptr;
-  auto getRes = driver_fn<PFN_cuDeviceGetDevResource_v12040>("cuDeviceGetDevResource");
-  auto split = driver_fn<PFN_cuDevSmResourceSplitByCount_v12040>("cuDevSmResourceSplitByCount");
-  auto gen = driver_fn<PFN_cuDevResourceGenerateDesc_v12040>("cuDevResourceGenerateDesc");
-  auto gcreate = driver_fn<PFN_cuGreenCtxCreate_v12040>("cuGreenCtxCreate");
-  if (!getRes || !split || !gen || !gcreate) return P;
-  CUdevResource all{}, part{}, rest{};
-  unsigned groups = 1;
-  CUdevResourceDesc d1, d2;
-  if (getRes(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
-      split(&part, &groups, &all, &rest, 0, n) != CUDA_SUCCESS || groups != 1 ||
-      gen(&d1, &part, 1) != CUDA_SUCCESS || gen(&d2, &rest, 1) != CUDA_SUCCESS ||
-      gcreate(&P.dit, d1, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
-      gcreate(&P.rest, d2, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
-    return P;
-  P.ok = true;
-  return P;
-}
-
-cudaStream_t partitioned_stream(int dev, bool dit, int prio) {
-  SmPartition& P = sm_partition(dev);
-  if (!P.ok || (!dit && !P.ar_rest)) return nullptr;
-  auto gstream = driver_fn<PFN_cuGreenCtxStreamCreate_v12050>("cuGreenCtxStreamCreate");
-  CUstream s = nullptr;
-  if (!gstream || gstream(&s, dit ? P.dit : P.rest, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS) return nullptr;
-  return reinterpret_cast<cudaStream_t>(s);
-}
 
 }  // namespace
 
@@ -1193,20 +916,6 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     st->lim = *limits;
     st->dev = dev;
     st->seed = weight_seed;
-    // OMNI_CHAIN=1: run small Thinker steps as one step-chain launch. Off by
-    // default: measured no faster than the PDL kernel chain (~370 vs ~330 us,
-    // profiles/r01_chain_trace.txt) -- the per-op post-dependency latency,
-    // not the kernel boundary, dominates.
-    const char* ce = std::getenv("OMNI_CHAIN");
-    st->chain_on = ce && ce[0] == '1';
-    // OMNI_FUSED_HEAD=1: one-kernel head (measured flat at 1 row, slower at 16; default off)
-    const char* fh = std::getenv("OMNI_FUSED_HEAD");
-    st->fused_head = fh && fh[0] == '1';
-    // Step descriptors copied from pinned staging by the step's first kernel
-    // (UVA loads) instead of a copy-engine H2D: -9..10 µs per AR step
-    // (profiles/r01_desc_kernel_ab.txt). OMNI_DESC_KERNEL=0: cudaMemcpyAsync.
-    const char* dk = std::getenv("OMNI_DESC_KERNEL");
-    st->desc_kernel = !(dk && dk[0] == '0');
     if (st->lim.max_batch_tokens <= 0) st->lim.max_batch_tokens = 256;
     if (st->lim.max_resident <= 0) st->lim.max_resident = 64;
     if (st->lim.max_seq_len <= 0) st->lim.max_seq_len = 512;
@@ -1226,11 +935,11 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     const int kind_ix = model->kind == OMNI_MODEL_THINKER ? 0 : model->kind == OMNI_MODEL_TALKER ? 1 : 2;
     const int rank = std::clamp(ranks[kind_ix] - '0', 0, 2);
     const int prio = hi + (lo - hi) * rank / 2;
-    st->stream = partitioned_stream(dev, model->kind == OMNI_MODEL_DIT, prio);
-    if (!st->stream) OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, prio));
+    OMNI_CUDA(cudaStreamCreateWithPriority(&st->stream, cudaStreamNonBlocking, prio));
     OMNI_CUDA(cudaEventCreate(&st->ev_start));
     OMNI_CUDA(cudaEventCreate(&st->ev_done));
     OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_link, cudaEventDisableTiming));
+    OMNI_CUDA(cudaEventCreateWithFlags(&st->ev_pack, cudaEventDisableTiming));
     if (model->kind == OMNI_MODEL_DIT) {
       build_dit(st);
       prewarm_dit_graphs(st);
@@ -1244,29 +953,6 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
   });
   if (rc != OMNI_OK && st) destroy_stage(st);
   return rc;
-}
-
-omni_status omni_stage_set_chain(omni_stage* st, int32_t on) {
-  return guarded([&] {
-    OMNI_REQUIRE(st != nullptr, OMNI_E_BADARG, "null stage");
-    ensure_idle(st);
-    if (st->chain_on != (on != 0)) drop_graphs(st);  // cached step graphs bake the mode in
-    st->chain_on = on != 0;
-  });
-}
-
-omni_status omni_stage_chain_trace(omni_stage* st, uint64_t trace_dev, int32_t* n_items, int32_t* n_ops,
-                                   int32_t* op_first) {
-  return guarded([&] {
-    OMNI_REQUIRE(st != nullptr, OMNI_E_BADARG, "null stage");
-    ensure_idle(st);
-    drop_graphs(st);  // the trace pointer is baked into captured launches
-    st->chain_trace = reinterpret_cast<unsigned long long*>(trace_dev);
-    if (n_items) *n_items = st->chain_last_items;
-    if (n_ops) *n_ops = st->chain_last_nops;
-    if (op_first)
-      for (int i = 0; i < st->chain_last_nops; ++i) op_first[i] = st->chain_last_first[i];
-  });
 }
 
 omni_status omni_stage_destroy(omni_stage* st) {
@@ -1461,10 +1147,10 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
     staging_reserve(src->pack, total);
     auto* cd = reinterpret_cast<PackChunkDesc*>(src->pack.host);
     auto* tk = reinterpret_cast<int32_t*>(src->pack.host + off_tok);
-    // desc_kernel: the pack kernel reads its descriptors straight from the
-    // pinned staging buffer (UVA) -- no copy-engine H2D ahead of it on the
-    // thinker stream, where the next Thinker step queues behind it
-    const uint8_t* desc_base = src->desc_kernel ? src->pack.host : src->pack.dev;
+    // the pack kernel reads its descriptors straight from the pinned staging
+    // buffer (UVA) -- no copy-engine H2D ahead of it on the thinker stream,
+    // where the next Thinker step queues behind it
+    const uint8_t* desc_base = src->pack.host;
     const auto* tk_dev = reinterpret_cast<const int32_t*>(desc_base + off_tok);
     int at = 0;
     for (int c = 0; c < n_chunks; ++c) {
@@ -1474,15 +1160,44 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
       for (int r = begin[c]; r < end[c]; ++r, ++at) tk[at] = tokens[at];
     }
     cudaStream_t s = src->stream;
-    if (!src->desc_kernel) {
-      OMNI_CUDA(cudaMemcpyAsync(src->pack.dev, src->pack.host, total, cudaMemcpyHostToDevice, s));
-      OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));
-    }
     counters().h2d_bytes += total;
     OMNI_KERNEL(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(desc_base), n_chunks, max_rows,
                                  src->ring, src->m.d_model, src->ring_rows, reinterpret_cast<uint8_t*>(dst_base),
                                  s));
-    if (src->desc_kernel) OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));  // staging read by the kernel
+    OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));  // staging read by the kernel
+    // consumers wait for exactly this pack (omni_stage_after_pack), not for
+    // whatever the producer enqueues after it (its next step)
+    OMNI_CUDA(cudaEventRecord(src->ev_pack, s));
+    src->pack_recorded = true;
+  });
+}
+
+omni_status omni_stage_after_pack(omni_stage* dst, omni_stage* src) {
+  return guarded([&] {
+    OMNI_REQUIRE(dst && src, OMNI_E_BADARG, "null stage");
+    if (!src->pack_recorded) return;
+    OMNI_CUDA(cudaSetDevice(dst->dev));
+    OMNI_CUDA(cudaStreamWaitEvent(dst->stream, src->ev_pack, 0));  // cross-device waits are legal
+  });
+}
+
+omni_status omni_seq_reserve(omni_stage* st, uint64_t seq_id, int32_t upto_tokens) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && st->m.kind != OMNI_MODEL_DIT, OMNI_E_BADARG, "omni_seq_reserve needs an AR stage");
+    OMNI_REQUIRE(upto_tokens >= 0, OMNI_E_BADARG, "negative token count");
+    ensure_pages(st, seq_for(st, seq_id), upto_tokens);
+  });
+}
+
+omni_status omni_stage_set_sampling(omni_stage* st, int32_t top_k, uint64_t seed) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && st->m.kind != OMNI_MODEL_DIT, OMNI_E_BADARG, "sampling applies to AR stages");
+    OMNI_REQUIRE(top_k >= 0 && top_k <= 32, OMNI_E_BADARG, "top_k must be in [0, 32]");
+    ensure_idle(st);
+    if (st->top_k != top_k || st->sample_seed != seed) drop_graphs(st);  // both are baked into step graphs
+    st->top_k = top_k;
+    st->sample_seed = seed;
+    if (top_k > 1) prewarm_decode_graphs(st);
   });
 }
 

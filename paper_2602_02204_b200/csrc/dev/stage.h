@@ -9,7 +9,6 @@
 #include <vector>
 
 #include "ar_kernels.h"
-#include "chain.h"
 #include "dit_kernels.h"
 #include "gemm.h"
 #include "omni_dev.h"
@@ -63,6 +62,8 @@ struct omni_stage {
   uint64_t seed = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_link = nullptr;
+  cudaEvent_t ev_pack = nullptr;  // recorded right after each connector pack
+  bool pack_recorded = false;
   std::vector<void*> allocs;
   std::unordered_map<std::string, omni_dev::DevTensor> named;
   uint64_t weight_bytes = 0;
@@ -83,13 +84,15 @@ struct omni_stage {
   __nv_bfloat16* condin = nullptr;
   float* hproj = nullptr;
   float* logits = nullptr;
-  int32_t* d_tok = nullptr;
-  int32_t* head_cnt = nullptr;  // fused head: per-decode-row CTA tickets
-  float* d_margin = nullptr;
+  int32_t* d_tok = nullptr;  // device alias of the mapped pinned h_tok
+  int top_k = 0;             // 0/1 greedy, k > 1 top-k sampling (omni_stage_set_sampling)
+  uint64_t sample_seed = 0;
   float* cond_table = nullptr;
   __nv_bfloat16* ring = nullptr;
   __nv_bfloat16* kv = nullptr;
   float2* rope = nullptr;
+  int32_t* page_table = nullptr;  // persistent [max_resident][max_pages]
+  std::vector<omni_dev::PageDelta> pending_deltas;  // page assignments not yet shipped to the device
   omni_dev::GemmInput in_xn, in_attn, in_act, in_hbuf, in_cond;
   std::unordered_map<uint64_t, omni_dev::SeqSlot> seqs;
   std::vector<int> free_slots, free_pages;
@@ -108,10 +111,8 @@ struct omni_stage {
 
   // ---- step staging / results ----
   omni_dev::Staging desc, pack;
-  int32_t* h_tok = nullptr;
-  bool zc_tok = false;
-  bool desc_kernel = false;  // step descriptors copied by the step's first kernel (OMNI_DESC_KERNEL)
-  unsigned long long* step_trace = nullptr;  // OMNI_STEP_TRACE debug stamps  // h_tok is mapped: kernels write results to host memory directly
+  int32_t* h_tok = nullptr;  // mapped: the sampler writes results to host memory directly
+  unsigned long long* step_trace = nullptr;  // OMNI_STEP_TRACE debug stamps
   int32_t* h_samples = nullptr;
   bool pending = false;
   int pending_kind = 0;  // 1 = AR, 2 = DiT
@@ -124,13 +125,4 @@ struct omni_stage {
   float last_step_us = 0.f;
   std::unordered_map<uint64_t, omni_dev::StepGraph> graphs;  // step graphs by launch geometry
   std::unordered_map<uint64_t, int> key_hits;                 // eager runs per geometry before capture
-  // step chain (chain.cu): global TMA descriptors, completion counters
-  CUtensorMap* chain_maps = nullptr;
-  int* chain_done = nullptr;
-  bool fused_head = false;  // final norm + LM head + argmax in one kernel (vocab <= 256)
-  bool chain_on = false;  // small Thinker steps (rows <= 16) as one step-chain launch (OMNI_CHAIN=1)
-  unsigned long long* chain_trace = nullptr;  // tools: per-ticket timestamps
-  int chain_last_items = 0, chain_last_nops = 0;
-  int chain_last_first[omni_dev::kChainMaxOps] = {};
-
 };

@@ -34,13 +34,14 @@ uint32_t mix(uint32_t h, uint32_t t) { return h * 1000003u + t + 1u; }  // refer
 // released when the request leaves the pipeline (connector cleanup).
 class Arena {
  public:
-  Arena(int dev, uint64_t bytes) : bytes_(bytes) {
+  Arena(int dev, uint64_t bytes) : dev_(dev), bytes_(bytes) {
     dev_ok(omni_arena_create(dev, bytes, &arena_), "omni_arena_create");
     dev_ok(omni_arena_base(arena_, &base_, nullptr), "omni_arena_base");
     free_[0] = bytes;
   }
   ~Arena() { omni_arena_destroy(arena_); }
   uint64_t base() const { return base_; }
+  int device() const { return dev_; }
   uint64_t alloc(uint64_t rid, uint64_t n) {
     n = (n + 255) & ~uint64_t(255);
     for (auto it = free_.begin(); it != free_.end(); ++it) {
@@ -75,6 +76,7 @@ class Arena {
 
  private:
   omni_arena* arena_ = nullptr;
+  int dev_ = 0;
   uint64_t base_ = 0, bytes_ = 0;
   std::map<uint64_t, uint64_t> free_;
   std::unordered_map<uint64_t, std::vector<std::pair<uint64_t, uint64_t>>> owned_;
@@ -109,14 +111,17 @@ struct HostTimer {
 };
 
 struct ArStage {
-  std::string name;
+  std::string name;  // forward name (trace lines); the registry key adds "#r" for replicas
   int kind = OMNI_MODEL_THINKER;
   int dev = 0;
   omni_model_desc model{};
   omni_stage* st = nullptr;
   bool pack_hidden = false;  // thinker_forward: FIX16 device chunks
-  std::unique_ptr<Arena> arena;
-  ArStage* upstream = nullptr;  // talker: the stage whose arena it reads
+  // thinker: the connector arena of each consumer (talker) replica, indexed
+  // by replica_for(rid, n) -- the same router the orchestrator admits with,
+  // so a request's rows land on the GPU of the talker replica that reads them
+  std::vector<Arena*> dst_arenas;
+  std::vector<ArStage*> upstreams;  // talker: every thinker replica that packs into its arena
   Tracer* tracer = nullptr;
   // parity capture (tests): thinker hidden rows per request, [index][d] bf16 bits
   std::map<uint64_t, std::vector<uint16_t>>* capture = nullptr;
@@ -132,7 +137,7 @@ struct ArStage {
   struct Pack {
     uint64_t rid;
     int32_t begin, end;
-    uint64_t offset;
+    uint64_t offset;  // absolute device address of the blob
   };
   std::vector<Pack> packs;
   std::vector<int32_t> pack_tokens;
@@ -187,7 +192,10 @@ struct ArStage {
         tracer->out += "D " + name + " " + std::to_string(tracer->now()) + " " + std::to_string(b.request_id) +
                        " " + std::to_string(b.out_index) + "\n";
     }
-    if (reads_rows && upstream) dev_ok(omni_stage_after(st, upstream->st), "omni_stage_after");
+    // order this step after the packs that wrote its rows (possibly on other
+    // GPUs) -- only the packs, not the producers' later steps
+    if (reads_rows)
+      for (ArStage* up : upstreams) dev_ok(omni_stage_after_pack(st, up->st), "omni_stage_after_pack");
     omni_ar_batch batch{};
     batch.n_entries = static_cast<int32_t>(n);
     batch.seq_id = seq_id.data();
@@ -246,13 +254,14 @@ struct ArStage {
     if (!pack_hidden) return Payload::from_i32(std::span<const int32_t>(s.emitted.data() + b, e - b));
     const int32_t rows = static_cast<int32_t>(e - b);
     const uint64_t nbytes = omni_pack_bytes(rows, model.d_model);
-    const uint64_t off = arena->alloc(s.request_id, nbytes);
-    packs.push_back({s.request_id, static_cast<int32_t>(b), static_cast<int32_t>(e), off});
+    Arena* arena = dst_arenas.at(replica_for(s.request_id, dst_arenas.size()));
+    const uint64_t addr = arena->base() + arena->alloc(s.request_id, nbytes);
+    packs.push_back({s.request_id, static_cast<int32_t>(b), static_cast<int32_t>(e), addr});
     Payload p;
     p.dtype = Dtype::FIX16;
     p.shape = {static_cast<uint32_t>(rows), static_cast<uint32_t>(model.d_model + 1)};
-    p.dev.device = dev;
-    p.dev.blob = arena->base() + off;
+    p.dev.device = arena->device();
+    p.dev.blob = addr;
     p.dev.nbytes = nbytes;
     p.host_tokens.assign(s.emitted.begin() + static_cast<std::ptrdiff_t>(b),
                          s.emitted.begin() + static_cast<std::ptrdiff_t>(e));
@@ -270,103 +279,74 @@ struct ArStage {
       e.push_back(p.end);
       off.push_back(p.offset);
     }
+    // absolute destinations (dst_base 0): one launch may write several
+    // consumer GPUs' arenas (remote stores over NVLink)
     dev_ok(omni_pack_hidden(st, static_cast<int32_t>(packs.size()), sid.data(), b.data(), e.data(),
-                            pack_tokens.data(), arena->base(), off.data()),
+                            pack_tokens.data(), 0, off.data()),
            "omni_pack_hidden");
     packs.clear();
     pack_tokens.clear();
   }
 };
 
-// The DiT plugin. One diffusion iteration's jobs (diffusion_engine.hpp:84-112)
-// are split into `ways` token-balanced groups, each run as its own batched
-// omni_dit_step on its own device stage (stream): the denoise chain of a
-// batch is latency-bound (~130 dependent kernels), so parallel chains fill
-// the SMs one chain leaves idle. The DiT is token-local and batch-invariant,
-// so the samples are bit-identical for any grouping (test_dit_parity_and_
-// chunking). OMNI_DIT_WAYS sets the group count; default 1 (2 and 3 measured
-// no better in the bench, profiles/r01_bench_ditways_ab.log).
+// The DiT plugin: one diffusion iteration's jobs (diffusion_engine.hpp:84-112)
+// become ONE batched omni_dit_step. The DiT is token-local and batch-
+// invariant, so samples are bit-identical for any batching / chunking
+// (test_dit_parity_and_chunking).
 struct DitStage {
   std::string name;
   int dev = 0;
   omni_model_desc model{};
-  std::vector<omni_stage*> sts;
+  omni_stage* st = nullptr;
   Tracer* tracer = nullptr;
-  struct Group {
-    std::vector<size_t> jobs;  // indices into the launched job list
-    std::vector<uint64_t> rid;
-    std::vector<int32_t> off, ntok, tokens, samples;
-  };
-  std::vector<Group> groups;
-  std::vector<size_t> job_ntok;
+  std::vector<uint64_t> rid;
+  std::vector<int32_t> off, ntok, tokens, samples;
   double dev_ms = 0;
   uint64_t steps = 0;
   HostTimer ht;
   ~DitStage() {
-    for (omni_stage* st : sts) omni_stage_destroy(st);
+    if (st) omni_stage_destroy(st);
   }
   void launch(const std::vector<DiffusionJob>& jobs) {
     HostTimer::Scope hs(ht);
-    groups.assign(sts.size(), Group{});
-    job_ntok.assign(jobs.size(), 0);
-    std::vector<size_t> load(sts.size(), 0);
-    for (size_t i = 0; i < jobs.size(); ++i) {
-      const auto& j = jobs[i];
+    rid.clear(), off.clear(), ntok.clear(), tokens.clear();
+    for (const auto& j : jobs) {
       if (j.input.dtype != Dtype::I32 || j.input.is_device())
         throw BadDtype("diffusion input must be I32 codec tokens");
       const auto t = j.input.as_i32();
-      const size_t g = std::min_element(load.begin(), load.end()) - load.begin();  // token-balanced
-      load[g] += t.size() + 1;
-      Group& G = groups[g];
-      G.jobs.push_back(i);
-      G.rid.push_back(j.request_id);
-      G.off.push_back(static_cast<int32_t>(j.token_offset));
-      G.ntok.push_back(static_cast<int32_t>(t.size()));
-      G.tokens.insert(G.tokens.end(), t.begin(), t.end());
-      job_ntok[i] = t.size();
+      rid.push_back(j.request_id);
+      off.push_back(static_cast<int32_t>(j.token_offset));
+      ntok.push_back(static_cast<int32_t>(t.size()));
+      tokens.insert(tokens.end(), t.begin(), t.end());
     }
-    for (size_t g = 0; g < groups.size(); ++g) {
-      Group& G = groups[g];
-      if (G.jobs.empty()) continue;
-      G.samples.assign(G.tokens.size() * static_cast<size_t>(model.dit_samples), 0);
-      omni_dit_batch b{};
-      b.n_jobs = static_cast<int32_t>(G.jobs.size());
-      b.request_id = G.rid.data();
-      b.token_offset = G.off.data();
-      b.n_tokens = G.ntok.data();
-      b.tokens = G.tokens.data();
-      dev_ok(omni_dit_step(sts[g], &b, G.samples.data()), "omni_dit_step");
-    }
+    samples.assign(tokens.size() * static_cast<size_t>(model.dit_samples), 0);
+    omni_dit_batch b{};
+    b.n_jobs = static_cast<int32_t>(jobs.size());
+    b.request_id = rid.data();
+    b.token_offset = off.data();
+    b.n_tokens = ntok.data();
+    b.tokens = tokens.data();
+    dev_ok(omni_dit_step(st, &b, samples.data()), "omni_dit_step");
   }
   bool ready() {
-    for (size_t g = 0; g < groups.size(); ++g) {
-      if (groups[g].jobs.empty()) continue;
-      const omni_status s = omni_stage_query(sts[g]);
-      if (s == OMNI_EAGAIN) return false;
-      dev_ok(s, "omni_stage_query");
-    }
+    const omni_status s = omni_stage_query(st);
+    if (s == OMNI_EAGAIN) return false;
+    dev_ok(s, "omni_stage_query");
     return true;
   }
   std::vector<Payload> collect() {
-    float worst = 0;
-    for (size_t g = 0; g < groups.size(); ++g) {
-      if (groups[g].jobs.empty()) continue;
-      dev_ok(omni_stage_wait(sts[g]), "omni_stage_wait");
-      float us = 0;
-      omni_stage_last_step_us(sts[g], &us);
-      worst = std::max(worst, us);
-    }
+    dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    float us = 0;
+    omni_stage_last_step_us(st, &us);
     ht.ready();
-    dev_ms += worst / 1e3;  // concurrent groups: the iteration lasts as long as the slowest
+    dev_ms += us / 1e3;
     ++steps;
-    std::vector<Payload> out(job_ntok.size());
-    for (const Group& G : groups) {
-      size_t at = 0;
-      for (size_t k = 0; k < G.jobs.size(); ++k) {
-        const size_t m = static_cast<size_t>(G.ntok[k]) * model.dit_samples;
-        out[G.jobs[k]] = Payload::from_i32(std::span<const int32_t>(G.samples.data() + at, m));
-        at += m;
-      }
+    std::vector<Payload> out(ntok.size());
+    size_t at = 0;
+    for (size_t k = 0; k < ntok.size(); ++k) {
+      const size_t m = static_cast<size_t>(ntok[k]) * model.dit_samples;
+      out[k] = Payload::from_i32(std::span<const int32_t>(samples.data() + at, m));
+      at += m;
     }
     return out;
   }
@@ -399,36 +379,57 @@ omni_model_desc model_for(int kind, bool small) {
 struct B200Pipeline::Impl {
   B200Options opt;
   std::map<uint64_t, std::vector<uint16_t>> captured;
+  // keyed by registry name: the forward name for replica 0, "name#r" after
   std::map<std::string, std::unique_ptr<ArStage>> ar;
   std::map<std::string, std::unique_ptr<DitStage>> dit;
+  std::map<int, std::unique_ptr<Arena>> arenas;  // connector arena per consumer GPU
   Tracer* tracer = nullptr;
 
-  int device_of(const std::string& name) const {
-    auto it = opt.device.find(name);
-    return it == opt.device.end() ? 0 : it->second;
+  std::vector<int> devices_of(const std::string& name) const {
+    auto it = opt.devices.find(name);
+    return it == opt.devices.end() || it->second.empty() ? std::vector<int>{0} : it->second;
   }
   EngineConfig engine_of(const std::string& name) const {
     auto it = opt.engines.find(name);
     return it == opt.engines.end() ? EngineConfig{} : it->second;
   }
+  Arena& arena_on(int dev) {
+    auto& a = arenas[dev];
+    if (!a) a = std::make_unique<Arena>(dev, opt.arena_bytes);
+    return *a;
+  }
 
-  ArStage& make_ar(const std::string& name, int kind, uint64_t seed_salt) {
-    auto s = std::make_unique<ArStage>();
-    s->name = name;
-    s->kind = kind;
-    s->dev = device_of(name);
-    s->model = model_for(kind, opt.small_models);
+  std::vector<ArStage*> make_ar(const std::string& name, int kind, uint64_t seed_salt) {
+    std::vector<ArStage*> out;
+    const std::vector<int> devs = devices_of(name);
     const EngineConfig ec = engine_of(name);
-    omni_stage_limits lim{};
-    lim.max_batch_tokens = static_cast<int32_t>(std::max<uint64_t>(ec.max_batch_tokens, 16));
-    lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
-    // thinker: prompt (<= kv budget, capped) + up to 64 outputs; talker: <= 64 rows + 4x codec
-    lim.max_seq_len = kind == OMNI_MODEL_TALKER ? 64 + 256 + 16
-                                                : static_cast<int32_t>(std::min<uint64_t>(ec.kv_budget_tokens, 448) + 64);
-    dev_ok(omni_stage_create(&s->model, &lim, s->dev, opt.weight_seed + seed_salt, &s->st), "omni_stage_create");
-    auto& ref = *s;
-    ar[name] = std::move(s);
-    return ref;
+    for (size_t r = 0; r < devs.size(); ++r) {
+      auto s = std::make_unique<ArStage>();
+      s->name = name;
+      s->kind = kind;
+      s->dev = devs[r];
+      s->model = model_for(kind, opt.small_models);
+      omni_stage_limits lim{};
+      lim.max_batch_tokens = static_cast<int32_t>(std::max<uint64_t>(ec.max_batch_tokens, 16));
+      lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
+      if (kind == OMNI_MODEL_TALKER) {
+        // prompt = the Thinker's text (<= 64 rows) + 4 codec tokens per row
+        lim.max_seq_len = 64 + 256 + 16;
+      } else {
+        // any prompt the engine admits (<= kv_budget_tokens, ar_engine.hpp:66-70)
+        // plus up to 64 generated tokens (target_length, reference_pipeline.hpp:
+        // 30-32); the page pool holds the kv budget plus the decode overrun the
+        // schedule allows (a sole resident, one token per decoder per step)
+        lim.max_seq_len = static_cast<int32_t>(ec.kv_budget_tokens + 64);
+        const uint64_t tokens = ec.kv_budget_tokens + 64 + 2 * ec.max_resident_requests;
+        lim.kv_pages = static_cast<int32_t>((tokens + 15) / 16 + ec.max_resident_requests);
+      }
+      // identical weights on every replica (same seed)
+      dev_ok(omni_stage_create(&s->model, &lim, s->dev, opt.weight_seed + seed_salt, &s->st), "omni_stage_create");
+      out.push_back(s.get());
+      ar[replica_name(name, r)] = std::move(s);
+    }
+    return out;
   }
 };
 
@@ -438,46 +439,50 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
   if (omni_device_count(&n) != OMNI_OK || n == 0)
     throw DeviceError("no CUDA device: the B200 pipeline has no CPU fallback");
   std::vector<int32_t> devs;
-  for (const auto& [_, d] : impl_->opt.device) devs.push_back(d);
+  for (const auto& [_, v] : impl_->opt.devices) devs.insert(devs.end(), v.begin(), v.end());
+  if (devs.empty()) devs.push_back(0);
   std::sort(devs.begin(), devs.end());
   devs.erase(std::unique(devs.begin(), devs.end()), devs.end());
+  for (int d : devs)
+    if (d < 0 || d >= n)
+      throw ConfigInvalid("placement names cuda:" + std::to_string(d) + " but " + std::to_string(n) +
+                          " device(s) are visible");
   dev_ok(omni_init(static_cast<int32_t>(devs.size()), devs.data()), "omni_init");
   auto& I = *impl_;
   auto want = [&I](const std::string& n) { return I.opt.needed.empty() || I.opt.needed.count(n) != 0; };
   // weight seeds: thinker / ar share the thinker model family, talker and DiT own seeds
-  ArStage* th = nullptr;
+  std::vector<ArStage*> thinkers, talkers;
   if (want("thinker_forward") || want("talker_forward")) {
-    th = &I.make_ar("thinker_forward", OMNI_MODEL_THINKER, 0);
-    th->pack_hidden = true;
+    thinkers = I.make_ar("thinker_forward", OMNI_MODEL_THINKER, 0);
+    for (ArStage* t : thinkers) t->pack_hidden = true;
   }
   if (want("talker_forward")) {
-    ArStage& ta = I.make_ar("talker_forward", OMNI_MODEL_TALKER, 1);
-    ta.upstream = th;
+    talkers = I.make_ar("talker_forward", OMNI_MODEL_TALKER, 1);
+    for (ArStage* t : talkers) t->upstreams = thinkers;
   }
-  if (th) th->arena = std::make_unique<Arena>(I.device_of("talker_forward"), I.opt.arena_bytes);
+  // connector arenas live on the consumer's GPU; with no talker in the graph
+  // the thinker's chunks stay on its own GPU
+  std::vector<Arena*> dst;
+  for (ArStage* t : talkers) dst.push_back(&I.arena_on(t->dev));
+  for (ArStage* t : thinkers) t->dst_arenas = dst.empty() ? std::vector<Arena*>{&I.arena_on(t->dev)} : dst;
   if (want("ar_forward")) I.make_ar("ar_forward", OMNI_MODEL_THINKER, 0);
   for (const char* dn : {"denoise", "dit_image"}) {
     if (!want(dn)) continue;
-    auto d = std::make_unique<DitStage>();
-    d->name = dn;
-    d->dev = I.device_of(dn);
-    d->model = model_for(OMNI_MODEL_DIT, I.opt.small_models);
+    const std::vector<int> ddevs = I.devices_of(dn);
     const EngineConfig ec = I.engine_of(dn);
-    omni_stage_limits lim{};
-    lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
-    lim.dit_max_tokens = 512;
-    static const int ways = [] {
-      const char* e = std::getenv("OMNI_DIT_WAYS");
-      return std::clamp(e ? std::atoi(e) : 1, 1, 4);
-    }();
-    for (int w = 0; w < ways; ++w) {  // identical weights (same seed) on every group's stage
-      omni_stage* st = nullptr;
+    for (size_t r = 0; r < ddevs.size(); ++r) {
+      auto d = std::make_unique<DitStage>();
+      d->name = dn;
+      d->dev = ddevs[r];
+      d->model = model_for(OMNI_MODEL_DIT, I.opt.small_models);
+      omni_stage_limits lim{};
+      lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
+      lim.dit_max_tokens = 512;
       dev_ok(omni_stage_create(&d->model, &lim, d->dev, I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3),
-                               &st),
+                               &d->st),
              "omni_stage_create(dit)");
-      d->sts.push_back(st);
+      I.dit[replica_name(dn, r)] = std::move(d);
     }
-    I.dit[dn] = std::move(d);
   }
 }
 
@@ -498,22 +503,31 @@ void B200Pipeline::set_tracer(Tracer* t) {
   for (auto& [_, s] : impl_->dit) s->tracer = t;
 }
 
+// Per forward name, summed over replicas (device busy time, steps); the
+// host-gap figure is the mean over the replicas' steps.
 std::map<std::string, double> B200Pipeline::device_ms() const {
   std::map<std::string, double> m;
-  for (const auto& [n, s] : impl_->ar) m[n] = s->dev_ms;
-  for (const auto& [n, s] : impl_->dit) m[n] = s->dev_ms;
+  for (const auto& [_, s] : impl_->ar) m[s->name] += s->dev_ms;
+  for (const auto& [_, s] : impl_->dit) m[s->name] += s->dev_ms;
   return m;
 }
 std::map<std::string, std::pair<double, double>> B200Pipeline::host_ms() const {
   std::map<std::string, std::pair<double, double>> m;
-  for (const auto& [n, s] : impl_->ar) m[n] = {s->ht.host_ms, s->ht.gaps ? s->ht.gap_ms / s->ht.gaps : 0.0};
-  for (const auto& [n, s] : impl_->dit) m[n] = {s->ht.host_ms, s->ht.gaps ? s->ht.gap_ms / s->ht.gaps : 0.0};
+  std::map<std::string, std::pair<double, uint64_t>> gaps;
+  auto add = [&](const std::string& n, const HostTimer& h) {
+    m[n].first += h.host_ms;
+    gaps[n].first += h.gap_ms;
+    gaps[n].second += h.gaps;
+  };
+  for (const auto& [_, s] : impl_->ar) add(s->name, s->ht);
+  for (const auto& [_, s] : impl_->dit) add(s->name, s->ht);
+  for (auto& [n, v] : m) v.second = gaps[n].second ? gaps[n].first / gaps[n].second : 0.0;
   return m;
 }
 std::map<std::string, uint64_t> B200Pipeline::step_counts() const {
   std::map<std::string, uint64_t> m;
-  for (const auto& [n, s] : impl_->ar) m[n] = s->steps;
-  for (const auto& [n, s] : impl_->dit) m[n] = s->steps;
+  for (const auto& [_, s] : impl_->ar) m[s->name] += s->steps;
+  for (const auto& [_, s] : impl_->dit) m[s->name] += s->steps;
   return m;
 }
 uint64_t B200Pipeline::weight_bytes() const {
@@ -521,7 +535,7 @@ uint64_t B200Pipeline::weight_bytes() const {
   for (const auto& [_, s] : impl_->ar)
     if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
   for (const auto& [_, s] : impl_->dit)
-    if (!s->sts.empty() && omni_stage_weight_bytes(s->sts[0], &b) == OMNI_OK) t += b;
+    if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
   return t;
 }
 void B200Pipeline::reset_counters() {
@@ -548,11 +562,14 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
                          " " + std::to_string(s.target_len) + "\n";
     };
   };
-  for (auto& [name, sp] : I.ar) {
+  for (auto& [key, sp] : I.ar) {
     ArStage* s = sp.get();
     StageModel m;
-    m.prefill = trace_prefill(name);
-    m.on_prompt_consumed = trace_consumed(name, s->kind == OMNI_MODEL_TALKER);
+    m.prefill = trace_prefill(s->name);
+    m.on_prompt_consumed = trace_consumed(s->name, s->kind == OMNI_MODEL_TALKER);
+    m.reserve = [s](const BatchSlot& b) {
+      dev_ok(omni_seq_reserve(s->st, b.request_id, static_cast<int32_t>(b.pos0 + b.span)), "omni_seq_reserve");
+    };
     m.pack_chunk = [s](const SeqState& q, size_t b, size_t e) { return s->pack_chunk(q, b, e); };
     m.launch_batch = [s](std::vector<BatchSlot>& slots) { s->launch(slots); };
     m.batch_ready = [s] { return s->ready(); };
@@ -560,9 +577,9 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
     m.release = [s](uint64_t rid) { dev_ok(omni_seq_release(s->st, rid), "omni_seq_release"); };
     m.flush = [s] { s->flush(); };
     m.cleanup = [s](uint64_t rid) {
-      if (s->arena) s->arena->release(rid);
+      for (Arena* a : s->dst_arenas) a->release(rid);  // idempotent; arenas may be shared
     };
-    reg.register_forward(name, std::move(m));
+    reg.register_forward(key, std::move(m));
   }
 
   // Talker preprocess over device chunks: same READY/STALL rule as the
@@ -613,13 +630,13 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
   // branching graphs (BASELINE config 5): Thinker text ids -> image DiT
   reg.register_transfer("Thinker2Image", [](TransferEnv& env) { env.wire_diffusion({4, 16}); });
 
-  for (auto& [name, dp] : I.dit) {
+  for (auto& [key, dp] : I.dit) {
     DitStage* d = dp.get();
     DiffusionModel dm;
     dm.launch_batch = [d](const std::vector<DiffusionJob>& jobs) { d->launch(jobs); };
     dm.batch_ready = [d] { return d->ready(); };
     dm.collect_batch = [d] { return d->collect(); };
-    reg.register_denoiser(name, std::move(dm));
+    reg.register_denoiser(key, std::move(dm));
   }
 }
 

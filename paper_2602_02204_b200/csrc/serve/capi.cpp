@@ -80,7 +80,8 @@ omni_status omni_pipeline_create(const char* config_json, const omni_pipeline_op
     for (const auto& n : p->plan.graph.nodes) {
       const std::string fn = n.kind == omni::StageKind::AR ? n.forward_ref
                                                            : (n.forward_ref.empty() ? "denoise" : n.forward_ref);
-      o.device[fn] = dev;
+      // the plan's placement (stage -> "cuda:N[,cuda:M...]"), else opts->device
+      o.devices[fn] = omni::placement_devices(p->plan, n.id, dev);
       o.engines[fn] = p->plan.engines.at(n.id);
       o.needed.insert(fn);
     }

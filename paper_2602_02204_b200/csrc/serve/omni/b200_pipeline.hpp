@@ -26,7 +26,9 @@ struct Tracer {
 
 struct B200Options {
   uint64_t weight_seed = 1234;
-  std::map<std::string, int> device;       // forward / denoiser name -> CUDA ordinal
+  // forward / denoiser name -> CUDA ordinals of its replicas (placement;
+  // one engine + one device stage per entry, routed by replica_for)
+  std::map<std::string, std::vector<int>> devices;
   bool small_models = false;               // reduced dims (tests)
   uint64_t arena_bytes = 256ull << 20;     // hidden-state connector arena per producer
   std::map<std::string, EngineConfig> engines;  // stage limits keyed by forward name

@@ -91,6 +91,10 @@ void Orchestrator::validate_plan() {
     if (n.kind == StageKind::DIFFUSION && !plan_.graph.edges_from(n.id).empty())
       throw ConfigInvalid("diffusion stage " + n.id + " cannot have outgoing edges");
   }
+  for (const auto& [stage, _] : plan_.placement) {
+    if (!plan_.graph.find_node(stage)) throw ConfigInvalid("placement names unknown stage " + stage);
+    placement_devices(plan_, stage);  // throws ConfigInvalid on a malformed device list
+  }
   std::set<std::string> endpoints;
   for (const auto& e : plan_.graph.edges) {
     auto it = plan_.transports.find(e.key());

@@ -88,8 +88,16 @@ class Stage:
         check(self.lib.omni_stage_tensor(self.h, name.encode(), C.byref(p), C.byref(r), C.byref(c)))
         return p.value, r.value, c.value
 
-    def set_chain(self, on: bool) -> None:
-        check(self.lib.omni_stage_set_chain(self.h, 1 if on else 0))
+    def set_sampling(self, top_k: int, seed: int = 0) -> None:
+        """Greedy (top_k <= 1) or top-k sampling of decode rows (omni_stage_set_sampling)."""
+        check(self.lib.omni_stage_set_sampling(self.h, top_k, C.c_uint64(seed)))
+
+    def reserve(self, seq_id: int, upto_tokens: int) -> None:
+        check(self.lib.omni_seq_reserve(self.h, C.c_uint64(seq_id), upto_tokens))
+
+    def after_pack(self, producer: "Stage") -> None:
+        """This stage's next step waits for the producer's last connector pack."""
+        check(self.lib.omni_stage_after_pack(self.h, producer.h))
 
     def weight_bytes(self) -> int:
         b = C.c_uint64()

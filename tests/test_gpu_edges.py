@@ -12,6 +12,7 @@ restated for the device path):
 import numpy as np
 import pytest
 
+import oracle
 from paper_2602_02204_b200 import dev as D
 from paper_2602_02204_b200._native import OmniError
 
@@ -124,83 +125,78 @@ def test_kv_pool_exhaustion_is_oom():
     st.close()
 
 
-@pytest.mark.parametrize("kind", [D.THINKER])
-def test_step_chain_bit_identical_to_kernel_chain(kind):
-    """The one-launch step chain (chain.cu) and the per-kernel PDL path give
-    bit-identical tokens and hidden rows (same tiles, same split-K order)."""
-    kw = dict(SMALL)
-    if kind == D.TALKER:
-        kw["cond_dim"] = 512
-    m = D.model_default(kind, **kw)
-    rng = np.random.default_rng(11)
-    prompts = {s: list(rng.integers(1, 256, size=n)) for s, n in ((1, 9), (2, 14), (3, 5))}
-    outs = []
-    for chain in (True, False):
-        st = D.Stage(m, D.StageLimits(256, 16, 256, 0, 16), seed=17)
-        st.set_chain(chain)
-        cond = None
-        if kind == D.TALKER:
-            cond = D.mem_alloc(2 * 512 * 16)
-            bits = ((rng.standard_normal(512 * 16).astype(np.float32) * 0.5).view(np.uint32) >> 16).astype(np.uint16)
-            D.h2d(cond, bits)
-        for s, p in prompts.items():
-            if kind == D.TALKER:
-                st.ar_step([s], [D.PREFILL], [len(p)], [0], [-1], p,
-                           cond_src=[cond + 2 * 512 * (j % 16) for j in range(len(p))],
-                           cond_row=list(range(len(p))))
-            else:
-                st.ar_step([s], [D.PREFILL], [len(p)], [0], [-1], p)
-        seqs = sorted(prompts)
-        toks = {s: [] for s in seqs}
-        hids = []
-        for k in range(4):
-            tin = [-1 if k == 0 else toks[s][-1] for s in seqs]
-            pos = [len(prompts[s]) + k for s in seqs]
-            extra = dict(cond_src=[0] * 3, cond_row=[k // 4] * 3) if kind == D.TALKER else {}
-            t, mg = st.ar_step(seqs, [D.DECODE] * 3, [1] * 3, pos, [k] * 3, tin, **extra)
-            for i, s in enumerate(seqs):
-                toks[s].append(int(t[i]))
-            if kind == D.THINKER:
-                hids.append(np.stack([D.d2h(st.hidden_row(s, k), (512,), np.uint16) for s in seqs]))
-            else:
-                lg = D.d2h(st.tensor("buf.logits")[0], (3, st.tensor("buf.logits")[2]), np.float32)
-                hids.append(lg[:, :m.vocab])  # columns >= vocab are padding (never written)
-        outs.append((toks, hids))
-        st.close()
-    assert outs[0][0] == outs[1][0]
-    for a, b in zip(outs[0][1], outs[1][1]):
-        assert np.array_equal(a, b)
+def _sample_ref(logits, lo, hi, k, seed, rid, index):
+    """numpy restatement of sample_row (ar_dev.cuh): top-k of [lo, hi), softmax
+    at temperature 1, u = sample_hash(seed, key(rid), index) * sum."""
+    ids = np.arange(lo, hi)
+    v = logits[lo:hi].astype(np.float64)
+    order = np.lexsort((ids, -v))[:k]          # descending logit, ties -> lowest id
+    top = v[order]
+    p = np.exp(top - top[0])
+    c = np.cumsum(p)
+    key = oracle.mix64(rid) & 0xFFFFFFFF
+    h = oracle.sample_hash(seed, key, index)
+    u = (h >> 40) / 16777216.0 * c[-1]
+    j = int(np.argmax(c > u)) if np.any(c > u) else k - 1
+    # a draw within float rounding of a cumulative boundary may legitimately
+    # land on the neighbour (fp32 prefix sum on the GPU)
+    near = np.any(np.abs(c - u) <= 1e-5 * c[-1])
+    return int(ids[order][j]), set(int(x) for x in ids[order]), near
 
 
-def test_fused_head_matches_kernel_head(monkeypatch):
-    """OMNI_FUSED_HEAD=1 (final norm + CUDA-core LM head + argmax in one
-    kernel, split over CTAs with a last-CTA argmax) gives the same tokens and
-    bit-identical hidden rows as final_gather + tcgen05 LM GEMM + argmax;
-    logits agree to fp32 summation-order tolerance."""
+def test_topk_sampler_matches_restatement_and_is_batch_invariant():
+    """omni_stage_set_sampling(top_k=8): every drawn id lies in the row's
+    top-8, equals the numpy restatement of the sampler on the GPU's own
+    logits, and a sequence redraws the SAME ids when replayed in a different
+    batch (the draw is keyed by request id + emitted index, not by row)."""
     m = D.model_default(D.THINKER, **SMALL)
-    rng = np.random.default_rng(21)
-    prompts = {s: list(rng.integers(1, 256, size=n)) for s, n in ((1, 7), (2, 12), (3, 20), (4, 3))}
-    outs = []
-    for fused in ("1", "0"):
-        monkeypatch.setenv("OMNI_FUSED_HEAD", fused)
-        st = D.Stage(m, D.StageLimits(256, 16, 256, 0, 16), seed=23)
-        for s, p in prompts.items():
-            st.ar_step([s], [D.PREFILL], [len(p)], [0], [-1], p)
-        seqs = sorted(prompts)
-        toks = {s: [] for s in seqs}
-        hids, lgs = [], []
-        for k in range(6):  # repeated steps replay the self-resetting CTA tickets
-            tin = [-1 if k == 0 else toks[s][-1] for s in seqs]
-            t, _ = st.ar_step(seqs, [D.DECODE] * 4, [1] * 4, [len(prompts[s]) + k for s in seqs], [k] * 4, tin)
-            for i, s in enumerate(seqs):
+    rng = np.random.default_rng(31)
+    prompts = {s: list(rng.integers(1, 256, size=n)) for s, n in ((3, 11), (5, 6), (8, 17))}
+    st = D.Stage(m, D.StageLimits(256, 16, 256, 0, 16), seed=37)
+    st.set_sampling(8, 4242)
+    runs = []
+    for batch in (sorted(prompts), [5]):
+        for s in batch:
+            st.ar_step([s], [D.PREFILL], [len(prompts[s])], [0], [-1], prompts[s])
+        toks = {s: [] for s in batch}
+        for k in range(6):
+            tin = [-1 if k == 0 else toks[s][-1] for s in batch]
+            t, mg = st.ar_step(batch, [D.DECODE] * len(batch), [1] * len(batch),
+                               [len(prompts[s]) + k for s in batch], [k] * len(batch), tin)
+            lg_p, _, ld = st.tensor("buf.logits")
+            lg = D.d2h(lg_p, (len(batch), ld), np.float32)
+            for i, s in enumerate(batch):
+                want, topset, near = _sample_ref(lg[i], 1, 256, 8, 4242, s, k)
+                assert int(t[i]) in topset
+                if not near:
+                    assert int(t[i]) == want, (s, k, int(t[i]), want)
                 toks[s].append(int(t[i]))
-            hids.append(np.stack([D.d2h(st.hidden_row(s, k), (512,), np.uint16) for s in seqs]))
-            lg = st.tensor("buf.logits")
-            lgs.append(D.d2h(lg[0], (4, lg[2]), np.float32)[:, :m.vocab])
-        outs.append((toks, hids, lgs))
-        st.close()
-    assert outs[0][0] == outs[1][0]
-    for a, b in zip(outs[0][1], outs[1][1]):
-        assert np.array_equal(a, b)
-    for a, b in zip(outs[0][2], outs[1][2]):
-        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-4)
+        for s in batch:
+            st.release(s)
+        runs.append(toks)
+    assert runs[0][5] == runs[1][5], "top-k draws depend on the batch"
+    # greedy again: top_k 1 == argmax
+    st.set_sampling(1, 0)
+    st.ar_step([9], [D.PREFILL], [4], [0], [-1], [1, 2, 3, 4])
+    t, _ = st.ar_step([9], [D.DECODE], [1], [4], [0], [-1])
+    lg = D.d2h(st.tensor("buf.logits")[0], (256,), np.float32)
+    assert int(t[0]) == 1 + int(np.argmax(lg[1:256]))
+    st.close()
+
+
+def test_per_entry_reserve_fails_alone():
+    """omni_seq_reserve admits a sequence's KV pages ahead of the batched
+    step: one sequence that does not fit gets OMNI_E_OOM by itself while the
+    others still run (the reference fails per entry, ar_engine.hpp:332-334)."""
+    m = D.model_default(D.THINKER, **SMALL)
+    st = D.Stage(m, D.StageLimits(256, 4, 64, 6, 16), seed=3)  # 6 pages of 16 tokens
+    st.reserve(1, 48)   # 3 pages
+    st.reserve(2, 32)   # 2 pages
+    with pytest.raises(RuntimeError) as e:
+        st.reserve(3, 40)  # needs 3, one left
+    assert "E_OOM" in str(e.value)
+    st.reserve(3, 16)      # fits
+    t, _ = st.ar_step([1, 2], [D.PREFILL, D.PREFILL], [8, 8], [0, 0], [-1, -1], [5] * 16)
+    for s in (1, 2, 3):
+        st.release(s)
+    st.close()

@@ -130,3 +130,41 @@ def test_full_size_omni3_device():
                                                   "dev_ms_thinker", "dev_ms_talker", "dev_ms_dit",
                                                   "steps_thinker", "steps_talker", "steps_dit", "wall_s")})
     p.close()
+
+
+def test_replicated_placement_same_outputs():
+    """Stage placement with replicas on the GPUs this box has:
+    Thinker x2, Talker x3, Code2Wav x2. On a 1-GPU box every replica lands on
+    cuda:0 (own streams, own KV pools, shared connector arena), which still
+    exercises the router, per-request connector arenas, absolute-address packs
+    and the pack-event ordering across producer replicas. Outputs must be
+    byte-identical to the single-replica pipeline (batch invariance)."""
+    import json
+    from paper_2602_02204_b200 import dev as D
+    import ctypes
+    n = ctypes.c_int32()
+    D.dev_lib().omni_device_count(ctypes.byref(n))
+    devs = [f"cuda:{i % n.value}" for i in range(8)]
+    text = (ROOT / "configs" / "omni3.json").read_text()
+    base = Pipeline(text, weight_seed=11, small_models=True)
+    r0 = base.bench(n=24, seed=5, concurrency=8, clock="device")
+    base.close()
+    cfg = json.loads(text)
+    cfg["placement"] = {"thinker": ",".join(devs[0:2]), "talker": ",".join(devs[2:5]),
+                        "vocoder": ",".join(devs[5:7])}
+    p = Pipeline(json.dumps(cfg), weight_seed=11, small_models=True)
+    r1 = p.bench(n=24, seed=5, concurrency=8, clock="device")
+    v = p.bench(n=24, seed=5, concurrency=8, clock="virtual")
+    p.close()
+    assert r0["completed"] == r1["completed"] == v["completed"] == 24
+    assert r0["output_digest"] == r1["output_digest"] == v["output_digest"]
+
+
+def test_placement_beyond_visible_devices_is_rejected():
+    import json
+    from paper_2602_02204_b200._native import OmniError
+    cfg = json.loads((ROOT / "configs" / "omni3.json").read_text())
+    cfg["placement"] = {"talker": "cuda:0,cuda:63"}
+    with pytest.raises(OmniError) as e:
+        Pipeline(json.dumps(cfg), weight_seed=1, small_models=True)
+    assert "cuda:63" in str(e.value)
