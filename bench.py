@@ -10,9 +10,16 @@ pipeline once: gen_workload(n=100, seed=7) (bench.hpp:31-56), closed loop with
 based function of the seed — synthetic, no checkpoints). Stage iterations
 complete on CUDA events (device-paced clock), JCT = done - submit.
 
---gpus N (torchrun): every rank runs a full pipeline replica on its own GPU
-over its own copy of the workload (requests are independent, no data-path
-collective) -> "scaling": "weak"; time = max over ranks.
+--gpus N: ONE stage graph over N GPUs of the box: every stage
+gets whole GPUs, the bottleneck stages replicas, placed by placement_for()
+from the measured per-stage device busy time (STAGE_BUSY_MS); the Thinker's
+hidden rows cross GPUs over NVLink (connector pack with peer stores into the
+consuming Talker replica's arena). The workload scales with N ("scaling":
+"weak"): gen_workload(n = 100 N, seed 7), closed loop 16 N. The orchestrator is
+the reference's single control-plane thread (orchestrator.hpp:377-437), so
+one process drives all N GPUs: launched plainly (`python bench.py --gpus N`)
+it is that process; under torchrun rank 0 is, and ranks 1..N-1 only join the
+barriers (gloo) and report zero device time, so max over ranks = rank 0's.
 
 --impl reference: the reference's own control plane (compiled from its
 headers, oracle/_ref/ref_cpu_pipeline) with CPU fp32 model hooks on the host
@@ -92,16 +99,50 @@ class ClockSampler:
 
 
 def dist_setup(n_gpus: int):
+    """torchrun plumbing: a CPU (gloo) group for the barriers and the
+    max-over-ranks reductions -- the data path has no collective."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("gloo")
         return world, rank, local, dist
     return 1, 0, local, None
+
+
+# Device busy time per stage of the 1-GPU bench (ms per 100-request step,
+# profiles/r02_bench_*.json "stages"): what one GPU-worth of each stage costs
+# under the reference workload. placement_for() apportions GPUs by it.
+STAGE_BUSY_MS = {"thinker": 429.0, "talker": 457.0, "vocoder": 484.0}
+
+
+def placement_for(n_gpus: int, busy: dict = STAGE_BUSY_MS) -> dict:
+    """Stage -> "cuda:i,cuda:j,..." for Thinker->Talker->Code2Wav on n GPUs.
+    1 GPU: everything on cuda:0 (own streams). 2 GPUs: the busiest stage alone
+    on cuda:1, the other two share cuda:0. >= 3: every stage gets whole GPUs,
+    one each, the rest by largest remainder of busy-time share (ties to the
+    later stage in the graph: its work is on every request's tail)."""
+    stages = list(busy)
+    if n_gpus <= 1:
+        return {st: "cuda:0" for st in stages}
+    if n_gpus == 2:
+        heavy = max(stages, key=lambda st: (busy[st], stages.index(st)))
+        return {st: ("cuda:1" if st == heavy else "cuda:0") for st in stages}
+    total = sum(busy.values())
+    quota = {st: n_gpus * busy[st] / total for st in stages}
+    count = {st: max(1, int(quota[st])) for st in stages}
+    while sum(count.values()) > n_gpus:
+        st = max((st for st in stages if count[st] > 1), key=lambda st: count[st] - quota[st])
+        count[st] -= 1
+    while sum(count.values()) < n_gpus:
+        st = max(stages, key=lambda st: (quota[st] - count[st], stages.index(st)))
+        count[st] += 1
+    out, nxt = {}, 0
+    for st in stages:
+        out[st] = ",".join(f"cuda:{nxt + i}" for i in range(count[st]))
+        nxt += count[st]
+    return out
 
 
 def _reduce(x: float, dist, op: str) -> float:
@@ -231,8 +272,13 @@ def main() -> None:
     ap.add_argument("--concurrency", type=int, default=16)
     ap.add_argument("--small", action="store_true", help="reduced model dims (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--placement", default="", help='JSON stage->devices override, e.g. \'{"talker": "cuda:1,cuda:2"}\'')
+    ap.add_argument("--fold-devices", action="store_true",
+                    help="debug: map cuda:i -> cuda:(i mod visible) to exercise the N-GPU code path on fewer "
+                         "GPUs (the line is marked folded and is not an N-GPU measurement)")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup(args.gpus)
+    n_gpus = world if world > 1 else max(1, args.gpus)
 
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -241,14 +287,37 @@ def main() -> None:
             dist.destroy_process_group()
         return
 
+    if rank != 0:
+        # rank 0 drives the whole stage graph over all N GPUs; this rank only
+        # brackets the timed region and reports zero device time
+        dist.barrier()
+        dist.barrier()
+        aggregate(0, 0.0, 0.0, dist)
+        dist.destroy_process_group()
+        return
+
     import torch
     from paper_2602_02204_b200 import dev as D
     from paper_2602_02204_b200.serve import Pipeline
 
-    torch.cuda.set_device(local)
+    visible = torch.cuda.device_count()
+    if visible < n_gpus and not args.fold_devices:
+        raise SystemExit(f"--gpus {n_gpus}: only {visible} CUDA device(s) visible")
+    torch.cuda.set_device(0)
     pk = peaks()
-    pipe = Pipeline(CONFIG.read_text(), weight_seed=1234, small_models=args.small, device=local)
-    spec = dict(n=args.n, seed=7, concurrency=args.concurrency, stream=True, clock="device")
+    placement = placement_for(n_gpus)
+    if args.placement:
+        placement.update(json.loads(args.placement))
+    if args.fold_devices:
+        placement = {k: ",".join(f"cuda:{int(d.split(':')[1]) % visible}" for d in v.split(","))
+                     for k, v in placement.items()}
+    gpus_used = sorted({int(d.split(":")[1]) for v in placement.values() for d in v.split(",")})
+    cfg = json.loads(CONFIG.read_text())
+    cfg["placement"] = placement
+    n_req = args.n * n_gpus
+    conc = args.concurrency * n_gpus
+    pipe = Pipeline(json.dumps(cfg), weight_seed=1234, small_models=args.small, device=0)
+    spec = dict(n=n_req, seed=7, concurrency=conc, stream=True, clock="device")
     for _ in range(args.warmup):
         pipe.bench(**spec)
     lib = D.dev_lib()
@@ -256,8 +325,9 @@ def main() -> None:
     results = []
     if dist is not None:
         dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    for g in gpus_used:
+        torch.cuda.synchronize(g)
+    with ClockSampler(",".join(str(g) for g in gpus_used)) as clk:
         lib.omni_dev_counters(C.byref(l0), C.byref(h0), C.byref(d0))
         gc0, gr0 = C.c_uint64(), C.c_uint64()
         lib.omni_dev_graph_counters(C.byref(gc0), C.byref(gr0))
@@ -267,7 +337,8 @@ def main() -> None:
         for _ in range(args.steps):
             results.append(pipe.bench(**spec))  # each step drains fully: all stage streams done
         e1.record()
-        torch.cuda.synchronize()
+        for g in gpus_used:  # bench() drained every stage stream on every GPU already
+            torch.cuda.synchronize(g)
         wall = time.perf_counter() - t0
     if dist is not None:
         dist.barrier()
@@ -282,10 +353,6 @@ def main() -> None:
     rps_makespan = statistics.mean(r["requests_per_s"] for r in results)
     mean_jct = statistics.mean(r["mean_jct_us"] for r in results)
     p99_jct = statistics.mean(r["p99_jct_us"] for r in results)
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return
     roof = gemm_roofline(pk)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -316,7 +383,7 @@ def main() -> None:
         "metric": METRIC,
         "value": round(value, 3),
         "unit": "requests/s",
-        "n_gpus": world,
+        "n_gpus": n_gpus,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": round(step_s * 1e3, 2),
@@ -325,12 +392,17 @@ def main() -> None:
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic: gen_workload(n=100, seed=7) prompts, random-init weights (counter RNG)",
-        "config": {"workload": f"omni3 = reference.json Thinker->Talker->Code2Wav, closed loop {args.concurrency}, "
-                               "streaming chunks 4/8, all stages on each GPU (replica per rank)",
-                   "n_requests_per_step": args.n, "concurrency": args.concurrency,
+        "config": {"workload": f"omni3 = reference.json Thinker->Talker->Code2Wav, gen_workload(n={n_req}, seed 7), "
+                               f"closed loop {conc} (16 per GPU), streaming chunks 4/8, one stage graph over "
+                               f"{n_gpus} GPU(s)",
+                   "n_requests_per_step": n_req, "concurrency": conc,
+                   "placement": placement,
+                   **({"folded": f"DEBUG: {n_gpus}-GPU placement folded onto {visible} GPU(s)"}
+                      if args.fold_devices else {}),
                    "models": "thinker 8L d2048 (16q/4kv heads, ffn 8192, V256); talker 4L d2048 (V64); "
                              "code2wav DiT 4L d1024 T4 S16",
-                   "parallelism": f"replicas{world}",
+                   "parallelism": "stage-per-GPU " + " ".join(f"{k}x{len(v.split(','))}" for k, v in placement.items())
+                                  if n_gpus > 1 else "all stages on cuda:0",
                    "l2": "weights 1.4 GB per AR step set >> 126 MB L2 (no flush needed)"},
         "mean_jct_us": round(mean_jct, 1),
         "p99_jct_us": round(p99_jct, 1),
