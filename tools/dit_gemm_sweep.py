@@ -18,7 +18,7 @@ for name, (N, K) in SHAPES.items():
     lib.omni_k_fill_weights(C.c_uint64(X), C.c_int64(8192 * K), C.c_uint64(3), C.c_uint32(2), C.c_float(1.0))
     O = D.mem_alloc(8192 * N * 2)
     arr = (C.c_uint64 * 2)(*Ws)
-    for M in (128, 640, 1024, 2048, 8192):
+    for M in (128, 640, 1024, 1360, 2048, 4096, 8192):
         ms = C.c_float()
         rc = lib.omni_k_gemm_time_multi(arr, 2, N, K, C.c_uint64(X), M, 0, C.c_uint64(O), N, -1, 32, C.byref(ms))
         us = ms.value * 1e3
