@@ -137,6 +137,12 @@ omni_status omni_ar_step(omni_stage* st, const omni_ar_batch* batch, int32_t* to
  * the top-2 logit margin. */
 omni_status omni_stage_set_sampling(omni_stage* st, int32_t top_k, uint64_t seed);
 
+/* SM share of a DiT stage: its denoise iteration is one persistent kernel that
+ * holds whole SMs (192 KB shared memory, all of TMEM) for the iteration, so
+ * beside AR stages on the same GPU it must leave them SMs. sms <= 0 = all SMs
+ * of the device (the DiT has its GPU to itself). No effect on results. */
+omni_status omni_stage_set_sm_share(omni_stage* st, int32_t sms);
+
 /* Admits a sequence's KV pages for positions [0, upto_tokens) ahead of a
  * step, so a sequence that does not fit fails alone (OMNI_E_OOM) instead of
  * failing the whole batched step (the reference fails per entry,

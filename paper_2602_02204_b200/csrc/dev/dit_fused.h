@@ -1,0 +1,58 @@
+// K6': persistent dataflow DiT iteration (dit_fused.cu). Internal to libomni_dev.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dit_kernels.h"
+
+namespace omni_dev {
+
+constexpr int kDitMaxLayers = 8;
+constexpr int kDitMaxPhases = 256;  // T * (3 + 7 L)
+constexpr int kDitTileRows = 256;  // rows of one row tile (16 tokens x 16 samples) = MMA N
+constexpr int kDitTileTok = 16;
+constexpr int kDitFeat = 128;      // output features per GEMM item = MMA M (TMEM lanes)
+
+// TMA descriptors of one DiT stage, resident in global memory (written once
+// at stage creation): keeping them out of the kernel parameter block keeps
+// the scalar parameters in a few constant-cache lines.
+struct DitMaps {
+  // weights (MMA A operand), 128-row boxes; w_out is [C_pad 128, d]
+  CUtensorMap w_in, w_out;
+  CUtensorMap wqkv[kDitMaxLayers], wo[kDitMaxLayers], w1[kDitMaxLayers], w2[kDitMaxLayers];
+  CUtensorMap x_x, x_a, x_o, x_u;  // activations (MMA B operand), 256-row boxes
+};
+
+// Everything else one iteration needs (a small __grid_constant__ parameter).
+struct DitFusedParams {
+  const DitMaps* maps;             // device copy, 64-byte aligned
+  const DitTokDesc* toks;          // [n_rt * 8] (batch padded to whole row tiles)
+  const __nv_bfloat16* pos_emb;    // [16][d]
+  const float* mod_table;          // [T][vocab][L * 6 * d]
+  float* x;                        // [rows][C] latent (fp32)
+  __nv_bfloat16* xb;               // [rows][C] its bf16 copy (IN-proj operand)
+  float* h;                        // [rows][d] residual stream
+  __nv_bfloat16 *a, *qkv, *o, *u;  // LN out [rows][d], [rows][3d], attn out [rows][d], [rows][ff]
+  float* part;                     // MLP-down first-half partials [n_rt * d/128][256 rows][128]
+  int32_t* samples;                // [rows] int32 samples (last Euler step)
+  int* progress;                   // [n_rt] units completed per row tile (zeroed per launch)
+  int* tile_cnt;                   // [n_rt * d/128] split-K arrivals (zeroed per launch)
+  int* ready;                      // [n_rt * d/128] first-arriver partials written (zeroed per launch)
+  int* next_item;                  // global item counter (zeroed per launch)
+  unsigned long long* trace;       // optional [items][5]: fetch, dep ok, mma done, done, smid
+  int n_rt, d, C, H, ff, L, T, vocab, down_split;
+  float dt, sample_scale;
+};
+
+// Total items of one launch (tests / tools).
+int dit_fused_items(int n_rt, int d, int H, int ff, int L, int T, int down_split);
+size_t dit_fused_smem(int stages);
+// Model shapes the fused iteration covers (others run one kernel per op).
+bool dit_fused_supported(int d, int C, int H, int ff, int L, int T);
+// stages: TMA ring depth (3 or 4); ctas: persistent grid.
+cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStream_t st);
+
+}  // namespace omni_dev

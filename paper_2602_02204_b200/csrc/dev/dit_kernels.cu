@@ -6,6 +6,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "dit_kernels.h"
 #include "launch.cuh"
 #include "ptx.cuh"
@@ -14,11 +16,14 @@
 namespace omni_dev {
 
 // x0[row, ch] ~ N(0,1) keyed by (request, global token position, sample, ch).
+// Also zeroes `n_zero` ints at `zero` (the fused iteration's counters).
 __global__ void dit_noise_kernel(const DitTokDesc* __restrict__ toks, int S, int C, uint64_t seed,
-                                 float* __restrict__ x, __nv_bfloat16* __restrict__ xb, int rows) {
+                                 float* __restrict__ x, __nv_bfloat16* __restrict__ xb, int rows,
+                                 int* __restrict__ zero, int n_zero) {
   pdl_wait();
   pdl_trigger();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n_zero) zero[i] = 0;
   if (i >= (int64_t)rows * C) return;
   const int r = (int)(i / C), ch = (int)(i % C);
   const DitTokDesc t = toks[r / S];
@@ -201,10 +206,11 @@ __global__ void __launch_bounds__(256)
 
 // ---------------------------------------------------------------------------
 cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t seed, float* x,
-                      __nv_bfloat16* xb, cudaStream_t st) {
+                      __nv_bfloat16* xb, cudaStream_t st, int* zero, int n_zero) {
   const int rows = n_tok * S;
-  const int64_t n = (int64_t)rows * C;
-  return launch_k(dit_noise_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, toks, S, C, seed, x, xb, rows);
+  const int64_t n = std::max<int64_t>((int64_t)rows * C, n_zero);
+  return launch_k(dit_noise_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, 1, toks, S, C, seed, x, xb,
+                  rows, zero, n_zero);
 }
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st) {

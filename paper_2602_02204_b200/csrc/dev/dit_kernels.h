@@ -20,7 +20,7 @@ struct DitTokDesc {  // one conditioning token of the batch
 };
 
 cudaError_t dit_noise(const DitTokDesc* toks, int n_tok, int S, int C, uint64_t seed, float* x,
-                      __nv_bfloat16* xb, cudaStream_t st);
+                      __nv_bfloat16* xb, cudaStream_t st, int* zero = nullptr, int n_zero = 0);
 cudaError_t dit_cond(const DitTokDesc* toks, int n_tok, const __nv_bfloat16* tok_emb,
                      const __nv_bfloat16* t_emb, int step, int d, __nv_bfloat16* cvec, cudaStream_t st);
 // mod_base: adaLN table rows of this Euler step ([vocab][ld_mod]); the row of

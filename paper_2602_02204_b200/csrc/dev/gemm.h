@@ -127,6 +127,12 @@ int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas = 192);
 bool gemm_make_weight(GemmWeight& w, const __nv_bfloat16* ptr, int N, int N_pad, int K,
                       int max_splits, int target_ctas = 192);
 bool gemm_make_input(GemmInput& x, const __nv_bfloat16* ptr, int rows_cap, int K);
+// bf16 K-major [rows, K] map, box [box_rows, 64], 128-B swizzle (an MMA operand).
+bool gemm_encode_kmajor(CUtensorMap& m, const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows);
+// Plain (unswizzled) 2-D tile map of a row-major [rows, cols] fp32 / bf16
+// matrix with box [box_rows, box_cols] (TMA stores / reduce-adds of epilogue tiles).
+bool encode_tile_map(CUtensorMap& m, const void* ptr, bool f32, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                     uint32_t box_rows);
 cudaError_t gemm_run(const GemmWeight& w, const GemmInput& x, int M, int epi,
                      const GemmEpilogue& e, cudaStream_t st);
 // Validates (w, x, M, epi, e) and fills the kernel argument block (the step

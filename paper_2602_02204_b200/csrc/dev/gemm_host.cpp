@@ -39,6 +39,25 @@ bool encode_2d(CUtensorMap& m, const void* ptr, uint64_t rows, uint64_t K, uint3
 
 }  // namespace
 
+bool gemm_encode_kmajor(CUtensorMap& m, const void* ptr, uint64_t rows, uint64_t K, uint32_t box_rows) {
+  return encode_2d(m, ptr, rows, K, box_rows);
+}
+
+bool encode_tile_map(CUtensorMap& m, const void* ptr, bool f32, uint64_t rows, uint64_t cols, uint32_t box_cols,
+                     uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * es};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int gemm_choose_splits(int N_pad, int K, int max_splits, int target_ctas) {
   // Fill up to `target_ctas` CTAs (decode weights: 192 — the in-chain optimum
   // measured by tools/gemm_sweep.py) with at least two 64-wide K blocks per

@@ -250,7 +250,7 @@ void build_dit(omni_stage* st) {
     ly.g2 = gemm_of(ly.w2, 1, 64);
     ly.g2.fill_sms = true;
   }
-  const int T = st->tok_cap = std::max(16, st->lim.dit_max_tokens);
+  const int T = st->tok_cap = round_up(std::max(16, st->lim.dit_max_tokens), kDitTileTok);  // whole row tiles
   const int R = st->drows_cap = T * kDitSamples;
   st->dx = dev_alloc<float>(st, (size_t)R * C);
   st->dxin = dev_alloc<__nv_bfloat16>(st, (size_t)R * C);
@@ -259,13 +259,49 @@ void build_dit(omni_stage* st) {
   st->dqkv = dev_alloc<__nv_bfloat16>(st, (size_t)R * 3 * d);
   st->dout = dev_alloc<__nv_bfloat16>(st, (size_t)R * d);
   st->du = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
+  // fused iteration: MLP-down split in two K halves (fixed per weight shape:
+  // batch invariance) so its items match the others' K = d mainloop
+  st->down_split = (ff >= 2 * d && (ff / 64) % 2 == 0) ? 2 : 1;
+  const int n_rt = R / kDitTileRows, nfd = d / kDitFeat;
+  st->dpart = dev_alloc<float>(st, (size_t)n_rt * nfd * kDitTileRows * kDitFeat);
+  st->dctl_n = n_rt + 2 * n_rt * nfd + 1;
+  st->dctl = dev_alloc<int>(st, (size_t)st->dctl_n);
+  {
+    int sms = 0;
+    OMNI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->dev));
+    st->dit_ctas = sms;
+  }
+  if (const char* e = std::getenv("OMNI_DIT_TRACE"); e && e[0] == '1') {
+    st->dit_trace_items = dit_fused_items(n_rt, d, m.n_heads, ff, L, m.dit_steps, st->down_split);
+    st->dit_trace = dev_alloc<unsigned long long>(st, (size_t)st->dit_trace_items * 8);
+  }
   const int cvec_rows = std::max(T, m.vocab);  // per-step rows / adaLN table rows
+  const bool fused = dit_fused_supported(d, C, m.n_heads, ff, L, m.dit_steps);
   st->dcvec = dev_alloc<__nv_bfloat16>(st, (size_t)cvec_rows * d);
   st->din_x = input_of(st->dxin, R, C);
   st->din_a = input_of(st->da, R, d);
   st->din_o = input_of(st->dout, R, d);
   st->din_u = input_of(st->du, R, ff);
   st->din_c = input_of(st->dcvec, cvec_rows, d);
+  if (fused) {  // TMA descriptors of the fused iteration, resident on the device
+    DitMaps mp{};
+    mp.w_in = st->g_in.tmap;  // 128-row boxes: MMA A (swap-AB)
+    mp.w_out = st->g_out.tmap;
+    for (int l = 0; l < L; ++l) {
+      const auto& ly = st->dlayers[l];
+      mp.wqkv[l] = ly.gqkv.tmap;
+      mp.wo[l] = ly.go.tmap;
+      mp.w1[l] = ly.g1.tmap;
+      mp.w2[l] = ly.g2.tmap;
+    }
+    mp.x_x = st->din_x.tmap_for(kDitTileRows);
+    mp.x_a = st->din_a.tmap_for(kDitTileRows);
+    mp.x_o = st->din_o.tmap_for(kDitTileRows);
+    mp.x_u = st->din_u.tmap_for(kDitTileRows);
+    st->dmaps = dev_alloc<DitMaps>(st, 1);
+    OMNI_CUDA(cudaMemcpyAsync(st->dmaps, &mp, sizeof(mp), cudaMemcpyHostToDevice, st->stream));
+  }
+
   // adaLN modulation table: mod[t][id] = W_mod . silu(tok_emb[id] + t_emb[t])
   // for every (Euler step, conditioning id) — the per-token GEMM of the
   // reference-shaped model depends on nothing else, so it is evaluated once
@@ -668,8 +704,60 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
 // ---------------------------------------------------------------------------
 // DiT step
 // ---------------------------------------------------------------------------
+bool dit_fused_enabled() {  // OMNI_DIT_FUSED=0: one kernel per op (A/B only)
+  static const bool on = [] {
+    const char* e = std::getenv("OMNI_DIT_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// The whole iteration as one persistent dataflow kernel (dit_fused.cu): noise
+// + counter reset, then T Euler steps x L layers in ONE launch.
+void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
+  const auto& m = st->m;
+  const int d = m.d_model, L = m.n_layers, C = m.dit_channels, S = kDitSamples;
+  const int n_rt = n_tok * S / kDitTileRows, nfd = d / kDitFeat;
+  cudaStream_t s = st->stream;
+  OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, st->dxin, s, st->dctl,
+                        n_rt + 2 * n_rt * nfd + 1));
+  DitFusedParams p{};
+  p.maps = st->dmaps;
+  p.toks = toks_dev;
+  p.pos_emb = st->pos_emb.p;
+  p.mod_table = st->mod_table;
+  p.x = st->dx;
+  p.xb = st->dxin;
+  p.h = st->dh;
+  p.a = st->da;
+  p.qkv = st->dqkv;
+  p.o = st->dout;
+  p.u = st->du;
+  p.part = st->dpart;
+  p.samples = samples_dev;
+  p.progress = st->dctl;
+  p.tile_cnt = st->dctl + n_rt;
+  p.ready = st->dctl + n_rt + n_rt * nfd;
+  p.next_item = st->dctl + n_rt + 2 * n_rt * nfd;
+  p.n_rt = n_rt;
+  p.d = d;
+  p.C = C;
+  p.H = m.n_heads;
+  p.ff = m.d_ff;
+  p.L = L;
+  p.T = m.dit_steps;
+  p.vocab = m.vocab;
+  p.down_split = st->down_split;
+  p.dt = 1.f / m.dit_steps;
+  p.sample_scale = kSampleScale;
+  p.trace = st->dit_trace;
+  OMNI_KERNEL(dit_fused_run(p, st->dit_stages, st->dit_ctas, s));
+}
+
 void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
   const auto& m = st->m;
+  if (dit_fused_enabled() && dit_fused_supported(m.d_model, m.dit_channels, m.n_heads, m.d_ff, m.n_layers, m.dit_steps))
+    return dit_chunk_fused(st, toks_dev, n_tok, samples_dev);
   const int d = m.d_model, L = m.n_layers, C = m.dit_channels, S = kDitSamples, T = m.dit_steps;
   const int rows = n_tok * S;
   const int ld_mod = L * 6 * d;
@@ -727,7 +815,7 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
   }
 }
 
-constexpr int kDitPadTok = 8;  // DiT batches are padded to whole 128-row token tiles
+constexpr int kDitPadTok = kDitTileTok;  // DiT batches are padded to whole 256-row tiles (16 tokens)
 uint64_t dit_graph_key(int nt, int64_t t0) { return (uint64_t)nt << 20 | (uint64_t)t0; }
 
 // Capture the DiT step graph of every padded batch size up front
@@ -992,6 +1080,12 @@ omni_status omni_stage_tensor(const omni_stage* st, const char* name, uint64_t* 
       if (cols) *cols = st->m.d_model;
       return;
     }
+    if (n == "buf.dit_trace" && st->dit_trace) {  // OMNI_DIT_TRACE=1: [item][5] u64 of the last DiT chunk
+      *dev_ptr = reinterpret_cast<uint64_t>(st->dit_trace);
+      if (rows) *rows = st->dit_trace_items;
+      if (cols) *cols = 8;
+      return;
+    }
     if (n == "buf.step_trace" && st->step_trace) {  // OMNI_STEP_TRACE=1: [launch][cta][8] u64
       *dev_ptr = reinterpret_cast<uint64_t>(st->step_trace);
       if (rows) *rows = kStepTraceLaunches * kStepTraceCtas;
@@ -1186,6 +1280,19 @@ omni_status omni_seq_reserve(omni_stage* st, uint64_t seq_id, int32_t upto_token
     OMNI_REQUIRE(st && st->m.kind != OMNI_MODEL_DIT, OMNI_E_BADARG, "omni_seq_reserve needs an AR stage");
     OMNI_REQUIRE(upto_tokens >= 0, OMNI_E_BADARG, "negative token count");
     ensure_pages(st, seq_for(st, seq_id), upto_tokens);
+  });
+}
+
+omni_status omni_stage_set_sm_share(omni_stage* st, int32_t sms) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && st->m.kind == OMNI_MODEL_DIT, OMNI_E_BADARG, "the SM share applies to DiT stages");
+    ensure_idle(st);
+    int n = 0;
+    OMNI_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, st->dev));
+    const int want = sms <= 0 ? n : std::min(sms, n);
+    if (want != st->dit_ctas) drop_graphs(st);  // the grid size is baked into the step graphs
+    st->dit_ctas = want;
+    prewarm_dit_graphs(st);
   });
 }
 

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "ar_kernels.h"
+#include "dit_fused.h"
 #include "dit_kernels.h"
 #include "gemm.h"
 #include "omni_dev.h"
@@ -108,6 +109,14 @@ struct omni_stage {
                 *dcvec = nullptr;
   int32_t* dsamples = nullptr;
   omni_dev::GemmInput din_x, din_a, din_o, din_u, din_c;
+  // persistent dataflow iteration (dit_fused.cu): split-K scratch + counters
+  float* dpart = nullptr;
+  int* dctl = nullptr;
+  int dctl_n = 0, down_split = 1, dit_stages = 4;
+  int dit_ctas = 0;  // persistent grid of the fused iteration (omni_stage_set_sm_share)
+  omni_dev::DitMaps* dmaps = nullptr;  // device copy of the fused iteration's TMA descriptors
+  unsigned long long* dit_trace = nullptr;  // OMNI_DIT_TRACE=1 (tools/dit_trace.py)
+  int dit_trace_items = 0;
 
   // ---- step staging / results ----
   omni_dev::Staging desc, pack;

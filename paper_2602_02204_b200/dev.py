@@ -92,6 +92,10 @@ class Stage:
         """Greedy (top_k <= 1) or top-k sampling of decode rows (omni_stage_set_sampling)."""
         check(self.lib.omni_stage_set_sampling(self.h, top_k, C.c_uint64(seed)))
 
+    def set_sm_share(self, sms: int) -> None:
+        """SMs a DiT stage's persistent iteration may hold (<= 0: all; omni_stage_set_sm_share)."""
+        check(self.lib.omni_stage_set_sm_share(self.h, sms))
+
     def reserve(self, seq_id: int, upto_tokens: int) -> None:
         check(self.lib.omni_seq_reserve(self.h, C.c_uint64(seq_id), upto_tokens))
 
