@@ -4,6 +4,8 @@
 
 #include <chrono>
 
+#include "omni/control.hpp"
+
 namespace omni {
 
 std::string ConnectorKey::canonical() const {
@@ -31,10 +33,25 @@ void Connector::put(const ConnectorKey& key, const Payload& p) {
   const std::string k = key.canonical();
   auto it = kv_.find(k);
   if (it != kv_.end()) {
-    if (it->second.hash == h && it->second.payload == p) return;  // idempotent re-put
+    const Payload& held = it->second.frame.empty()
+                              ? it->second.payload
+                              : payload_from_locator(decode_control_frame(it->second.frame).locator);
+    if (it->second.hash == h && held == p) return;  // idempotent re-put
     throw WriteConflict(k);
   }
-  kv_.emplace(k, Slot{p, h, false, key.request_id});
+  Slot slot{p, {}, h, false, key.request_id};
+  if (p.is_device()) {
+    ControlMessage m;
+    m.kind = ControlMessage::Kind::PUT_NOTICE;
+    m.key = k;
+    m.request_id = key.request_id;
+    m.edge = edge_;
+    m.locator = device_locator(p);
+    slot.frame = encode_control_frame(m);
+    slot.payload = Payload{};
+    ++frames_;
+  }
+  kv_.emplace(k, std::move(slot));
   cv_.notify_all();
 }
 
@@ -46,7 +63,11 @@ Payload Connector::get(const ConnectorKey& key, uint64_t timeout_ms) {
     auto it = kv_.find(k);
     if (it != kv_.end() && !it->second.consumed) {
       it->second.consumed = true;
-      return it->second.payload;
+      if (it->second.frame.empty()) return it->second.payload;
+      const ControlMessage m = decode_control_frame(it->second.frame);
+      if (m.kind != ControlMessage::Kind::PUT_NOTICE || m.key != k)
+        throw ProtocolViolation("put notice does not match key " + k);
+      return payload_from_locator(m.locator);
     }
     if (cv_.wait_until(lk, deadline) == std::cv_status::timeout) throw TimeoutError("get timed out on " + k);
   }
@@ -73,7 +94,9 @@ uint64_t Connector::cleanup(uint64_t rid) {
   uint64_t freed = 0;
   for (auto it = kv_.begin(); it != kv_.end();) {
     if (it->second.request_id == rid) {
-      if (!it->second.consumed) freed += payload_bytes(it->second.payload);
+      if (!it->second.consumed)
+        freed += it->second.frame.empty() ? payload_bytes(it->second.payload)
+                                          : decode_control_frame(it->second.frame).locator.length;
       it = kv_.erase(it);
     } else {
       ++it;
@@ -81,7 +104,8 @@ uint64_t Connector::cleanup(uint64_t rid) {
   }
   auto st = streams_.find(rid);
   if (st != streams_.end()) {
-    for (const auto& b : st->second.q) freed += payload_bytes(b.payload);
+    for (const auto& b : st->second.q)
+      freed += b.frame.empty() ? payload_bytes(b.payload) : decode_control_frame(b.frame).locator.length;
     streams_.erase(st);
   }
   return freed;
@@ -94,7 +118,18 @@ void Connector::stream_send(uint64_t rid, const StreamChunk& c) {
   if (c.seq != s.next_seq)
     throw ProtocolViolation("out-of-order chunk seq " + std::to_string(c.seq) + " (expected " +
                             std::to_string(s.next_seq) + ")");
-  s.q.push_back(Buffered{c.seq, c.eos, c.payload});
+  if (c.payload.is_device()) {
+    ControlMessage m;
+    m.kind = c.eos ? ControlMessage::Kind::EOS : ControlMessage::Kind::CHUNK_NOTICE;
+    m.request_id = rid;
+    m.edge = edge_;
+    m.seq = c.seq;
+    m.locator = device_locator(c.payload);
+    s.q.push_back(Buffered{c.seq, c.eos, Payload{}, encode_control_frame(m)});
+    ++frames_;
+  } else {
+    s.q.push_back(Buffered{c.seq, c.eos, c.payload, {}});
+  }
   ++s.next_seq;
   ++chunks_sent_;
   s.eos_sent = c.eos;
@@ -113,7 +148,15 @@ std::optional<StreamChunk> Connector::stream_try_recv(uint64_t rid) {
   c.to = to_;
   c.seq = b.seq;
   c.eos = b.eos;
-  c.payload = std::move(b.payload);
+  if (b.frame.empty()) {
+    c.payload = std::move(b.payload);
+    return c;
+  }
+  const ControlMessage m = decode_control_frame(b.frame);
+  const auto want = b.eos ? ControlMessage::Kind::EOS : ControlMessage::Kind::CHUNK_NOTICE;
+  if (m.kind != want || m.request_id != rid || m.seq != b.seq || m.edge != edge_)
+    throw ProtocolViolation("chunk notice does not match its stream slot on edge " + edge_);
+  c.payload = payload_from_locator(m.locator);
   return c;
 }
 

@@ -87,12 +87,17 @@ class Connector {
   // Drops everything of a request; returns payload bytes released.
   uint64_t cleanup(uint64_t request_id);
   uint64_t chunks_sent() const { return chunks_sent_; }
+  uint64_t frames_encoded() const { return frames_; }
 
  private:
   friend class StreamSender;
   friend class StreamReceiver;
+  // Device payloads travel as encoded DEVICE control frames (control.hpp):
+  // the frame is what a cross-process DEVICE transport puts on the wire, and
+  // decoding it on the receive side re-checks the locator.
   struct Slot {
     Payload payload;
+    std::vector<uint8_t> frame;
     uint64_t hash = 0;
     bool consumed = false;
     uint64_t request_id = 0;
@@ -101,6 +106,7 @@ class Connector {
     uint32_t seq;
     bool eos;
     Payload payload;
+    std::vector<uint8_t> frame;
   };
   struct Stream {
     bool sender_open = false, receiver_open = false, eos_sent = false;
@@ -119,6 +125,7 @@ class Connector {
   std::map<std::string, Slot> kv_;
   std::map<uint64_t, Stream> streams_;
   uint64_t chunks_sent_ = 0;
+  uint64_t frames_ = 0;
 };
 
 }  // namespace omni

@@ -24,6 +24,7 @@ struct DeviceRef {
   int32_t device = -1;   // CUDA ordinal; -1 = host payload
   uint64_t blob = 0;     // device address of the encoded blob (header + body)
   uint64_t nbytes = 0;   // encoded length
+  uint64_t arena = 0;    // 0: `blob` is an address; else CUDA-IPC arena id, `blob` an offset
   bool valid() const { return device >= 0; }
 };
 
@@ -38,7 +39,8 @@ struct Payload {
   bool is_device() const { return dev.valid(); }
   bool operator==(const Payload& o) const {
     return dtype == o.dtype && shape == o.shape && bytes == o.bytes && dev.blob == o.dev.blob &&
-           dev.device == o.dev.device;
+           dev.device == o.dev.device && dev.arena == o.dev.arena && dev.nbytes == o.dev.nbytes &&
+           host_tokens == o.host_tokens;
   }
   bool size_consistent() const { return is_device() || bytes.size() == element_count() * dtype_width(dtype); }
 
