@@ -214,6 +214,37 @@ omni_status omni_stage_after(omni_stage* dst, omni_stage* src);
  * step. No-op before the first pack. */
 omni_status omni_stage_after_pack(omni_stage* dst, omni_stage* src);
 
+/* ------------------------------------------------------------------------ */
+/* Multi-process placement (the reference's SHM / TCP        */
+/* transports, connector.hpp:23-30, 77-90, shm_region.hpp). A consumer      */
+/* process exports its connector arena; the producer process imports it     */
+/* and packs straight into it (omni_pack_hidden with absolute destinations  */
+/* inside the imported arena), then records an interprocess event that the  */
+/* consumer's stage waits on. The control frames (DEVICE locators, arena-   */
+/* relative offsets) travel over the serve library's IPC channel.           */
+/* ------------------------------------------------------------------------ */
+typedef struct omni_ipc_handle {
+  uint8_t handle[64]; /* cudaIpcMemHandle_t */
+  uint64_t bytes;
+  int32_t dev;
+  int32_t reserved;
+} omni_ipc_handle;
+typedef struct omni_ipc_event_handle {
+  uint8_t handle[64]; /* cudaIpcEventHandle_t */
+} omni_ipc_event_handle;
+typedef struct omni_ipc_event omni_ipc_event;
+omni_status omni_arena_export(const omni_arena* a, omni_ipc_handle* out);
+/* Maps another process's exported arena; omni_arena_destroy unmaps it. */
+omni_status omni_arena_import(const omni_ipc_handle* h, omni_arena** out);
+omni_status omni_ipc_event_create(int32_t dev, omni_ipc_event** out, omni_ipc_event_handle* handle);
+omni_status omni_ipc_event_open(int32_t dev, const omni_ipc_event_handle* handle, omni_ipc_event** out);
+omni_status omni_ipc_event_destroy(omni_ipc_event* e);
+/* Records `e` on src's stream (call right after omni_pack_hidden). */
+omni_status omni_stage_record_pack(omni_stage* src, omni_ipc_event* e);
+/* dst's next step waits (on-device) for the last record of `e`, which may
+ * have been made by another process. */
+omni_status omni_stage_wait_event(omni_stage* dst, omni_ipc_event* e);
+omni_status omni_ipc_event_sync(omni_ipc_event* e);
 /* Plumbing for tests / bench (no compute): device memory and copies. */
 omni_status omni_mem_alloc(int32_t dev, uint64_t bytes, uint64_t* dev_ptr);
 omni_status omni_mem_free(uint64_t dev_ptr);

@@ -932,6 +932,12 @@ struct omni_arena {
   int dev = 0;
   uint8_t* base = nullptr;
   uint64_t bytes = 0;
+  bool imported = false;  // mapped from another process (cudaIpcOpenMemHandle)
+};
+
+struct omni_ipc_event {
+  int dev = 0;
+  cudaEvent_t ev = nullptr;
 };
 
 extern "C" {
@@ -1206,7 +1212,10 @@ omni_status omni_arena_destroy(omni_arena* a) {
     if (!a) return;
     cudaSetDevice(a->dev);
     cudaDeviceSynchronize();
-    cudaFree(a->base);
+    if (a->imported)
+      cudaIpcCloseMemHandle(a->base);
+    else
+      cudaFree(a->base);
     delete a;
   });
 }
@@ -1305,6 +1314,119 @@ omni_status omni_stage_set_sampling(omni_stage* st, int32_t top_k, uint64_t seed
     st->top_k = top_k;
     st->sample_seed = seed;
     if (top_k > 1) prewarm_decode_graphs(st);
+  });
+}
+
+omni_status omni_arena_export(const omni_arena* a, omni_ipc_handle* out) {
+  return guarded([&] {
+    OMNI_REQUIRE(a && out && !a->imported, OMNI_E_BADARG, "only an arena this process allocated can be exported");
+    static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(out->handle), "IPC handle size");
+    cudaIpcMemHandle_t h;
+    OMNI_CUDA(cudaSetDevice(a->dev));
+    OMNI_CUDA(cudaIpcGetMemHandle(&h, a->base));
+    std::memcpy(out->handle, &h, sizeof(h));
+    out->bytes = a->bytes;
+    out->dev = a->dev;
+    out->reserved = 0;
+  });
+}
+
+omni_status omni_arena_import(const omni_ipc_handle* h, omni_arena** out) {
+  return guarded([&] {
+    require_device();
+    OMNI_REQUIRE(h && out, OMNI_E_BADARG, "null IPC handle");
+    int n = 0;
+    OMNI_CUDA(cudaGetDeviceCount(&n));
+    OMNI_REQUIRE(h->dev >= 0 && h->dev < n, OMNI_E_BADARG, "IPC arena on a device this process cannot see");
+    cudaIpcMemHandle_t mh;
+    std::memcpy(&mh, h->handle, sizeof(mh));
+    OMNI_CUDA(cudaSetDevice(h->dev));
+    void* base = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&base, mh, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw DevError(OMNI_E_TRANSPORT, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    }
+    auto* a = new omni_arena();
+    a->dev = h->dev;
+    a->base = static_cast<uint8_t*>(base);
+    a->bytes = h->bytes;
+    a->imported = true;
+    *out = a;
+  });
+}
+
+omni_status omni_ipc_event_create(int32_t dev, omni_ipc_event** out, omni_ipc_event_handle* handle) {
+  return guarded([&] {
+    require_device();
+    OMNI_REQUIRE(out && handle, OMNI_E_BADARG, "null output");
+    static_assert(sizeof(cudaIpcEventHandle_t) == sizeof(handle->handle), "IPC event handle size");
+    OMNI_CUDA(cudaSetDevice(dev));
+    auto* e = new omni_ipc_event();
+    e->dev = dev;
+    OMNI_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming | cudaEventInterprocess));
+    // an interprocess event must have been recorded once before a peer waits on it
+    OMNI_CUDA(cudaEventRecord(e->ev, 0));
+    OMNI_CUDA(cudaEventSynchronize(e->ev));
+    cudaIpcEventHandle_t h;
+    OMNI_CUDA(cudaIpcGetEventHandle(&h, e->ev));
+    std::memcpy(handle->handle, &h, sizeof(h));
+    *out = e;
+  });
+}
+
+omni_status omni_ipc_event_open(int32_t dev, const omni_ipc_event_handle* handle, omni_ipc_event** out) {
+  return guarded([&] {
+    require_device();
+    OMNI_REQUIRE(out && handle, OMNI_E_BADARG, "null IPC event handle");
+    cudaIpcEventHandle_t h;
+    std::memcpy(&h, handle->handle, sizeof(h));
+    OMNI_CUDA(cudaSetDevice(dev));
+    auto* e = new omni_ipc_event();
+    e->dev = dev;
+    const cudaError_t r = cudaIpcOpenEventHandle(&e->ev, h);
+    if (r != cudaSuccess) {
+      cudaGetLastError();
+      delete e;
+      throw DevError(OMNI_E_TRANSPORT, std::string("cudaIpcOpenEventHandle: ") + cudaGetErrorString(r));
+    }
+    *out = e;
+  });
+}
+
+omni_status omni_ipc_event_destroy(omni_ipc_event* e) {
+  return guarded([&] {
+    if (!e) return;
+    cudaSetDevice(e->dev);
+    cudaEventDestroy(e->ev);
+    delete e;
+  });
+}
+
+omni_status omni_stage_record_pack(omni_stage* src, omni_ipc_event* e) {
+  return guarded([&] {
+    OMNI_REQUIRE(src && e, OMNI_E_BADARG, "null stage / event");
+    OMNI_CUDA(cudaSetDevice(src->dev));
+    // ordered after the stage's most recent pack (recorded on the same stream
+    // right behind it); later steps on the stream are not included only if
+    // this is called before they are enqueued -- the connector calls it right
+    // after omni_pack_hidden
+    OMNI_CUDA(cudaEventRecord(e->ev, src->stream));
+  });
+}
+
+omni_status omni_stage_wait_event(omni_stage* dst, omni_ipc_event* e) {
+  return guarded([&] {
+    OMNI_REQUIRE(dst && e, OMNI_E_BADARG, "null stage / event");
+    OMNI_CUDA(cudaSetDevice(dst->dev));
+    OMNI_CUDA(cudaStreamWaitEvent(dst->stream, e->ev, 0));
+  });
+}
+
+omni_status omni_ipc_event_sync(omni_ipc_event* e) {
+  return guarded([&] {
+    OMNI_REQUIRE(e, OMNI_E_BADARG, "null event");
+    OMNI_CUDA(cudaEventSynchronize(e->ev));
   });
 }
 
