@@ -84,6 +84,15 @@ enum {
 };
 size_t omni_pipeline_output(omni_pipeline* p, uint64_t request_id, int32_t what, void* buf, size_t cap);
 
+/* Live serving (reference http_service.hpp:88-212): starts an
+ * Orchestrator loop on the device clock plus the HTTP/1.1 front end on
+ * `listen` ("host:port", port 0 = any free port; the bound port is returned).
+ * Routes: POST /v1/generate (JSON, or NDJSON waveform chunks when "stream"),
+ * GET /v1/health, GET /v1/metrics -- the reference's bodies and status codes. */
+omni_status omni_pipeline_serve_start(omni_pipeline* p, const char* listen, int32_t* port);
+/* Stops accepting, drains in-flight requests, stops the loop. */
+omni_status omni_pipeline_serve_stop(omni_pipeline* p);
+
 const char* omni_serve_last_error(void);
 
 #ifdef __cplusplus

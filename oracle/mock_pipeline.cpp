@@ -16,6 +16,7 @@
 #include "omni/bench.hpp"
 #include "omni/config.hpp"
 #include "omni/orchestrator.hpp"
+#include "omni/http_service.hpp"
 
 using namespace omni;
 
@@ -196,7 +197,46 @@ struct Tr {
 
 }  // namespace
 
+// live HTTP serving over the mock hooks (tests/test_http_service.py)
+struct MockServer {
+  FunctionRegistry reg;
+  std::unique_ptr<Orchestrator> orch;
+  std::unique_ptr<HttpService> http;
+};
+MockServer* g_server = nullptr;
+
 extern "C" {
+
+// Starts the control plane (wall clock) + HTTP front end over the reference's
+// mock hooks. Returns the bound port, or -1 (message in `err`).
+int oracle_mock_serve_start(const char* config_json, const char* listen, char* err, size_t cap) {
+  try {
+    if (g_server) throw std::runtime_error("already serving");
+    auto s = std::make_unique<MockServer>();
+    DeploymentPlan plan = parse_plan_text(config_json);
+    plan.clock_kind = "wall";
+    register_mock(s->reg);
+    s->orch = std::make_unique<Orchestrator>(plan, &s->reg);
+    s->orch->start();
+    s->orch->serve_async();
+    s->http = std::make_unique<HttpService>(*s->orch);
+    s->http->start(listen);
+    const int port = s->http->port();
+    g_server = s.release();
+    return port;
+  } catch (const std::exception& e) {
+    std::snprintf(err, cap, "%s", e.what());
+    return -1;
+  }
+}
+
+void oracle_mock_serve_stop() {
+  if (!g_server) return;
+  g_server->http->stop();
+  g_server->orch->shutdown(true);
+  delete g_server;
+  g_server = nullptr;
+}
 
 // Runs the workload through the new control plane with the mock hooks on a
 // virtual clock and writes the trace (same format as ref_harness). Returns the

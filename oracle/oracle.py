@@ -167,6 +167,10 @@ def codec_token(t: int, hsum: int, i: int) -> int:  # reference_pipeline.hpp:43-
 M64 = 0xFFFFFFFFFFFFFFFF
 
 
+def talker_generate(text, hidden):  # reference_pipeline.hpp:66-75
+    return [codec_token(t, sum(h), i) for t, h in zip(text, hidden) for i in range(4)]
+
+
 def mix64(x: int) -> int:  # csrc/dev/rng.h mix64 (splitmix64 finaliser)
     x = (x + 0x9E3779B97F4A7C15) & M64
     x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64

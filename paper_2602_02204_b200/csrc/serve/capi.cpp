@@ -10,6 +10,7 @@
 #include "omni/b200_pipeline.hpp"
 #include "omni/bench.hpp"
 #include "omni/config.hpp"
+#include "omni/http_service.hpp"
 #include "omni_serve.h"
 
 namespace {
@@ -61,6 +62,13 @@ struct omni_pipeline {
     std::vector<int32_t> text, codec, wave;
   };
   std::map<uint64_t, Captured> outputs;  // spec->capture: per-request outputs of the last bench
+  // live serving (omni_pipeline_serve_start): orchestrator loop + HTTP front end
+  std::unique_ptr<omni::Orchestrator> orch;
+  std::unique_ptr<omni::HttpService> http;
+  ~omni_pipeline() {
+    if (http) http->stop();
+    if (orch) orch->shutdown(false);
+  }
 };
 
 extern "C" {
@@ -88,6 +96,29 @@ omni_status omni_pipeline_create(const char* config_json, const omni_pipeline_op
     p->dev = std::make_unique<omni::B200Pipeline>(std::move(o));
     p->dev->register_into(p->reg);
     *out = p.release();
+  });
+}
+
+omni_status omni_pipeline_serve_start(omni_pipeline* p, const char* listen, int32_t* port) {
+  return guard([&] {
+    if (p->http) throw omni::AlreadyOpen("pipeline is already serving");
+    omni::DeploymentPlan plan = p->plan;
+    plan.clock_kind = "device";
+    p->orch = std::make_unique<omni::Orchestrator>(plan, &p->reg);
+    p->orch->start();
+    p->orch->serve_async();
+    p->http = std::make_unique<omni::HttpService>(*p->orch);
+    p->http->start(listen && *listen ? listen : "127.0.0.1:0");
+    if (port) *port = p->http->port();
+  });
+}
+
+omni_status omni_pipeline_serve_stop(omni_pipeline* p) {
+  return guard([&] {
+    if (p->http) p->http->stop();
+    if (p->orch) p->orch->shutdown(true);
+    p->http.reset();
+    p->orch.reset();
   });
 }
 

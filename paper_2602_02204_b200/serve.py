@@ -64,6 +64,15 @@ class Pipeline:
         check(self.lib.omni_pipeline_bench(self.h, C.byref(spec), C.byref(res)), self.lib)
         return res.as_dict()
 
+    def serve_start(self, listen: str = "127.0.0.1:0") -> int:
+        """Live serving: orchestrator loop (device clock) + HTTP front end; returns the port."""
+        port = C.c_int32()
+        check(self.lib.omni_pipeline_serve_start(self.h, listen.encode(), C.byref(port)), self.lib)
+        return port.value
+
+    def serve_stop(self) -> None:
+        check(self.lib.omni_pipeline_serve_stop(self.h), self.lib)
+
     def output(self, request_id: int, what: int):
         """Per-request output of the last bench(capture=True) run (OMNI_OUT_*)."""
         import numpy as np
