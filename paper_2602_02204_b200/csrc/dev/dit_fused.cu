@@ -4,7 +4,7 @@
 // Replaces the per-job denoise() of diffusion_engine.hpp:28-43 (called at
 // :98). The model is token-local: the S = 16 sample rows of a conditioning
 // token only ever interact with each other (attention is among a token's own
-// samples), so a tile of 256 rows (16 tokens) can run through the iteration
+// samples), so a tile of 128 rows (8 tokens) can run through the iteration
 // independently of every other tile. The kernel exploits that instead of
 // global barriers:
 //
@@ -19,10 +19,10 @@
 //    earlier phases of the tile. Items only wait on smaller indices, all
 //    held by resident CTAs, so the schedule cannot deadlock, and tiles at
 //    different phases overlap freely (no grid-wide barrier, no launch gaps);
-//  * GEMM items: 128 output features x 256 rows, swap-AB tcgen05 kind::f16
+//  * GEMM items: 128 output features x 128 rows, swap-AB tcgen05 kind::f16
 //    (weights = MMA A / TMEM lanes, rows = MMA B), TMA (SWIZZLE_128B) into a
 //    4-deep ring, one elected thread issues the MMAs, accumulators
-//    double-buffered in TMEM (2 x 256 columns) so an item's epilogue overlaps
+//    double-buffered in TMEM (2 x 128 columns) so an item's epilogue overlaps
 //    the next mainloop; weight tiles are requested BEFORE the dependency wait;
 //  * epilogue thread = one output feature, so each warp store covers one
 //    row's 32 consecutive features (one 64 / 128-byte line): TMEM ->
@@ -37,8 +37,12 @@
 //  * LN and attention items run on the four epilogue warps (same arithmetic
 //    as the standalone kernels in dit_kernels.cu).
 //
-// Warp roles (192 threads): 0 = scheduler + TMA producer, 1 = MMA issuer,
-// 2..5 = epilogue / LN / attention (TMEM lane quadrant = warp % 4).
+// Warp roles (320 threads): 0 = scheduler + TMA producer, 1 = MMA issuer,
+// 2..9 = epilogue / LN / attention (TMEM lane quadrant = warp % 4; the two
+// warps of a quadrant take alternate 16-row chunks of an item). Measured
+// (profiles/r02_dit_fused_v7.txt): 128-row tiles halve every item's
+// mainloop and the 8 epilogue warps halve its epilogue, which together set
+// the per-layer latency of a row tile through the dependency chain.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -53,11 +57,17 @@
 namespace omni_dev {
 namespace {
 
-constexpr int kThreadsF = 192;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, each half of an item's 16-row chunks
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kThreadsF = 64 + kEpiThreads;
+constexpr int kChunks = kDitTileRows / 16;          // 16-row chunks (one token each) per item
+constexpr int kMyChunks = kChunks / (kEpiWarps / 4);  // chunks per epilogue warp
 constexpr int kQ = 1;  // item ring depth: fetch item i+1 once item i started (deeper run-ahead
                        // strands short LN / attention items behind long GEMM items of the same CTA)
 constexpr int kABytes = kDitFeat * 64 * 2;      // weight tile (128 features x 64 k)
-constexpr int kBBytes = kDitTileRows * 64 * 2;  // row tile (256 rows x 64 k)
+constexpr int kBBytes = kDitTileRows * 64 * 2;  // row tile (128 rows x 64 k)
+static_assert(kEpiWarps == kDitTileTok, "attention items: one epilogue warp per token of the tile");
+static_assert(16 % kEpiWarps == 0 && kChunks % 2 == 0, "LN rows / chunk halves");
 constexpr uint32_t kIdesc = idesc_bf16_f32(kDitFeat, kDitTileRows);
 constexpr int kStageBytes = kABytes + kBBytes;
 
@@ -85,7 +95,7 @@ __device__ __forceinline__ PhaseInfo phase_info(const DitFusedParams& p, int ph)
   switch ((ph - 1) % 7) {
     case 0: return {K_LN1, l, kDitTileTok, kDitTileTok};
     case 1: return {K_QKV, l, 3 * nf, 3 * nf};
-    case 2: return {K_ATT, l, 4 * p.H, 4 * p.H};
+    case 2: return {K_ATT, l, p.H, p.H};  // one head of every token of the tile (a warp per token)
     case 3: return {K_O, l, nf, nf};
     case 4: return {K_LN2, l, kDitTileTok, kDitTileTok};
     case 5: return {K_UP, l, p.ff / kDitFeat, p.ff / kDitFeat};
@@ -133,17 +143,17 @@ __device__ __forceinline__ void st_f4_cg(float* p, float a, float b, float c, fl
 __device__ __forceinline__ void st_bf16x4(__nv_bfloat16* p, float a, float b, float c, float d) {
   *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16x2(a, b), pack_bf16x2(c, d));
 }
-__device__ __forceinline__ void ep_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void ep_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
 
-// a = bf16(LN(h) * (1 + scale) + shift) for 4 consecutive rows of one token
+// a = bf16(LN(h) * (1 + scale) + shift) for NR consecutive rows of one token
 // (one warp; the token's modulation rows preloaded), same arithmetic as
 // dit_ln_mod_kernel. The two rows of a pair have their loads in flight together.
-template <int PER>
-__device__ __forceinline__ void ln_rows4(const float* hr, bool mod, const float4 (&sc)[PER], const float4 (&sh)[PER],
+template <int PER, int NR>
+__device__ __forceinline__ void ln_rows(const float* hr, bool mod, const float4 (&sc)[PER], const float4 (&sh)[PER],
                                          __nv_bfloat16* out_row, int lane) {
   constexpr int d = PER * 128;
 #pragma unroll 1
-  for (int q0 = 0; q0 < 4; q0 += 2) {
+  for (int q0 = 0; q0 < NR; q0 += 2) {
     float4 x[2][PER];
 #pragma unroll
     for (int q = 0; q < 2; ++q)
@@ -284,7 +294,7 @@ __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int to
 // token c (rotated one per chunk).
 template <int KIND, int MODE>
 __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta, int row0, int ft, int tix, int quad,
-                                           int lane, float (&aux)[16], int step) {
+                                           int half, int lane, float (&aux)[16], int step) {
   constexpr bool kGated = KIND == K_O || KIND == K_DOWN;
   const int g4 = lane >> 2, t4 = lane & 3;
   const int fw = ft * kDitFeat + quad * 32 + 4 * g4;  // first of my 4 features after the transpose
@@ -303,14 +313,15 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
       for (int m = 0; m < 4; ++m)
         dst[m] = __ldcg(reinterpret_cast<const float4*>(part4 + (size_t)(cc * 16 + 4 * m + t4) * kDitFeat));
   };
+  // this warp's chunks: c = half, half + 2, ... (its quadrant partner takes the others)
   float4 nx[4] = {};
-  load_side(0, nx);
+  load_side(half, nx);
 #pragma unroll 1
-  for (int c = 0; c < kDitTileRows / 16; ++c) {
+  for (int c = half; c < kChunks; c += 2) {
     float4 ld[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) ld[m] = nx[m];
-    if (c + 1 < kDitTileRows / 16) load_side(c + 1, nx);
+    if (c + 2 < kChunks) load_side(c + 2, nx);
     float v[16];
     tmem_ld16(ta + c * 16, v);
     const int rb = row0 + c * 16;  // rows of token row0 / 16 + c
@@ -360,7 +371,7 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
     }
     if constexpr (kGated)
 #pragma unroll
-      for (int k = 0; k < 15; ++k) aux[k] = aux[k + 1];  // static indices: aux stays in registers
+      for (int k = 0; k < kMyChunks - 1; ++k) aux[k] = aux[k + 1];  // static indices: aux stays in registers
   }
 }
 
@@ -373,7 +384,7 @@ struct Smem {
   int last_flag, last_old;
   int item_start[kDitMaxPhases + 1];  // global item index where (step, phase) tp starts
   int unit_cum[kDitMaxPhases + 1];    // per-tile units completed before tp
-  float attnP[4][16][17];
+  float attnP[kEpiWarps][16][17];
 };
 
 template <int PER, int STAGES>
@@ -390,8 +401,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&sm.full[s], 1), mbar_init(&sm.empty[s], 1);
-    for (int a = 0; a < 2; ++a) mbar_init(&sm.acc_full[a], 1), mbar_init(&sm.acc_empty[a], 4);
-    for (int q = 0; q < kQ; ++q) mbar_init(&sm.q_full[q], 1), mbar_init(&sm.q_empty[q], 1 + 4);
+    for (int a = 0; a < 2; ++a) mbar_init(&sm.acc_full[a], 1), mbar_init(&sm.acc_empty[a], kEpiWarps);
+    for (int q = 0; q < kQ; ++q) mbar_init(&sm.q_full[q], 1), mbar_init(&sm.q_empty[q], 1 + kEpiWarps);
     int items = 0, units = 0;
     for (int tp = 0; tp < TP; ++tp) {
       const PhaseInfo ph = phase_info(p, tp % P);
@@ -527,9 +538,10 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
     }
   } else {
     // ---------------- epilogue / LN / attention (warps 2..5) ----------------
-    const int ew = warp - 2;          // 0..3 worker index
+    const int ew = warp - 2;          // 0..7 worker index
+    const int half = ew >> 2;         // which half of the item's chunks (quadrant partner: ew ^ 4)
     const int quad = warp & 3;        // TMEM lane quadrant this warp may access
-    const int et = ew * 32 + lane;    // 0..127
+    const int et = ew * 32 + lane;    // 0..255
     const int fl = quad * 32 + lane;  // output feature (TMEM lane) of this thread within a tile
     const int ld_mod = p.L * 6 * p.d;
     uint32_t qi = 0, gi = 0;
@@ -559,9 +571,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
           const int goff = it.layer * 6 * p.d + (it.kind == K_O ? 2 : 5) * p.d + f;
           int id[16];
 #pragma unroll
-          for (int c = 0; c < 16; ++c) id[c] = p.toks[tok0 + c].id;
+          for (int c = 0; c < kMyChunks; ++c) id[c] = p.toks[tok0 + half + 2 * c].id;  // my chunks' tokens
 #pragma unroll
-          for (int c = 0; c < 16; ++c) aux[c] = mod_t[(size_t)id[c] * ld_mod + goff];
+          for (int c = 0; c < kMyChunks; ++c) aux[c] = mod_t[(size_t)id[c] * ld_mod + goff];
         }
         const int acc = gi & 1;
         mbar_wait_sleep(&sm.acc_full[acc], (gi >> 1) & 1);
@@ -586,15 +598,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         }
         const uint32_t ta = tmem + acc * kDitTileRows + (static_cast<uint32_t>(quad * 32) << 16);
         switch (it.kind) {  // once per item: the chunk loop is specialised per kind (no jump table inside)
-          case K_IN: epi_chunks<K_IN, 0>(p, ta, row0, ft, tix, quad, lane, aux, it.step); break;
-          case K_QKV: epi_chunks<K_QKV, 0>(p, ta, row0, ft, tix, quad, lane, aux, it.step); break;
-          case K_UP: epi_chunks<K_UP, 0>(p, ta, row0, ft, tix, quad, lane, aux, it.step); break;
-          case K_OUT: epi_chunks<K_OUT, 0>(p, ta, row0, ft, tix, quad, lane, aux, it.step); break;
-          case K_O: epi_chunks<K_O, 0>(p, ta, row0, ft, tix, quad, lane, aux, it.step); break;
+          case K_IN: epi_chunks<K_IN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_QKV: epi_chunks<K_QKV, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_UP: epi_chunks<K_UP, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_OUT: epi_chunks<K_OUT, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_O: epi_chunks<K_O, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
           default:
-            if (mode == 1) epi_chunks<K_DOWN, 1>(p, ta, row0, ft, tix, quad, lane, aux, it.step);
-            else if (mode == 2) epi_chunks<K_DOWN, 2>(p, ta, row0, ft, tix, quad, lane, aux, it.step);
-            else epi_chunks<K_DOWN, 0>(p, ta, row0, ft, tix, quad, lane, aux, it.step);
+            if (mode == 1) epi_chunks<K_DOWN, 1>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
+            else if (mode == 2) epi_chunks<K_DOWN, 2>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
+            else epi_chunks<K_DOWN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
             break;
         }
         if (p.trace && et == 0) p.trace[(size_t)it.idx * 8 + 5] = globaltimer();
@@ -629,11 +641,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         }
         ep_bar();
         if (it.kind == K_ATT) {
-          const int quarter = it.j / p.H, h = it.j % p.H;
-          attn_token_head(p.qkv, tok0 + quarter * 4 + ew, h, p.d, p.o, sm.attnP[ew], lane);
+          attn_token_head(p.qkv, tok0 + ew, it.j, p.d, p.o, sm.attnP[ew], lane);  // warp = token, item = head
         } else {
-          const int row = (tok0 + it.j) * 16 + ew * 4;
-          ln_rows4<PER>(p.h + (size_t)row * p.d, mod, sc, sh, p.a + (size_t)row * p.d, lane);
+          constexpr int kRows = 16 / kEpiWarps;  // rows of the token per warp
+          const int row = (tok0 + it.j) * 16 + ew * kRows;
+          ln_rows<PER, kRows>(p.h + (size_t)row * p.d, mod, sc, sh, p.a + (size_t)row * p.d, lane);
         }
       }
       // completion: publish this item's writes (generic proxy; the consumers
@@ -657,7 +669,7 @@ template <int STAGES>
 constexpr size_t smem_bytes() {
   return 1024 + (size_t)STAGES * kStageBytes + sizeof(Smem);
 }
-static_assert(smem_bytes<4>() <= 227 * 1024, "4-stage ring must fit");
+static_assert(smem_bytes<6>() <= 227 * 1024, "6-stage ring must fit");
 
 template <int PER, int STAGES>
 cudaError_t launch_fused(const DitFusedParams& p, int ctas, cudaStream_t st) {
@@ -673,11 +685,11 @@ cudaError_t launch_fused(const DitFusedParams& p, int ctas, cudaStream_t st) {
 int dit_fused_items(int n_rt, int d, int H, int ff, int L, int T, int down_split) {
   const int nf = d / kDitFeat;
   const int per_step =
-      nf + L * (kDitTileTok + 3 * nf + 4 * H + nf + kDitTileTok + ff / kDitFeat + nf * down_split) + kDitTileTok + 1;
+      nf + L * (kDitTileTok + 3 * nf + H + nf + kDitTileTok + ff / kDitFeat + nf * down_split) + kDitTileTok + 1;
   return per_step * T * n_rt;
 }
 
-size_t dit_fused_smem(int stages) { return stages == 3 ? smem_bytes<3>() : smem_bytes<4>(); }
+size_t dit_fused_smem(int stages) { return stages == 6 ? smem_bytes<6>() : smem_bytes<4>(); }
 
 bool dit_fused_supported(int d, int C, int H, int ff, int L, int T) {
   return (d == 256 || d == 512 || d == 1024) && ff % kDitFeat == 0 && C == 64 && H * 128 == d &&
@@ -688,11 +700,11 @@ cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStr
   if (!dit_fused_supported(p.d, p.C, p.H, p.ff, p.L, p.T) || p.down_split < 1 || p.down_split > 2 ||
       (p.ff / 64) % p.down_split != 0 || p.n_rt <= 0)
     return cudaErrorInvalidValue;
-  const bool s3 = stages == 3;
+  const bool s6 = stages == 6;
   switch (p.d / 128) {
-    case 2: return s3 ? launch_fused<2, 3>(p, ctas, st) : launch_fused<2, 4>(p, ctas, st);
-    case 4: return s3 ? launch_fused<4, 3>(p, ctas, st) : launch_fused<4, 4>(p, ctas, st);
-    case 8: return s3 ? launch_fused<8, 3>(p, ctas, st) : launch_fused<8, 4>(p, ctas, st);
+    case 2: return s6 ? launch_fused<2, 6>(p, ctas, st) : launch_fused<2, 4>(p, ctas, st);
+    case 4: return s6 ? launch_fused<4, 6>(p, ctas, st) : launch_fused<4, 4>(p, ctas, st);
+    case 8: return s6 ? launch_fused<8, 6>(p, ctas, st) : launch_fused<8, 4>(p, ctas, st);
   }
   return cudaErrorInvalidValue;
 }

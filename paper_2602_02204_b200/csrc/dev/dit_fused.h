@@ -12,8 +12,8 @@ namespace omni_dev {
 
 constexpr int kDitMaxLayers = 8;
 constexpr int kDitMaxPhases = 256;  // T * (3 + 7 L)
-constexpr int kDitTileRows = 256;  // rows of one row tile (16 tokens x 16 samples) = MMA N
-constexpr int kDitTileTok = 16;
+constexpr int kDitTileRows = 128;  // rows of one row tile (8 tokens x 16 samples) = MMA N
+constexpr int kDitTileTok = 8;
 constexpr int kDitFeat = 128;      // output features per GEMM item = MMA M (TMEM lanes)
 
 // TMA descriptors of one DiT stage, resident in global memory (written once
@@ -52,7 +52,7 @@ int dit_fused_items(int n_rt, int d, int H, int ff, int L, int T, int down_split
 size_t dit_fused_smem(int stages);
 // Model shapes the fused iteration covers (others run one kernel per op).
 bool dit_fused_supported(int d, int C, int H, int ff, int L, int T);
-// stages: TMA ring depth (3 or 4); ctas: persistent grid.
+// stages: TMA ring depth (4 or 6); ctas: persistent grid.
 cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStream_t st);
 
 }  // namespace omni_dev
