@@ -370,6 +370,12 @@ __device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const A
   const int n_chunks = (kend + CHUNK - 1) / CHUNK;
   const int warp = warp_id(), lane = lane_id();
   const int g = lane >> 2, t4 = lane & 3;
+  // split-KV: this CTA owns chunks [c_lo, c_hi) of the block's keys
+  const int parts = attn_split_parts(blk.split), part = attn_split_part(blk.split);
+  const bool split = parts > 1;
+  const int per = split ? (n_chunks + parts - 1) / parts : n_chunks;
+  const int c_lo = split ? part * per : 0;
+  const int c_hi = split ? min(n_chunks, c_lo + per) : n_chunks;
 
   if (threadIdx.x == 0) {
     mbar_init(&sm.bar[0], 1);
@@ -393,14 +399,14 @@ __device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const A
   };
   if (threadIdx.x == 0) {
     if (tr) tr[0] = globaltimer();
-    issue(0, 0, 0);
-    if (n_chunks > 1) issue(1, 1, 0);
+    issue(c_lo, 0, 0);
+    if (c_lo + 1 < c_hi) issue(c_lo + 1, 1, 0);
   }
   dep();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
   if (threadIdx.x == 0) {
-    issue(0, 0, 1);
-    if (n_chunks > 1) issue(1, 1, 1);
+    issue(c_lo, 0, 1);
+    if (c_lo + 1 < c_hi) issue(c_lo + 1, 1, 1);
   }
   __syncthreads();  // barrier init visible before any wait
 
@@ -434,10 +440,10 @@ __device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const A
 #pragma unroll
   for (int nd = 0; nd < 16; ++nd) o[nd][0] = o[nd][1] = o[nd][2] = o[nd][3] = 0.f;
 
-  for (int c = 0; c < n_chunks; ++c) {
-    const int buf = c & 1;
-    mbar_wait(&sm.bar[buf], (c >> 1) & 1);
-    if (tr && c == 0 && threadIdx.x == 0) tr[3] = globaltimer();
+  for (int c = c_lo; c < c_hi; ++c) {
+    const int buf = (c - c_lo) & 1;
+    mbar_wait(&sm.bar[buf], ((c - c_lo) >> 1) & 1);
+    if (tr && c == c_lo && threadIdx.x == 0) tr[3] = globaltimer();
     const int k0 = c * CHUNK + warp * 16;  // this warp's first key
     // warp-uniform skip: no key of the slab is visible to any row of the block
     const int blk_qmax = ed.pos0 + blk.tok0 + blk.ntok - 1;
@@ -538,7 +544,7 @@ __device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const A
       }
     }
     __syncthreads();  // every warp is done with `buf`
-    if (threadIdx.x == 0 && c + 2 < n_chunks) {
+    if (threadIdx.x == 0 && c + 2 < c_hi) {
       issue(c + 2, buf, 0);
       issue(c + 2, buf, 1);
     }
@@ -576,10 +582,56 @@ __device__ __forceinline__ void attention_block_mma(int blk_idx, int kh, const A
       a0 += v.x * f;
       a1 += v.y * f;
     }
+    if (split) {  // this part's unnormalised state -> scratch; the last part merges
+      float* sp = s.split_part +
+                  ((((size_t)attn_split_group(blk.split) * n_kv + kh) * kAttnMaxParts + part) * 16 + r) * (HD + 2);
+      *reinterpret_cast<float2*>(sp + d0) = make_float2(a0, a1);
+      if (d0 == 0) sp[HD] = mt, sp[HD + 1] = lt;
+      continue;
+    }
     const float inv = 1.f / lt;
     const int tok = blk.tok0 + r / group, hq = kh * group + r % group;
     *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + d0) =
         __floats2bfloat162_rn(a0 * inv, a1 * inv);
+  }
+  if (split) {
+    // last-arriver merge in FIXED part order (bit-identical whichever part
+    // finishes last); P depends only on the sequence's own context length,
+    // so a sequence's output does not depend on the rest of the batch
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    int* cnt = s.split_cnt + (size_t)attn_split_group(blk.split) * n_kv + kh;
+    if (threadIdx.x == 0) {
+      const int old = atomicAdd(cnt, 1);
+      s_last = old == parts - 1;
+      if (s_last) *cnt = 0;  // ready for the next launch (every part has arrived)
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const float* base =
+          s.split_part + (((size_t)attn_split_group(blk.split) * n_kv + kh) * kAttnMaxParts) * 16 * (HD + 2);
+      for (int idx = threadIdx.x; idx < nq * (HD / 2); idx += W * 32) {
+        const int r = idx / (HD / 2), d0 = (idx % (HD / 2)) * 2;
+        float mt = -INFINITY;
+        for (int pp = 0; pp < parts; ++pp) mt = fmaxf(mt, __ldcg(base + ((size_t)pp * 16 + r) * (HD + 2) + HD));
+        float lt = 0.f, a0 = 0.f, a1 = 0.f;
+        for (int pp = 0; pp < parts; ++pp) {
+          const float* sp = base + ((size_t)pp * 16 + r) * (HD + 2);
+          const float mp = __ldcg(sp + HD);
+          const float f = mp == -INFINITY ? 0.f : exp2f(mp - mt);
+          lt += __ldcg(sp + HD + 1) * f;
+          const float2 v = __ldcg(reinterpret_cast<const float2*>(sp + d0));
+          a0 += v.x * f;
+          a1 += v.y * f;
+        }
+        const float inv = 1.f / lt;
+        const int tok = blk.tok0 + r / group, hq = kh * group + r % group;
+        *reinterpret_cast<__nv_bfloat162*>(out + (size_t)(ed.row0 + tok) * n_heads * HD + hq * HD + d0) =
+            __floats2bfloat162_rn(a0 * inv, a1 * inv);
+      }
+    }
   }
   if (tr && threadIdx.x == 0) tr[5] = globaltimer();
 }

@@ -37,8 +37,18 @@ struct AttnBlockDesc {  // one attention CTA row: tokens [tok0, tok0+ntok) of an
   int32_t entry;
   int32_t tok0;
   int32_t ntok;
-  int32_t pad;
+  // split-KV (long contexts): bits 0-7 part, 8-15 parts P
+  // (P <= 1: the block owns all of its keys), 16-31 split group (scratch slot)
+  int32_t split;
 };
+constexpr int kAttnSplitChunks = 8;   // a split part covers <= 8 chunks of 128 keys
+constexpr int kAttnMaxParts = 8;
+__host__ __device__ inline int attn_split_part(int32_t v) { return v & 0xff; }
+__host__ __device__ inline int attn_split_parts(int32_t v) { return (v >> 8) & 0xff; }
+__host__ __device__ inline int attn_split_group(int32_t v) { return (v >> 16) & 0xffff; }
+__host__ __device__ inline int32_t attn_split_pack(int part, int parts, int group) {
+  return part | parts << 8 | group << 16;
+}
 
 struct ArStepDev {
   const ArEntryDesc* entries;
@@ -47,6 +57,11 @@ struct ArStepDev {
   const int32_t* dec_entries;  // [n_dec] entry index of each decode row
   const AttnBlockDesc* attn_blocks;
   int32_t max_pages;
+  // split-KV scratch: [group][kv head][part][16 rows][kHeadDim + 2] fp32
+  // (unnormalised O, running max, sum) and [group][kv head] arrival counters
+  // (zero between launches: the last arriver resets its counter)
+  float* split_part;
+  int* split_cnt;
 };
 
 cudaError_t launch_embed(const ArStepDev& s, int n_rows, const __nv_bfloat16* emb,

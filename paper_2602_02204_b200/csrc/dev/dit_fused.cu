@@ -60,16 +60,23 @@ namespace {
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, each half of an item's 16-row chunks
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreadsF = 64 + kEpiThreads;
-constexpr int kChunks = kDitTileRows / 16;          // 16-row chunks (one token each) per item
-constexpr int kMyChunks = kChunks / (kEpiWarps / 4);  // chunks per epilogue warp
 constexpr int kQ = 1;  // item ring depth: fetch item i+1 once item i started (deeper run-ahead
                        // strands short LN / attention items behind long GEMM items of the same CTA)
-constexpr int kABytes = kDitFeat * 64 * 2;      // weight tile (128 features x 64 k)
-constexpr int kBBytes = kDitTileRows * 64 * 2;  // row tile (128 rows x 64 k)
-static_assert(kEpiWarps == kDitTileTok, "attention items: one epilogue warp per token of the tile");
-static_assert(16 % kEpiWarps == 0 && kChunks % 2 == 0, "LN rows / chunk halves");
-constexpr uint32_t kIdesc = idesc_bf16_f32(kDitFeat, kDitTileRows);
-constexpr int kStageBytes = kABytes + kBBytes;
+constexpr int kABytes = kDitFeat * 64 * 2;  // weight tile (128 features x 64 k)
+static_assert(16 % kEpiWarps == 0, "LN rows per warp");
+
+// Row-tile geometry: TR rows = TR / 16 tokens = MMA N (128 or 256).
+template <int TR>
+struct Tile {
+  static constexpr int rows = TR, tok = TR / 16;
+  static constexpr int chunks = TR / 16;                  // 16-row chunks (one token each) per item
+  static constexpr int my_chunks = chunks / (kEpiWarps / 4);  // chunks per epilogue warp
+  static constexpr int b_bytes = TR * 64 * 2;             // row tile (TR rows x 64 k)
+  static constexpr int stage_bytes = kABytes + b_bytes;
+  static constexpr int att_groups = tok / kEpiWarps;      // attention items per head (a warp per token)
+  static constexpr uint32_t idesc = idesc_bf16_f32(kDitFeat, TR);
+  static_assert(tok % kEpiWarps == 0 && chunks % 2 == 0, "attention groups / chunk halves");
+};
 
 enum Kind : int { K_IN = 0, K_LN1, K_QKV, K_ATT, K_O, K_LN2, K_UP, K_DOWN, K_LNF, K_OUT, K_END };
 
@@ -86,18 +93,20 @@ struct PhaseInfo {
 };
 
 // Phase ph of one Euler step (P = 3 + 7 L phases); items / units per row tile.
+template <int TR>
 __device__ __forceinline__ PhaseInfo phase_info(const DitFusedParams& p, int ph) {
+  using T = Tile<TR>;
   const int nf = p.d / kDitFeat, P = 3 + 7 * p.L;
   if (ph == 0) return {K_IN, 0, nf, nf};
-  if (ph == P - 2) return {K_LNF, 0, kDitTileTok, kDitTileTok};
+  if (ph == P - 2) return {K_LNF, 0, T::tok, T::tok};
   if (ph == P - 1) return {K_OUT, 0, 1, 1};
   const int l = (ph - 1) / 7;
   switch ((ph - 1) % 7) {
-    case 0: return {K_LN1, l, kDitTileTok, kDitTileTok};
+    case 0: return {K_LN1, l, T::tok, T::tok};
     case 1: return {K_QKV, l, 3 * nf, 3 * nf};
-    case 2: return {K_ATT, l, p.H, p.H};  // one head of every token of the tile (a warp per token)
+    case 2: return {K_ATT, l, p.H * T::att_groups, p.H * T::att_groups};  // (head, 8-token group)
     case 3: return {K_O, l, nf, nf};
-    case 4: return {K_LN2, l, kDitTileTok, kDitTileTok};
+    case 4: return {K_LN2, l, T::tok, T::tok};
     case 5: return {K_UP, l, p.ff / kDitFeat, p.ff / kDitFeat};
     default: return {K_DOWN, l, nf * p.down_split, nf};
   }
@@ -210,21 +219,25 @@ __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int to
   uint2 vr[S];
 #pragma unroll
   for (int j = 0; j < S; ++j) vr[j] = __ldcg(reinterpret_cast<const uint2*>(V + (size_t)j * ld + 4 * lane));
-  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+  // every Q / K fragment in flight at once (one L2 round trip, not one per k-step)
+  uint32_t qa[HD / 16][4], kb[HD / 16][4];
 #pragma unroll
   for (int kk = 0; kk < HD / 16; ++kk) {
     const int col = kk * 16 + 2 * t;
-    uint32_t a[4];
-    a[0] = ldcg_u32(Q + (size_t)g * ld + col);
-    a[1] = ldcg_u32(Q + (size_t)(g + 8) * ld + col);
-    a[2] = ldcg_u32(Q + (size_t)g * ld + col + 8);
-    a[3] = ldcg_u32(Q + (size_t)(g + 8) * ld + col + 8);
-    const uint32_t b00 = ldcg_u32(K + (size_t)g * ld + col);
-    const uint32_t b01 = ldcg_u32(K + (size_t)g * ld + col + 8);
-    const uint32_t b10 = ldcg_u32(K + (size_t)(g + 8) * ld + col);
-    const uint32_t b11 = ldcg_u32(K + (size_t)(g + 8) * ld + col + 8);
-    mma_bf16_16816(c0, a, b00, b01);
-    mma_bf16_16816(c1, a, b10, b11);
+    qa[kk][0] = ldcg_u32(Q + (size_t)g * ld + col);
+    qa[kk][1] = ldcg_u32(Q + (size_t)(g + 8) * ld + col);
+    qa[kk][2] = ldcg_u32(Q + (size_t)g * ld + col + 8);
+    qa[kk][3] = ldcg_u32(Q + (size_t)(g + 8) * ld + col + 8);
+    kb[kk][0] = ldcg_u32(K + (size_t)g * ld + col);
+    kb[kk][1] = ldcg_u32(K + (size_t)g * ld + col + 8);
+    kb[kk][2] = ldcg_u32(K + (size_t)(g + 8) * ld + col);
+    kb[kk][3] = ldcg_u32(K + (size_t)(g + 8) * ld + col + 8);
+  }
+  float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int kk = 0; kk < HD / 16; ++kk) {
+    mma_bf16_16816(c0, qa[kk], kb[kk][0], kb[kk][1]);
+    mma_bf16_16816(c1, qa[kk], kb[kk][2], kb[kk][3]);
   }
   const float scale = rsqrtf((float)HD);
   float r0[4] = {c0[0] * scale, c0[1] * scale, c1[0] * scale, c1[1] * scale};
@@ -292,7 +305,7 @@ __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int to
 // 8 / 16 bytes per thread (4x fewer store instructions than one feature per
 // thread). aux: IN pos_emb[sample][own feature]; O / DOWN the adaLN gate of
 // token c (rotated one per chunk).
-template <int KIND, int MODE>
+template <int TR, int KIND, int MODE>
 __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta, int row0, int ft, int tix, int quad,
                                            int half, int lane, float (&aux)[16], int step) {
   constexpr bool kGated = KIND == K_O || KIND == K_DOWN;
@@ -300,7 +313,8 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
   const int fw = ft * kDitFeat + quad * 32 + 4 * g4;  // first of my 4 features after the transpose
   const int d = p.d;
   if (KIND == K_OUT && quad * 32 >= p.C) return;  // OUT: the C channels are the first C lanes
-  const float* part4 = p.part + (size_t)tix * kDitTileRows * kDitFeat + quad * 32 + 4 * g4;
+  constexpr int kChunks = Tile<TR>::chunks, kMyChunks = Tile<TR>::my_chunks;
+  const float* part4 = p.part + (size_t)tix * TR * kDitFeat + quad * 32 + 4 * g4;
   // side inputs (x / partner partial) of chunk cc, my 4 rows 4m + t4
   // (post-transpose layout); the next chunk's are in flight
   auto load_side = [&](int cc, float4(&dst)[4]) {
@@ -387,9 +401,12 @@ struct Smem {
   float attnP[kEpiWarps][16][17];
 };
 
-template <int PER, int STAGES>
+template <int PER, int STAGES, int TR>
 __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_constant__ DitFusedParams p) {
   static_assert(STAGES <= 8, "barrier slots");
+  using Tl = Tile<TR>;
+  constexpr int kBBytes = Tl::b_bytes, kStageBytes = Tl::stage_bytes;
+  constexpr uint32_t kIdesc = Tl::idesc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -405,7 +422,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
     for (int q = 0; q < kQ; ++q) mbar_init(&sm.q_full[q], 1), mbar_init(&sm.q_empty[q], 1 + kEpiWarps);
     int items = 0, units = 0;
     for (int tp = 0; tp < TP; ++tp) {
-      const PhaseInfo ph = phase_info(p, tp % P);
+      const PhaseInfo ph = phase_info<TR>(p, tp % P);
       sm.item_start[tp] = items;
       sm.unit_cum[tp] = units;
       items += ph.items * p.n_rt;
@@ -426,6 +443,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
     // ---------------- scheduler + TMA producer ----------------
     if (lane == 0) {
       const DitMaps* mp = p.maps;
+      constexpr int ti = TR == 256 ? 1 : 0;  // activation maps with TR-row boxes
       const uint64_t pol = policy_evict_last();  // weights re-read by every row tile; activations hot
       int tp = 0;
       uint32_t qi = 0, kbi = 0;
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         it.kind = K_END;
         if (idx < total) {
           while (idx >= sm.item_start[tp + 1]) ++tp;
-          const PhaseInfo ph = phase_info(p, tp % P);
+          const PhaseInfo ph = phase_info<TR>(p, tp % P);
           const int local = idx - sm.item_start[tp];
           it.kind = ph.kind;
           it.layer = ph.layer;
@@ -463,20 +481,20 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         const CUtensorMap* xm;
         int nkb, kb0 = 0, wrow = it.j * kDitFeat;
         switch (it.kind) {
-          case K_IN: wm = &mp->w_in; xm = &mp->x_x; nkb = p.C / 64; break;
-          case K_QKV: wm = &mp->wqkv[it.layer]; xm = &mp->x_a; nkb = p.d / 64; break;
-          case K_O: wm = &mp->wo[it.layer]; xm = &mp->x_o; nkb = p.d / 64; break;
-          case K_UP: wm = &mp->w1[it.layer]; xm = &mp->x_a; nkb = p.d / 64; break;
+          case K_IN: wm = &mp->w_in; xm = &mp->x_x[ti]; nkb = p.C / 64; break;
+          case K_QKV: wm = &mp->wqkv[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
+          case K_O: wm = &mp->wo[it.layer]; xm = &mp->x_o[ti]; nkb = p.d / 64; break;
+          case K_UP: wm = &mp->w1[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
           case K_DOWN:
             wm = &mp->w2[it.layer];
-            xm = &mp->x_u;
+            xm = &mp->x_u[ti];
             nkb = p.ff / 64 / p.down_split;
             kb0 = (it.j % p.down_split) * nkb;
             wrow = (it.j / p.down_split) * kDitFeat;
             break;
-          default: wm = &mp->w_out; xm = &mp->x_a; nkb = p.d / 64; wrow = 0; break;
+          default: wm = &mp->w_out; xm = &mp->x_a[ti]; nkb = p.d / 64; wrow = 0; break;
         }
-        const int xrow = it.r * kDitTileRows;
+        const int xrow = it.r * TR;
         const int pre = nkb < STAGES ? nkb : STAGES;
         for (int i = 0; i < pre; ++i) {  // weights first: they never depend on another item
           const uint32_t k = kbi + i;
@@ -519,7 +537,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         const int acc = gi & 1;
         mbar_wait_sleep(&sm.acc_empty[acc], ((gi >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t td = tmem + acc * kDitTileRows;
+        const uint32_t td = tmem + acc * TR;
         for (int i = 0; i < nkb; ++i) {
           const uint32_t k = kbi + i;
           const int s = k % STAGES;
@@ -554,8 +572,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
       ++qi;
       if (it.kind == K_END) break;
       const float* mod_t = p.mod_table + (size_t)it.step * p.vocab * ld_mod;
-      const int row0 = it.r * kDitTileRows;
-      const int tok0 = it.r * kDitTileTok;
+      const int row0 = it.r * TR;
+      const int tok0 = it.r * Tl::tok;
       if (is_gemm(it.kind)) {
         const bool gated = it.kind == K_O || it.kind == K_DOWN;
         const int ft = it.kind == K_DOWN ? it.j / p.down_split : it.kind == K_OUT ? 0 : it.j;
@@ -569,11 +587,11 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
           for (int jj = 0; jj < 16; ++jj) aux[jj] = bf2f(p.pos_emb[(size_t)jj * p.d + f]);  // row % 16 = sample
         } else if (gated) {
           const int goff = it.layer * 6 * p.d + (it.kind == K_O ? 2 : 5) * p.d + f;
-          int id[16];
+          int id[Tile<TR>::my_chunks];
 #pragma unroll
-          for (int c = 0; c < kMyChunks; ++c) id[c] = p.toks[tok0 + half + 2 * c].id;  // my chunks' tokens
+          for (int c = 0; c < Tl::my_chunks; ++c) id[c] = p.toks[tok0 + half + 2 * c].id;  // my chunks' tokens
 #pragma unroll
-          for (int c = 0; c < kMyChunks; ++c) aux[c] = mod_t[(size_t)id[c] * ld_mod + goff];
+          for (int c = 0; c < Tl::my_chunks; ++c) aux[c] = mod_t[(size_t)id[c] * ld_mod + goff];
         }
         const int acc = gi & 1;
         mbar_wait_sleep(&sm.acc_full[acc], (gi >> 1) & 1);
@@ -596,17 +614,17 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
             ep_bar();
           }
         }
-        const uint32_t ta = tmem + acc * kDitTileRows + (static_cast<uint32_t>(quad * 32) << 16);
+        const uint32_t ta = tmem + acc * TR + (static_cast<uint32_t>(quad * 32) << 16);
         switch (it.kind) {  // once per item: the chunk loop is specialised per kind (no jump table inside)
-          case K_IN: epi_chunks<K_IN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_QKV: epi_chunks<K_QKV, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_UP: epi_chunks<K_UP, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_OUT: epi_chunks<K_OUT, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_O: epi_chunks<K_O, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_IN: epi_chunks<TR, K_IN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_QKV: epi_chunks<TR, K_QKV, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_UP: epi_chunks<TR, K_UP, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_OUT: epi_chunks<TR, K_OUT, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_O: epi_chunks<TR, K_O, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
           default:
-            if (mode == 1) epi_chunks<K_DOWN, 1>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
-            else if (mode == 2) epi_chunks<K_DOWN, 2>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
-            else epi_chunks<K_DOWN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
+            if (mode == 1) epi_chunks<TR, K_DOWN, 1>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
+            else if (mode == 2) epi_chunks<TR, K_DOWN, 2>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
+            else epi_chunks<TR, K_DOWN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
             break;
         }
         if (p.trace && et == 0) p.trace[(size_t)it.idx * 8 + 5] = globaltimer();
@@ -641,7 +659,8 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         }
         ep_bar();
         if (it.kind == K_ATT) {
-          attn_token_head(p.qkv, tok0 + ew, it.j, p.d, p.o, sm.attnP[ew], lane);  // warp = token, item = head
+          const int h = it.j % p.H, grp = it.j / p.H;  // item = (head, group of kEpiWarps tokens)
+          attn_token_head(p.qkv, tok0 + grp * kEpiWarps + ew, h, p.d, p.o, sm.attnP[ew], lane);
         } else {
           constexpr int kRows = 16 / kEpiWarps;  // rows of the token per warp
           const int row = (tok0 + it.j) * 16 + ew * kRows;
@@ -665,16 +684,16 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
   if (warp == 1) tmem_free<512>(tmem);
 }
 
-template <int STAGES>
+template <int STAGES, int TR>
 constexpr size_t smem_bytes() {
-  return 1024 + (size_t)STAGES * kStageBytes + sizeof(Smem);
+  return 1024 + (size_t)STAGES * Tile<TR>::stage_bytes + sizeof(Smem);
 }
-static_assert(smem_bytes<6>() <= 227 * 1024, "6-stage ring must fit");
+static_assert(smem_bytes<4, 256>() <= 227 * 1024, "4-stage 256-row ring must fit");
 
-template <int PER, int STAGES>
+template <int PER, int STAGES, int TR>
 cudaError_t launch_fused(const DitFusedParams& p, int ctas, cudaStream_t st) {
-  auto kern = dit_fused_kernel<PER, STAGES>;
-  constexpr size_t smem = smem_bytes<STAGES>();
+  auto kern = dit_fused_kernel<PER, STAGES, TR>;
+  constexpr size_t smem = smem_bytes<STAGES, TR>();
   static std::atomic<uint64_t> configured{0};
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
   return launch_k(kern, dim3(ctas), dim3(kThreadsF), smem, st, 1, p);
@@ -682,14 +701,11 @@ cudaError_t launch_fused(const DitFusedParams& p, int ctas, cudaStream_t st) {
 
 }  // namespace
 
-int dit_fused_items(int n_rt, int d, int H, int ff, int L, int T, int down_split) {
-  const int nf = d / kDitFeat;
-  const int per_step =
-      nf + L * (kDitTileTok + 3 * nf + H + nf + kDitTileTok + ff / kDitFeat + nf * down_split) + kDitTileTok + 1;
+int dit_fused_items(int n_rt, int tile_rows, int d, int H, int ff, int L, int T, int down_split) {
+  const int nf = d / kDitFeat, tok = tile_rows / 16, att = H * tok / kEpiWarps;
+  const int per_step = nf + L * (tok + 3 * nf + att + nf + tok + ff / kDitFeat + nf * down_split) + tok + 1;
   return per_step * T * n_rt;
 }
-
-size_t dit_fused_smem(int stages) { return stages == 6 ? smem_bytes<6>() : smem_bytes<4>(); }
 
 bool dit_fused_supported(int d, int C, int H, int ff, int L, int T) {
   return (d == 256 || d == 512 || d == 1024) && ff % kDitFeat == 0 && C == 64 && H * 128 == d &&
@@ -700,11 +716,14 @@ cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStr
   if (!dit_fused_supported(p.d, p.C, p.H, p.ff, p.L, p.T) || p.down_split < 1 || p.down_split > 2 ||
       (p.ff / 64) % p.down_split != 0 || p.n_rt <= 0)
     return cudaErrorInvalidValue;
-  const bool s6 = stages == 6;
+  // 4-stage rings for both tiles (128 rows: 32 KB stages -- 6 stages measured slower, r02_dit_fused_v7.txt)
+  const bool wide = p.tile_rows == 256;
+  if (!wide && p.tile_rows != 128) return cudaErrorInvalidValue;
+  (void)stages;
   switch (p.d / 128) {
-    case 2: return s6 ? launch_fused<2, 6>(p, ctas, st) : launch_fused<2, 4>(p, ctas, st);
-    case 4: return s6 ? launch_fused<4, 6>(p, ctas, st) : launch_fused<4, 4>(p, ctas, st);
-    case 8: return s6 ? launch_fused<8, 6>(p, ctas, st) : launch_fused<8, 4>(p, ctas, st);
+    case 2: return wide ? launch_fused<2, 4, 256>(p, ctas, st) : launch_fused<2, 4, 128>(p, ctas, st);
+    case 4: return wide ? launch_fused<4, 4, 256>(p, ctas, st) : launch_fused<4, 4, 128>(p, ctas, st);
+    case 8: return wide ? launch_fused<8, 4, 256>(p, ctas, st) : launch_fused<8, 4, 128>(p, ctas, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -12,7 +12,9 @@ namespace omni_dev {
 
 constexpr int kDitMaxLayers = 8;
 constexpr int kDitMaxPhases = 256;  // T * (3 + 7 L)
-constexpr int kDitTileRows = 128;  // rows of one row tile (8 tokens x 16 samples) = MMA N
+// Row tiles are 128 rows (8 tokens) or 256 rows (16 tokens) = MMA N, chosen
+// per launch by batch size (dit_tile_rows); buffers are sized for 128.
+constexpr int kDitTileRows = 128;  // the smaller tile: padding unit and counter sizing
 constexpr int kDitTileTok = 8;
 constexpr int kDitFeat = 128;      // output features per GEMM item = MMA M (TMEM lanes)
 
@@ -23,7 +25,7 @@ struct DitMaps {
   // weights (MMA A operand), 128-row boxes; w_out is [C_pad 128, d]
   CUtensorMap w_in, w_out;
   CUtensorMap wqkv[kDitMaxLayers], wo[kDitMaxLayers], w1[kDitMaxLayers], w2[kDitMaxLayers];
-  CUtensorMap x_x, x_a, x_o, x_u;  // activations (MMA B operand), 256-row boxes
+  CUtensorMap x_x[2], x_a[2], x_o[2], x_u[2];  // activations (MMA B operand), [0] 128- / [1] 256-row boxes
 };
 
 // Everything else one iteration needs (a small __grid_constant__ parameter).
@@ -43,16 +45,23 @@ struct DitFusedParams {
   int* ready;                      // [n_rt * d/128] first-arriver partials written (zeroed per launch)
   int* next_item;                  // global item counter (zeroed per launch)
   unsigned long long* trace;       // optional [items][5]: fetch, dep ok, mma done, done, smid
-  int n_rt, d, C, H, ff, L, T, vocab, down_split;
+  int n_rt, tile_rows, d, C, H, ff, L, T, vocab, down_split;
   float dt, sample_scale;
 };
 
 // Total items of one launch (tests / tools).
-int dit_fused_items(int n_rt, int d, int H, int ff, int L, int T, int down_split);
-size_t dit_fused_smem(int stages);
+int dit_fused_items(int n_rt, int tile_rows, int d, int H, int ff, int L, int T, int down_split);
+// Row tile of a batch of n_tok (padded) tokens on a persistent grid of
+// `ctas`: 128 rows (more, shorter items: the per-layer dependency chain of a
+// tile is the iteration's latency floor) until the batch has as many tokens
+// as the grid has CTAs, 256 rows from there (throughput: half the weight
+// re-reads and per-item overheads). Measured crossovers
+// (profiles/r02_dit_fused_v7.txt): ~128 tokens on 148 CTAs, 16-96 on 64.
+// n_tok must be a multiple of tile/16 (dit_pad_tokens).
+inline int dit_tile_rows(int n_tok, int ctas) { return n_tok >= ctas && n_tok % 16 == 0 ? 256 : 128; }
 // Model shapes the fused iteration covers (others run one kernel per op).
 bool dit_fused_supported(int d, int C, int H, int ff, int L, int T);
-// stages: TMA ring depth (4 or 6); ctas: persistent grid.
+// ctas: persistent grid (stages: ignored, 4-stage rings).
 cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStream_t st);
 
 }  // namespace omni_dev

@@ -181,6 +181,12 @@ void build_ar(omni_stage* st) {
   OMNI_CUDA(cudaMemsetAsync(st->page_table, 0, (size_t)st->lim.max_resident * st->max_pages * sizeof(int32_t),
                             st->stream));
   st->kv = dev_alloc<__nv_bfloat16>(st, (size_t)pages * L * 2 * KVH * kPageTokens * kHeadDim);
+  if (st->lim.max_seq_len > kAttnSplitChunks * 128) {  // contexts long enough to split (attention CHUNK 128)
+    st->split_groups = st->lim.max_resident + (st->rows_cap + kAttnQTok - 1) / kAttnQTok;
+    st->split_part = dev_alloc<float>(st, (size_t)st->split_groups * KVH * kAttnMaxParts * 16 * (kHeadDim + 2));
+    st->split_cnt = dev_alloc<int>(st, (size_t)st->split_groups * KVH);
+    OMNI_CUDA(cudaMemsetAsync(st->split_cnt, 0, (size_t)st->split_groups * KVH * sizeof(int), st->stream));
+  }
   st->free_pages.resize(pages);
   for (int i = 0; i < pages; ++i) st->free_pages[i] = pages - 1 - i;
   st->free_slots.resize(st->lim.max_resident);
@@ -250,7 +256,7 @@ void build_dit(omni_stage* st) {
     ly.g2 = gemm_of(ly.w2, 1, 64);
     ly.g2.fill_sms = true;
   }
-  const int T = st->tok_cap = round_up(std::max(16, st->lim.dit_max_tokens), kDitTileTok);  // whole row tiles
+  const int T = st->tok_cap = round_up(std::max(16, st->lim.dit_max_tokens), 2 * kDitTileTok);  // whole 256-row tiles
   const int R = st->drows_cap = T * kDitSamples;
   st->dx = dev_alloc<float>(st, (size_t)R * C);
   st->dxin = dev_alloc<__nv_bfloat16>(st, (size_t)R * C);
@@ -272,7 +278,7 @@ void build_dit(omni_stage* st) {
     st->dit_ctas = sms;
   }
   if (const char* e = std::getenv("OMNI_DIT_TRACE"); e && e[0] == '1') {
-    st->dit_trace_items = dit_fused_items(n_rt, d, m.n_heads, ff, L, m.dit_steps, st->down_split);
+    st->dit_trace_items = dit_fused_items(n_rt, kDitTileRows, d, m.n_heads, ff, L, m.dit_steps, st->down_split);
     st->dit_trace = dev_alloc<unsigned long long>(st, (size_t)st->dit_trace_items * 8);
   }
   const int cvec_rows = std::max(T, m.vocab);  // per-step rows / adaLN table rows
@@ -294,10 +300,12 @@ void build_dit(omni_stage* st) {
       mp.w1[l] = ly.g1.tmap;
       mp.w2[l] = ly.g2.tmap;
     }
-    mp.x_x = st->din_x.tmap_for(kDitTileRows);
-    mp.x_a = st->din_a.tmap_for(kDitTileRows);
-    mp.x_o = st->din_o.tmap_for(kDitTileRows);
-    mp.x_u = st->din_u.tmap_for(kDitTileRows);
+    for (int i = 0; i < 2; ++i) {  // 128- and 256-row boxes (dit_tile_rows)
+      mp.x_x[i] = st->din_x.tmap_for(128 << i);
+      mp.x_a[i] = st->din_a.tmap_for(128 << i);
+      mp.x_o[i] = st->din_o.tmap_for(128 << i);
+      mp.x_u[i] = st->din_u.tmap_for(128 << i);
+    }
     st->dmaps = dev_alloc<DitMaps>(st, 1);
     OMNI_CUDA(cudaMemcpyAsync(st->dmaps, &mp, sizeof(mp), cudaMemcpyHostToDevice, st->stream));
   }
@@ -468,7 +476,7 @@ ArDescLayout ar_desc_layout(const omni_stage* st) {
   ArDescLayout l;
   l.off_dec = align16(cap_e * sizeof(ArEntryDesc));
   l.off_blk = l.off_dec + align16(cap_e * sizeof(int32_t));
-  l.off_rows = l.off_blk + align16((cap_r + cap_e) * sizeof(AttnBlockDesc));
+  l.off_rows = l.off_blk + align16((cap_r + cap_e) * kAttnMaxParts * sizeof(AttnBlockDesc));
   l.off_delta = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
   l.cap_delta = kPageDeltaCap;
   l.reserve = l.off_delta + sizeof(PageDeltaHeader) + l.cap_delta * sizeof(PageDelta);
@@ -482,6 +490,8 @@ ArStepDev ar_step_dev(const omni_stage* st, const ArDescLayout& lay) {
   sd.dec_entries = reinterpret_cast<const int32_t*>(st->desc.dev + lay.off_dec);
   sd.attn_blocks = reinterpret_cast<const AttnBlockDesc*>(st->desc.dev + lay.off_blk);
   sd.max_pages = st->max_pages;
+  sd.split_part = st->split_part;
+  sd.split_cnt = st->split_cnt;
   return sd;
 }
 // The per-kernel AR step (PDL chain) for one launch geometry; everything
@@ -629,7 +639,7 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   auto* blks = reinterpret_cast<AttnBlockDesc*>(st->desc.host + lay.off_blk);
   auto* dh = reinterpret_cast<PageDeltaHeader*>(st->desc.host + lay.off_delta);
   auto* dl = reinterpret_cast<PageDelta*>(st->desc.host + lay.off_delta + sizeof(PageDeltaHeader));
-  int n_blocks = 0;
+  int n_blocks = 0, n_groups = 0;
   std::vector<int> dec_list;
   int r = 0, n_prefill_rows = 0;
   for (int e = 0; e < ne; ++e) {
@@ -651,8 +661,22 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       dec[dec_list.size()] = e;
       dec_list.push_back(e);
     }
-    for (int t0 = 0; t0 < b->span[e]; t0 += kAttnQTok)
-      blks[n_blocks++] = AttnBlockDesc{e, t0, std::min(kAttnQTok, b->span[e] - t0), 0};
+    for (int t0 = 0; t0 < b->span[e]; t0 += kAttnQTok) {
+      const int ntok = std::min(kAttnQTok, b->span[e] - t0);
+      // long contexts: split the keys over P CTAs (flash-decoding), merged
+      // in fixed part order by the last arriver. P is a function of this
+      // block's own context length only (batch invariance).
+      const int n_chunks = (b->pos0[e] + t0 + ntok + 127) / 128;
+      const int parts = std::min(kAttnMaxParts, (n_chunks + kAttnSplitChunks - 1) / kAttnSplitChunks);
+      if (parts > 1 && st->split_part) {
+        OMNI_REQUIRE(n_groups < st->split_groups, OMNI_E_BADARG, "split-KV groups exhausted");
+        for (int pp = 0; pp < parts; ++pp)
+          blks[n_blocks++] = AttnBlockDesc{e, t0, ntok, attn_split_pack(pp, parts, n_groups)};
+        ++n_groups;
+      } else {
+        blks[n_blocks++] = AttnBlockDesc{e, t0, ntok, 0};
+      }
+    }
     for (int t = 0; t < b->span[e]; ++t, ++r) {
       ArRowDesc& rd = rows[r];
       rd.entry = e;
@@ -717,7 +741,8 @@ bool dit_fused_enabled() {  // OMNI_DIT_FUSED=0: one kernel per op (A/B only)
 void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
   const auto& m = st->m;
   const int d = m.d_model, L = m.n_layers, C = m.dit_channels, S = kDitSamples;
-  const int n_rt = n_tok * S / kDitTileRows, nfd = d / kDitFeat;
+  const int tile_rows = dit_tile_rows(n_tok, st->dit_ctas);
+  const int n_rt = n_tok * S / tile_rows, nfd = d / kDitFeat;
   cudaStream_t s = st->stream;
   OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, st->dxin, s, st->dctl,
                         n_rt + 2 * n_rt * nfd + 1));
@@ -740,6 +765,7 @@ void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int3
   p.ready = st->dctl + n_rt + n_rt * nfd;
   p.next_item = st->dctl + n_rt + 2 * n_rt * nfd;
   p.n_rt = n_rt;
+  p.tile_rows = tile_rows;
   p.d = d;
   p.C = C;
   p.H = m.n_heads;
@@ -815,7 +841,13 @@ void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* s
   }
 }
 
-constexpr int kDitPadTok = kDitTileTok;  // DiT batches are padded to whole 256-row tiles (16 tokens)
+constexpr int kDitPadTok = kDitTileTok;  // DiT batches are padded to whole 128-row tiles (8 tokens)
+// ... and to whole 256-row tiles once dit_tile_rows picks them
+int64_t dit_pad_tokens(const omni_stage* st, int64_t n) {
+  if (n == 0) return 0;
+  const int64_t p8 = (n + kDitPadTok - 1) / kDitPadTok * kDitPadTok;
+  return p8 >= st->dit_ctas ? (n + 15) / 16 * 16 : p8;
+}
 uint64_t dit_graph_key(int nt, int64_t t0) { return (uint64_t)nt << 20 | (uint64_t)t0; }
 
 // Capture the DiT step graph of every padded batch size up front
@@ -832,6 +864,7 @@ void prewarm_dit_graphs(omni_stage* st) {
   if (staging_reserve(st->desc, align16((size_t)st->tok_cap * sizeof(DitTokDesc)))) drop_graphs(st);
   const auto* toks_dev = reinterpret_cast<const DitTokDesc*>(st->desc.dev);
   for (int nt = kDitPadTok; nt <= upto; nt += kDitPadTok) {
+    if (dit_pad_tokens(st, nt) != nt) continue;  // not a padded size
     const uint64_t key = dit_graph_key(nt, 0);
     if (!st->graphs.count(key))
       capture_graph(st, key, [&] {
@@ -855,7 +888,7 @@ void dit_step(omni_stage* st, const omni_dit_batch* b, int32_t* samples_out) {
   // computed and dropped. Rows never interact (token-local DiT), so real
   // outputs are unchanged, and the step-graph geometries shrink 8x (all
   // prewarmed at stage creation).
-  const int64_t n_pad = n_tok == 0 ? 0 : (n_tok + kDitPadTok - 1) / kDitPadTok * kDitPadTok;
+  const int64_t n_pad = dit_pad_tokens(st, n_tok);
   const size_t bytes = align16((size_t)n_pad * sizeof(DitTokDesc));
   if (staging_reserve(st->desc, std::max(bytes, align16((size_t)st->tok_cap * sizeof(DitTokDesc)))))
     drop_graphs(st);

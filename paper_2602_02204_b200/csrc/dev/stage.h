@@ -93,6 +93,9 @@ struct omni_stage {
   __nv_bfloat16* kv = nullptr;
   float2* rope = nullptr;
   int32_t* page_table = nullptr;  // persistent [max_resident][max_pages]
+  float* split_part = nullptr;     // split-KV attention scratch (long contexts; null: never split)
+  int* split_cnt = nullptr;
+  int split_groups = 0;            // >= attention blocks of any step: the split never runs out
   std::vector<omni_dev::PageDelta> pending_deltas;  // page assignments not yet shipped to the device
   omni_dev::GemmInput in_xn, in_attn, in_act, in_hbuf, in_cond;
   std::unordered_map<uint64_t, omni_dev::SeqSlot> seqs;

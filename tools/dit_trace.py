@@ -2,7 +2,8 @@
 
 For each item kind: count, mean fetch->dep-ok wait, dep-ok->mainloop-done,
 mainloop-done->done (epilogue), and per-phase critical-path time of row tile 0.
-Usage: OMNI_DIT_TRACE=1 python tools/dit_trace.py [tokens ...]
+Usage: OMNI_DIT_TRACE=1 python tools/dit_trace.py [--sms=N] [tokens ...]
+(--sms: the persistent grid, as omni_stage_set_sm_share sets it beside AR stages)
 """
 import json
 import os
@@ -27,9 +28,12 @@ def phases(L):
 
 
 def main():
-    ntoks = [int(a) for a in sys.argv[1:]] or [8, 64]
+    ntoks = [int(a) for a in sys.argv[1:] if not a.startswith("--")] or [8, 64]
+    sms = [int(a.split("=")[1]) for a in sys.argv[1:] if a.startswith("--sms=")]
     m = D.model_default(D.DIT)
     st = D.Stage(m, D.StageLimits(256, 64, 512, 0, 512), seed=9)
+    if sms:
+        st.set_sm_share(sms[0])
     d, L, T, H, ff = m.d_model, m.n_layers, m.dit_steps, m.n_heads, m.d_ff
     nf, ds = d // 128, (2 if ff >= 2 * d else 1)
     for n in ntoks:
@@ -38,10 +42,16 @@ def main():
             st.dit_step([1], [0], [n], toks)
         us = st.last_step_us()
         ptr, rows, cols = st.tensor("buf.dit_trace")
-        n_rt = (n + 15) // 16
+        wide_from = sms[0] if sms else 148
+        n_pad = (n + 7) // 8 * 8
+        if n_pad >= wide_from:
+            n_pad = (n + 15) // 16 * 16
+        tr_rows = 256 if n_pad >= wide_from and n_pad % 16 == 0 else 128
+        tok = tr_rows // 16
+        n_rt = n_pad * 16 // tr_rows
         ph = phases(L)
-        items_pp = {"IN": nf, "LN1": 16, "QKV": 3 * nf, "ATT": 4 * H, "O": nf, "LN2": 16, "UP": ff // 128,
-                    "DOWN": nf * ds, "LNF": 16, "OUT": 1}
+        items_pp = {"IN": nf, "LN1": tok, "QKV": 3 * nf, "ATT": H * tok // 8, "O": nf, "LN2": tok, "UP": ff // 128,
+                    "DOWN": nf * ds, "LNF": tok, "OUT": 1}
         total = sum(items_pp[k] for k in ph) * T * n_rt
         tr = D.d2h(ptr, (total, 8), np.uint64).astype(np.int64)
         t0 = tr[:, 0].min()
@@ -55,7 +65,18 @@ def main():
                         tiles.append(r)
                         tps.append(t * len(ph) + pi)
         kinds, tiles, tps = np.array(kinds), np.array(tiles), np.array(tps)
-        rep = {"tokens": n, "us_per_step": round(us, 1), "items": total, "span_us": round((tr[:, 3].max() - t0) / 1e3, 1)}
+        span = tr[:, 3].max() - t0
+        rep = {"tokens": n, "tile_rows": tr_rows, "sms": sms[0] if sms else None, "us_per_step": round(us, 1),
+               "items": total, "span_us": round(span / 1e3, 1)}
+        # per-CTA occupancy: share of the span each CTA spends waiting for
+        # dependencies, in GEMM mainloops (dep ok -> accumulator ready), in
+        # epilogues / LN / attention work, and idle between items
+        gemm = np.isin(kinds, ["IN", "QKV", "O", "UP", "DOWN", "OUT"])
+        ncta = len(np.unique(tr[:, 4]))
+        w = float(np.sum(tr[:, 1] - tr[:, 0])) / (span * ncta)
+        mm = float(np.sum((tr[:, 2] - tr[:, 1])[gemm])) / (span * ncta)
+        ep = float(np.sum((tr[:, 3] - tr[:, 2]))) / (span * ncta)
+        rep["cta_share"] = {"ctas": ncta, "dep_wait": round(w, 3), "gemm_main": round(mm, 3), "epi_or_ln_att": round(ep, 3)}
         per = {}
         for k in KINDS:
             sel = kinds == k
