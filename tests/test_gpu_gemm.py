@@ -22,7 +22,8 @@ def gemm(W, X, M, epi, out, ldo, gate=None, ldg=0, goff=0, rpg=16, max_splits=8)
 
 
 @pytest.mark.parametrize("N,K,M", [(128, 64, 1), (256, 2048, 5), (3072, 2048, 16), (2048, 8192, 200),
-                                   (1024, 1024, 300), (16384, 2048, 33), (128, 128, 257)])
+                                   (1024, 1024, 300), (16384, 2048, 33), (128, 128, 257),
+                                   (3072, 2048, 48), (2048, 8192, 64), (2048, 2048, 37)])
 @pytest.mark.parametrize("max_splits", [1, 8])
 def test_f32_matches_torch(N, K, M, max_splits):
     g = torch.Generator(device="cuda").manual_seed(N * 7 + M)

@@ -1,4 +1,5 @@
 """Phase trace of the decode GEMMs in a PDL chain (omni_k_gemm_trace).
+python tools/gemm_trace.py [GHZ] [M ...]
 Per launch: CTA entry/exit skew (globaltimer, ns) and per-CTA phase offsets
 (clock64 cycles -> us at the sampled SM clock): setup, producer past
 griddepcontrol.wait, last TMA issued, mainloop done, TMEM drained (+cluster
@@ -25,7 +26,7 @@ for name, (N, K, epi) in SHAPES.items():
     lib.omni_k_fill_weights(C.c_uint64(X), C.c_int64(256 * K), C.c_uint64(3), C.c_uint32(2), C.c_float(1.0))
     O = D.mem_alloc(256 * N * 4)
     arr = (C.c_uint64 * 8)(*Ws)
-    for M in (4, 16):
+    for M in [int(x) for x in sys.argv[2:]] or (4, 16):
         T = D.mem_alloc(8 * 8 * 4096)
         D.mem_set(T, 0, 8 * 8 * 4096)
         g = C.c_int32()
