@@ -205,41 +205,60 @@ __device__ __forceinline__ uint32_t ldcg_u32(const __nv_bfloat16* p) {
   return __ldcg(reinterpret_cast<const unsigned int*>(p));
 }
 
-// Attention among the 16 samples of token `tok`, head h (one warp). Same
-// arithmetic as dit_attn_kernel.
+// Attention among the 16 samples of token `tok`, head h (one warp), all on
+// the warp MMA (mma.sync m16n8k16): S = Q K^T, softmax on the S accumulators,
+// O = P V with P kept in registers -- the S accumulator fragments ARE the A
+// fragments of the PV product (rows = samples, k = keys), split into bf16 hi
+// + lo halves (two MMAs: ~fp32 precision of the probabilities). Every global
+// access is 16 bytes (24 loads + 8 stores per lane instead of 96 + 32 narrow
+// ones, which made attention items ~10 us):
+//  * Q / K: lane (g, t) loads 8 consecutive dims of rows g and g + 8; the head
+//    dimension is consumed in a permuted order (the fragment's k slots 2t /
+//    8 + 2t of k-step 2c + e take dims 32c + 8t + 4e + {0,1} / {2,3}),
+//    identical for Q and K, so S is the same dot product;
+//  * V: a 4x4 lane transpose (tr4) turns the quad's 16-byte row segments into
+//    rows of 8x8 tiles, and movmatrix.trans into the PV B fragments;
+//  * O: the transpose back turns the C fragments into 16-byte row segments.
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t a) {
+  uint32_t d;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(d) : "r"(a));
+  return d;
+}
+__device__ __forceinline__ void tr4u(uint32_t (&a)[4], int lane) {
+  float f0 = __uint_as_float(a[0]), f1 = __uint_as_float(a[1]), f2 = __uint_as_float(a[2]),
+        f3 = __uint_as_float(a[3]);
+  tr4(f0, f1, f2, f3, lane);
+  a[0] = __float_as_uint(f0), a[1] = __float_as_uint(f1), a[2] = __float_as_uint(f2), a[3] = __float_as_uint(f3);
+}
 __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int tok, int h, int d,
-                                                __nv_bfloat16* out, float (*P)[17], int lane) {
-  constexpr int S = 16, HD = 128;
+                                                __nv_bfloat16* out, int lane) {
+  constexpr int S = 16, HD = 128, NC = HD / 32;
   const int g = lane >> 2, t = lane & 3;
   const size_t ld = 3 * (size_t)d;
-  const __nv_bfloat16* Q = qkv + (size_t)tok * S * ld + h * HD;
+  const __nv_bfloat16* Q = qkv + (size_t)tok * S * ld + h * HD + 8 * t;
   const __nv_bfloat16* K = Q + d;
   const __nv_bfloat16* V = Q + 2 * d;
-  // the V rows this lane needs, in flight with the Q / K fragments
-  uint2 vr[S];
+  uint4 q0[NC], q1[NC], k0[NC], k1[NC], v0[NC], v1[NC];
 #pragma unroll
-  for (int j = 0; j < S; ++j) vr[j] = __ldcg(reinterpret_cast<const uint2*>(V + (size_t)j * ld + 4 * lane));
-  // every Q / K fragment in flight at once (one L2 round trip, not one per k-step)
-  uint32_t qa[HD / 16][4], kb[HD / 16][4];
-#pragma unroll
-  for (int kk = 0; kk < HD / 16; ++kk) {
-    const int col = kk * 16 + 2 * t;
-    qa[kk][0] = ldcg_u32(Q + (size_t)g * ld + col);
-    qa[kk][1] = ldcg_u32(Q + (size_t)(g + 8) * ld + col);
-    qa[kk][2] = ldcg_u32(Q + (size_t)g * ld + col + 8);
-    qa[kk][3] = ldcg_u32(Q + (size_t)(g + 8) * ld + col + 8);
-    kb[kk][0] = ldcg_u32(K + (size_t)g * ld + col);
-    kb[kk][1] = ldcg_u32(K + (size_t)g * ld + col + 8);
-    kb[kk][2] = ldcg_u32(K + (size_t)(g + 8) * ld + col);
-    kb[kk][3] = ldcg_u32(K + (size_t)(g + 8) * ld + col + 8);
+  for (int c = 0; c < NC; ++c) {
+    q0[c] = __ldcg(reinterpret_cast<const uint4*>(Q + (size_t)g * ld + 32 * c));
+    q1[c] = __ldcg(reinterpret_cast<const uint4*>(Q + (size_t)(g + 8) * ld + 32 * c));
+    k0[c] = __ldcg(reinterpret_cast<const uint4*>(K + (size_t)g * ld + 32 * c));
+    k1[c] = __ldcg(reinterpret_cast<const uint4*>(K + (size_t)(g + 8) * ld + 32 * c));
+    v0[c] = __ldcg(reinterpret_cast<const uint4*>(V + (size_t)g * ld + 32 * c));
+    v1[c] = __ldcg(reinterpret_cast<const uint4*>(V + (size_t)(g + 8) * ld + 32 * c));
   }
   float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-  for (int kk = 0; kk < HD / 16; ++kk) {
-    mma_bf16_16816(c0, qa[kk], kb[kk][0], kb[kk][1]);
-    mma_bf16_16816(c1, qa[kk], kb[kk][2], kb[kk][3]);
+  for (int c = 0; c < NC; ++c) {
+    const uint32_t qa0[4] = {q0[c].x, q1[c].x, q0[c].y, q1[c].y}, qa1[4] = {q0[c].z, q1[c].z, q0[c].w, q1[c].w};
+    mma_bf16_16816(c0, qa0, k0[c].x, k0[c].y);
+    mma_bf16_16816(c1, qa0, k1[c].x, k1[c].y);
+    mma_bf16_16816(c0, qa1, k0[c].z, k0[c].w);
+    mma_bf16_16816(c1, qa1, k1[c].z, k1[c].w);
   }
   const float scale = rsqrtf((float)HD);
+  // rows g (c*[0..1]) and g + 8 (c*[2..3]); keys 2t, 2t + 1 (c0) and 8 + 2t, 9 + 2t (c1)
   float r0[4] = {c0[0] * scale, c0[1] * scale, c1[0] * scale, c1[1] * scale};
   float r1[4] = {c0[2] * scale, c0[3] * scale, c1[2] * scale, c1[3] * scale};
   float m0 = fmaxf(fmaxf(r0[0], r0[1]), fmaxf(r0[2], r0[3]));
@@ -263,38 +282,40 @@ __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int to
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
   }
   const float i0 = 1.f / s0, i1 = 1.f / s1;
-  __syncwarp();  // the previous item's P reads are done
-  P[g][2 * t] = r0[0] * i0;
-  P[g][2 * t + 1] = r0[1] * i0;
-  P[g][8 + 2 * t] = r0[2] * i0;
-  P[g][9 + 2 * t] = r0[3] * i0;
-  P[g + 8][2 * t] = r1[0] * i1;
-  P[g + 8][2 * t + 1] = r1[1] * i1;
-  P[g + 8][8 + 2 * t] = r1[2] * i1;
-  P[g + 8][9 + 2 * t] = r1[3] * i1;
-  __syncwarp();
-  float acc[S][4];
+  // A fragments of P (m16 x k16): {row g keys 2t..}, {row g+8 keys 2t..}, {row g keys 8+2t..}, {row g+8 keys 8+2t..}
+  const float pv[4][2] = {{r0[0] * i0, r0[1] * i0}, {r1[0] * i1, r1[1] * i1}, {r0[2] * i0, r0[3] * i0},
+                          {r1[2] * i1, r1[3] * i1}};
+  uint32_t ph[4], pl[4];
 #pragma unroll
-  for (int i = 0; i < S; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-#pragma unroll
-  for (int j = 0; j < S; ++j) {
-    const float2 v01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[j].x));
-    const float2 v23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&vr[j].y));
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-      const float pij = P[i][j];
-      acc[i][0] += pij * v01.x;
-      acc[i][1] += pij * v01.y;
-      acc[i][2] += pij * v23.x;
-      acc[i][3] += pij * v23.y;
-    }
+  for (int r = 0; r < 4; ++r) {
+    const __nv_bfloat162 hb = __floats2bfloat162_rn(pv[r][0], pv[r][1]);
+    const float2 hf = __bfloat1622float2(hb);
+    ph[r] = *reinterpret_cast<const uint32_t*>(&hb);
+    pl[r] = pack_bf16x2(pv[r][0] - hf.x, pv[r][1] - hf.y);
   }
+  __nv_bfloat16* orow0 = out + ((size_t)tok * S + g) * d + h * HD + 8 * t;
+  __nv_bfloat16* orow1 = orow0 + (size_t)8 * d;
 #pragma unroll
-  for (int i = 0; i < S; ++i) {
-    const __nv_bfloat162 lo = __floats2bfloat162_rn(acc[i][0], acc[i][1]);
-    const __nv_bfloat162 hi = __floats2bfloat162_rn(acc[i][2], acc[i][3]);
-    *reinterpret_cast<uint2*>(out + ((size_t)tok * S + i) * d + h * HD + 4 * lane) =
-        make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+  for (int c = 0; c < NC; ++c) {
+    // lane (g, t) holds dims 32c + 8t .. +7 of key rows g / g + 8 = row g of
+    // 8x8 tile 4c + t; after the transpose: u32 t of row g of tiles 4c .. 4c+3
+    uint32_t a[4] = {v0[c].x, v0[c].y, v0[c].z, v0[c].w}, b[4] = {v1[c].x, v1[c].y, v1[c].z, v1[c].w};
+    tr4u(a, lane);
+    tr4u(b, lane);
+    uint32_t o0[4], o1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // tile 4c + u: dims 32c + 8u .. +7
+      const uint32_t bb0 = movmatrix_t(a[u]), bb1 = movmatrix_t(b[u]);  // (keys 2t.., dim g) / (keys 8+2t..)
+      float o[4] = {0.f, 0.f, 0.f, 0.f};
+      mma_bf16_16816(o, ph, bb0, bb1);
+      mma_bf16_16816(o, pl, bb0, bb1);
+      o0[u] = pack_bf16x2(o[0], o[1]);  // row g, dims 32c + 8u + 2t, +1
+      o1[u] = pack_bf16x2(o[2], o[3]);  // row g + 8
+    }
+    tr4u(o0, lane);  // -> lane t: row g, dims 32c + 8t .. +7
+    tr4u(o1, lane);
+    *reinterpret_cast<uint4*>(orow0 + 32 * c) = make_uint4(o0[0], o0[1], o0[2], o0[3]);
+    *reinterpret_cast<uint4*>(orow1 + 32 * c) = make_uint4(o1[0], o1[1], o1[2], o1[3]);
   }
 }
 
@@ -398,7 +419,6 @@ struct Smem {
   int last_flag, last_old;
   int item_start[kDitMaxPhases + 1];  // global item index where (step, phase) tp starts
   int unit_cum[kDitMaxPhases + 1];    // per-tile units completed before tp
-  float attnP[kEpiWarps][16][17];
 };
 
 template <int PER, int STAGES, int TR>
@@ -660,7 +680,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         ep_bar();
         if (it.kind == K_ATT) {
           const int h = it.j % p.H, grp = it.j / p.H;  // item = (head, group of kEpiWarps tokens)
-          attn_token_head(p.qkv, tok0 + grp * kEpiWarps + ew, h, p.d, p.o, sm.attnP[ew], lane);
+          attn_token_head(p.qkv, tok0 + grp * kEpiWarps + ew, h, p.d, p.o, lane);
         } else {
           constexpr int kRows = 16 / kEpiWarps;  // rows of the token per warp
           const int row = (tok0 + it.j) * 16 + ew * kRows;
