@@ -319,44 +319,56 @@ __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int to
   }
 }
 
-// The epilogue of one GEMM item for one kind (MODE: 0 plain, 1 first MLP-down
-// half writes its partial, 2 second half adds it). Each chunk = 16 rows (one
+// The epilogue of one GEMM item for one kind. MLP-down K parts meet in a
+// fixed binary tree of commutative two-way sums, (p0 + p1) + (p2 + p3), so
+// the result does not depend on which part arrives first. MODE: 0 plain;
+// 1 write my partial to `dst` (first of a pair); 2 final: gate * (acc + s1)
+// (split 2); 3 pair sum acc + s1 to `dst` (first pair to finish, split 4);
+// 4 final: gate * ((acc + s1) + s2) (split 4). Each chunk = 16 rows (one
 // token) x this warp's 32 features; after a 4x4 lane-group transpose (tr4)
 // lane 4g+t owns row 4m+t, features fw .. fw+3 of group m, so every store is
 // 8 / 16 bytes per thread (4x fewer store instructions than one feature per
 // thread). aux: IN pos_emb[sample][own feature]; O / DOWN the adaLN gate of
 // token c (rotated one per chunk).
 template <int TR, int KIND, int MODE>
-__device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta, int row0, int ft, int tix, int quad,
-                                           int half, int lane, float (&aux)[16], int step) {
+__device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta, int row0, int ft, const float* s1b,
+                                           const float* s2b, float* dstb, int quad, int half, int lane,
+                                           float (&aux)[16], int step) {
   constexpr bool kGated = KIND == K_O || KIND == K_DOWN;
   const int g4 = lane >> 2, t4 = lane & 3;
   const int fw = ft * kDitFeat + quad * 32 + 4 * g4;  // first of my 4 features after the transpose
   const int d = p.d;
   if (KIND == K_OUT && quad * 32 >= p.C) return;  // OUT: the C channels are the first C lanes
   constexpr int kChunks = Tile<TR>::chunks, kMyChunks = Tile<TR>::my_chunks;
-  const float* part4 = p.part + (size_t)tix * TR * kDitFeat + quad * 32 + 4 * g4;
-  // side inputs (x / partner partial) of chunk cc, my 4 rows 4m + t4
+  const int off4 = quad * 32 + 4 * g4;  // my 4 features within the 128-feature partial tile
+  const float* s1 = s1b + off4;
+  const float* s2 = s2b + off4;
+  float* dst4 = dstb + off4;
+  // side inputs (x / partial sums) of chunk cc, my 4 rows 4m + t4
   // (post-transpose layout); the next chunk's are in flight
-  auto load_side = [&](int cc, float4(&dst)[4]) {
+  auto load_side = [&](int cc, float4(&dst)[4], float4(&dst2)[4]) {
     if constexpr (KIND == K_OUT)
 #pragma unroll
       for (int m = 0; m < 4; ++m)
         dst[m] = __ldcg(reinterpret_cast<const float4*>(p.x + (size_t)(row0 + cc * 16 + 4 * m + t4) * p.C + fw));
-    if constexpr (MODE == 2)
+    if constexpr (MODE >= 2)
 #pragma unroll
       for (int m = 0; m < 4; ++m)
-        dst[m] = __ldcg(reinterpret_cast<const float4*>(part4 + (size_t)(cc * 16 + 4 * m + t4) * kDitFeat));
+        dst[m] = __ldcg(reinterpret_cast<const float4*>(s1 + (size_t)(cc * 16 + 4 * m + t4) * kDitFeat));
+    if constexpr (MODE == 4)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        dst2[m] = __ldcg(reinterpret_cast<const float4*>(s2 + (size_t)(cc * 16 + 4 * m + t4) * kDitFeat));
   };
   // this warp's chunks: c = half, half + 2, ... (its quadrant partner takes the others)
-  float4 nx[4] = {};
-  load_side(half, nx);
+  float4 nx[4] = {}, nx2[4] = {};
+  load_side(half, nx, nx2);
 #pragma unroll 1
   for (int c = half; c < kChunks; c += 2) {
-    float4 ld[4];
+    float4 ld[4], ld2[4];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) ld[m] = nx[m];
-    if (c + 2 < kChunks) load_side(c + 2, nx);
+    for (int m = 0; m < 4; ++m) ld[m] = nx[m], ld2[m] = nx2[m];
+    if (c + 2 < kChunks) load_side(c + 2, nx, nx2);
     float v[16];
     tmem_ld16(ta + c * 16, v);
     const int rb = row0 + c * 16;  // rows of token row0 / 16 + c
@@ -370,8 +382,8 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj) v[jj] *= aux[0];
     }
-    float gq[4];  // MODE 2: the gates of my 4 post-transpose features
-    if constexpr (MODE == 2)
+    float gq[4];  // MODE 2 / 4: the gates of my 4 post-transpose features
+    if constexpr (MODE == 2 || MODE == 4)
 #pragma unroll
       for (int i = 0; i < 4; ++i) gq[i] = __shfl_sync(0xffffffffu, aux[0], 4 * g4 + i);
 #pragma unroll
@@ -396,10 +408,17 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
           p.samples[row] = (int32_t)sq;
         }
       } else if constexpr (MODE == 1) {
-        st_f4_cg(const_cast<float*>(part4) + (size_t)(c * 16 + 4 * m + t4) * kDitFeat, q[0], q[1], q[2], q[3]);
+        st_f4_cg(dst4 + (size_t)(c * 16 + 4 * m + t4) * kDitFeat, q[0], q[1], q[2], q[3]);
+      } else if constexpr (MODE == 3) {
+        st_f4_cg(dst4 + (size_t)(c * 16 + 4 * m + t4) * kDitFeat, q[0] + ld[m].x, q[1] + ld[m].y, q[2] + ld[m].z,
+                 q[3] + ld[m].w);
       } else if constexpr (MODE == 2) {
         red_add_v4(p.h + (size_t)row * d + fw, gq[0] * (q[0] + ld[m].x), gq[1] * (q[1] + ld[m].y),
                    gq[2] * (q[2] + ld[m].z), gq[3] * (q[3] + ld[m].w));
+      } else if constexpr (MODE == 4) {
+        red_add_v4(p.h + (size_t)row * d + fw, gq[0] * ((q[0] + ld[m].x) + ld2[m].x),
+                   gq[1] * ((q[1] + ld[m].y) + ld2[m].y), gq[2] * ((q[2] + ld[m].z) + ld2[m].z),
+                   gq[3] * ((q[3] + ld[m].w) + ld2[m].w));
       } else {
         red_add_v4(p.h + (size_t)row * d + fw, q[0], q[1], q[2], q[3]);
       }
@@ -416,7 +435,7 @@ struct Smem {
   uint64_t q_full[kQ], q_empty[kQ];
   Item ring[kQ];
   uint32_t tmem;
-  int last_flag, last_old;
+  int mode;
   int item_start[kDitMaxPhases + 1];  // global item index where (step, phase) tp starts
   int unit_cum[kDitMaxPhases + 1];    // per-tile units completed before tp
 };
@@ -618,47 +637,64 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         tc_fence_after();
         ++gi;
         if (p.trace && et == 0) p.trace[(size_t)it.idx * 8 + 2] = globaltimer();
-        // split MLP-down: the first arriving K half writes its partial, the
-        // second adds it (commutative) and applies the gated residual
-        int mode = 0;  // 0 = plain epilogue, 1 = first half (write partial), 2 = second half (reduce)
-        if (it.kind == K_DOWN && p.down_split == 2) {
+        // split MLP-down: parts meet pairwise, (p0 + p1) [+ (p2 + p3)]; in
+        // each pair / between the pairs the first arriver writes its partial
+        // and the second adds it (commutative: arrival order never changes bits)
+        int mode = 0;
+        const int pr = it.kind == K_DOWN ? (it.j % p.down_split) / 2 : 0;  // my pair
+        const int tix2 = tix * 2 + pr;
+        if (it.kind == K_DOWN && p.down_split > 1) {
           if (et == 0) {
-            const int old = atomicAdd(p.tile_cnt + tix, 1);
-            sm.last_flag = old & 1;
-            sm.last_old = old;
+            const int old1 = atomicAdd(p.tile_cnt + tix2, 1);
+            int md = 1;
+            if (old1 & 1) {  // second of my pair: the pair sum is mine
+              wait_ge(p.ready + tix2, (old1 + 1) / 2);
+              md = 2;
+              if (p.down_split == 4) {
+                const int old2 = atomicAdd(p.tile_cnt2 + tix, 1);
+                md = 3;
+                if (old2 & 1) {
+                  wait_ge(p.ready2 + tix, (old2 + 1) / 2);
+                  md = 4;
+                }
+              }
+            }
+            sm.mode = md;
           }
           ep_bar();
-          mode = sm.last_flag ? 2 : 1;
-          if (mode == 2) {
-            if (et == 0) wait_ge(p.ready + tix, (sm.last_old + 1) / 2);
-            ep_bar();
-          }
+          mode = sm.mode;
         }
+        const float* part1 = p.part + (size_t)tix2 * TR * kDitFeat;  // my pair's first partial
+        float* part2 = p.part2 + (size_t)tix * TR * kDitFeat;        // the first pair sum
         const uint32_t ta = tmem + acc * TR + (static_cast<uint32_t>(quad * 32) << 16);
         switch (it.kind) {  // once per item: the chunk loop is specialised per kind (no jump table inside)
-          case K_IN: epi_chunks<TR, K_IN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_QKV: epi_chunks<TR, K_QKV, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_UP: epi_chunks<TR, K_UP, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_OUT: epi_chunks<TR, K_OUT, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
-          case K_O: epi_chunks<TR, K_O, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step); break;
+          case K_IN: epi_chunks<TR, K_IN, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_QKV: epi_chunks<TR, K_QKV, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_UP: epi_chunks<TR, K_UP, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_OUT: epi_chunks<TR, K_OUT, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_O: epi_chunks<TR, K_O, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
           default:
-            if (mode == 1) epi_chunks<TR, K_DOWN, 1>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
-            else if (mode == 2) epi_chunks<TR, K_DOWN, 2>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
-            else epi_chunks<TR, K_DOWN, 0>(p, ta, row0, ft, tix, quad, half, lane, aux, it.step);
+            switch (mode) {
+              case 1: epi_chunks<TR, K_DOWN, 1>(p, ta, row0, ft, part1, part2, const_cast<float*>(part1), quad, half, lane, aux, it.step); break;
+              case 2: epi_chunks<TR, K_DOWN, 2>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+              case 3: epi_chunks<TR, K_DOWN, 3>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+              case 4: epi_chunks<TR, K_DOWN, 4>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+              default: epi_chunks<TR, K_DOWN, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+            }
             break;
         }
         if (p.trace && et == 0) p.trace[(size_t)it.idx * 8 + 5] = globaltimer();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
-        if (mode == 1) {
+        if (mode == 1 || mode == 3) {
           ep_bar();
           if (et == 0) {
             __threadfence();
-            atomicAdd(p.ready + tix, 1);
+            atomicAdd(mode == 1 ? p.ready + tix2 : p.ready2 + tix, 1);
             if (p.trace) p.trace[(size_t)it.idx * 8 + 3] = globaltimer();
           }
-          continue;  // no unit of progress: the second half completes the tile
+          continue;  // no unit of progress: the final sum completes the tile
         }
       } else {
         // LN / attention items: wait for the tile's earlier phases
@@ -733,7 +769,7 @@ bool dit_fused_supported(int d, int C, int H, int ff, int L, int T) {
 }
 
 cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStream_t st) {
-  if (!dit_fused_supported(p.d, p.C, p.H, p.ff, p.L, p.T) || p.down_split < 1 || p.down_split > 2 ||
+  if (!dit_fused_supported(p.d, p.C, p.H, p.ff, p.L, p.T) || (p.down_split != 1 && p.down_split != 2 && p.down_split != 4) ||
       (p.ff / 64) % p.down_split != 0 || p.n_rt <= 0)
     return cudaErrorInvalidValue;
   // 4-stage rings for both tiles (128 rows: 32 KB stages -- 6 stages measured slower, r02_dit_fused_v7.txt)

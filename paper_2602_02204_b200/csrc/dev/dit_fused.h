@@ -38,11 +38,14 @@ struct DitFusedParams {
   __nv_bfloat16* xb;               // [rows][C] its bf16 copy (IN-proj operand)
   float* h;                        // [rows][d] residual stream
   __nv_bfloat16 *a, *qkv, *o, *u;  // LN out [rows][d], [rows][3d], attn out [rows][d], [rows][ff]
-  float* part;                     // MLP-down first-half partials [n_rt * d/128][256 rows][128]
+  float* part;                     // MLP-down first partial of each pair [n_rt * d/128][2][TR rows][128]
+  float* part2;                    // first pair sum (split 4) [n_rt * d/128][TR rows][128]
   int32_t* samples;                // [rows] int32 samples (last Euler step)
   int* progress;                   // [n_rt] units completed per row tile (zeroed per launch)
-  int* tile_cnt;                   // [n_rt * d/128] split-K arrivals (zeroed per launch)
-  int* ready;                      // [n_rt * d/128] first-arriver partials written (zeroed per launch)
+  int* tile_cnt;                   // [n_rt * d/128][2] arrivals per pair (zeroed per launch)
+  int* ready;                      // [n_rt * d/128][2] pair partials written (zeroed per launch)
+  int* tile_cnt2;                  // [n_rt * d/128] pair sums finished (split 4)
+  int* ready2;                     // [n_rt * d/128] first pair sum written
   int* next_item;                  // global item counter (zeroed per launch)
   unsigned long long* trace;       // optional [items][5]: fetch, dep ok, mma done, done, smid
   int n_rt, tile_rows, d, C, H, ff, L, T, vocab, down_split;

@@ -267,10 +267,13 @@ void build_dit(omni_stage* st) {
   st->du = dev_alloc<__nv_bfloat16>(st, (size_t)R * ff);
   // fused iteration: MLP-down split in two K halves (fixed per weight shape:
   // batch invariance) so its items match the others' K = d mainloop
+  // K halves meet in a commutative pair sum (dit_fused.cu). Four parts (a
+  // tree of pair sums, also supported) measured slower at every batch size:
+  // 3x the partial-sum traffic (profiles/r02_dit_fused_v7.txt)
   st->down_split = (ff >= 2 * d && (ff / 64) % 2 == 0) ? 2 : 1;
   const int n_rt = R / kDitTileRows, nfd = d / kDitFeat;
-  st->dpart = dev_alloc<float>(st, (size_t)n_rt * nfd * kDitTileRows * kDitFeat);
-  st->dctl_n = n_rt + 2 * n_rt * nfd + 1;
+  st->dpart = dev_alloc<float>(st, (size_t)3 * n_rt * nfd * kDitTileRows * kDitFeat);  // [2 pairs] + pair sum
+  st->dctl_n = n_rt + 6 * n_rt * nfd + 1;
   st->dctl = dev_alloc<int>(st, (size_t)st->dctl_n);
   {
     int sms = 0;
@@ -745,7 +748,7 @@ void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int3
   const int n_rt = n_tok * S / tile_rows, nfd = d / kDitFeat;
   cudaStream_t s = st->stream;
   OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, st->dxin, s, st->dctl,
-                        n_rt + 2 * n_rt * nfd + 1));
+                        n_rt + 6 * n_rt * nfd + 1));
   DitFusedParams p{};
   p.maps = st->dmaps;
   p.toks = toks_dev;
@@ -759,11 +762,14 @@ void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int3
   p.o = st->dout;
   p.u = st->du;
   p.part = st->dpart;
+  p.part2 = st->dpart + (size_t)2 * n_rt * nfd * tile_rows * kDitFeat;
   p.samples = samples_dev;
   p.progress = st->dctl;
   p.tile_cnt = st->dctl + n_rt;
-  p.ready = st->dctl + n_rt + n_rt * nfd;
-  p.next_item = st->dctl + n_rt + 2 * n_rt * nfd;
+  p.ready = st->dctl + n_rt + 2 * n_rt * nfd;
+  p.tile_cnt2 = st->dctl + n_rt + 4 * n_rt * nfd;
+  p.ready2 = st->dctl + n_rt + 5 * n_rt * nfd;
+  p.next_item = st->dctl + n_rt + 6 * n_rt * nfd;
   p.n_rt = n_rt;
   p.tile_rows = tile_rows;
   p.d = d;
