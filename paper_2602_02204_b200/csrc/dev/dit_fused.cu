@@ -123,12 +123,15 @@ __device__ __forceinline__ void wait_ge(const int* ptr, int target) {
   }
   asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
-// gelu_tanh with tanh(y) = 1 - 2 / (exp(2y) + 1) on the SFU (|rel err| ~1e-6,
-// far below the bf16 rounding of the result)
+// gelu_tanh with one MUFU tanh.approx.f32 (|rel err| <= 2^-10.99 on tanh,
+// below the bf16 rounding of the result): ~6 instructions per element -- the
+// MLP-up epilogue was instruction-bound on the exp / divide form
 __device__ __forceinline__ float gelu_fast(float x) {
-  const float y = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  const float t = 1.f - __fdividef(2.f, __expf(2.f * y) + 1.f);
-  return 0.5f * x * (1.f + t);
+  const float y = x * fmaf(0.0356774081f, x * x, 0.7978845608f);  // sqrt(2/pi) (x + 0.044715 x^3)
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(y));
+  const float hx = 0.5f * x;
+  return fmaf(hx, t, hx);
 }
 // 4x4 transpose inside each group of 4 lanes: lane 4g+k holds feature 4g+k
 // of rows 0..3 on entry, and rows... on exit lane 4g+t holds row t of
@@ -360,17 +363,24 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
       for (int m = 0; m < 4; ++m)
         dst2[m] = __ldcg(reinterpret_cast<const float4*>(s2 + (size_t)(cc * 16 + 4 * m + t4) * kDitFeat));
   };
-  // this warp's chunks: c = half, half + 2, ... (its quadrant partner takes the others)
+  // this warp's chunks: c = half, half + 2, ... (its quadrant partner takes the
+  // others); the next chunk's TMEM load and side inputs are in flight while
+  // this one is processed
   float4 nx[4] = {}, nx2[4] = {};
   load_side(half, nx, nx2);
+  uint32_t tr[16];
+  tmem_ld16_issue(ta + half * 16, tr);
 #pragma unroll 1
   for (int c = half; c < kChunks; c += 2) {
     float4 ld[4], ld2[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) ld[m] = nx[m], ld2[m] = nx2[m];
     if (c + 2 < kChunks) load_side(c + 2, nx, nx2);
+    tmem_ld16_wait(tr);
     float v[16];
-    tmem_ld16(ta + c * 16, v);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(tr[i]);
+    if (c + 2 < kChunks) tmem_ld16_issue(ta + (c + 2) * 16, tr);
     const int rb = row0 + c * 16;  // rows of token row0 / 16 + c
     if constexpr (KIND == K_IN) {
 #pragma unroll

@@ -35,7 +35,7 @@ def main():
     if sms:
         st.set_sm_share(sms[0])
     d, L, T, H, ff = m.d_model, m.n_layers, m.dit_steps, m.n_heads, m.d_ff
-    nf, ds = d // 128, (1 if ff < 2 * d else 4 if (ff // 64) % 4 == 0 else 2 if (ff // 64) % 2 == 0 else 1)
+    nf, ds = d // 128, (2 if ff >= 2 * d and (ff // 64) % 2 == 0 else 1)  # stage.cpp down_split
     for n in ntoks:
         toks = [(5 * i) % 64 for i in range(n)]
         for _ in range(3):
