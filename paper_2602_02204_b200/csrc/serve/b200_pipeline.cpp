@@ -433,7 +433,11 @@ struct B200Pipeline::Impl {
   }
 };
 
-constexpr int32_t kDitSharedSms = 64;
+// SMs of the persistent DiT iteration when it shares its GPU with AR stages.
+// 48 leaves 100 SMs: a Thinker QKV grid (192 CTAs, two per SM) still fits in
+// one wave beside it. Pipeline req/s by share (profiles/r02_dit_sm_share.txt):
+// 32: 173, 40: 204, 44: 212, 48: 214-218, 52: 205-212, 56: 197-205, 64: 193-200.
+constexpr int32_t kDitSharedSms = 48;
 
 B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
   impl_->opt = std::move(opt);
