@@ -13,6 +13,9 @@
 
 namespace omni_dev {
 
+// wait for the predecessor, THEN let dependents launch: the kernel following
+// desc_copy_kernel must use this order (later kernels read step descriptors
+// before their own pdl_wait)
 struct PdlDep {
   __device__ __forceinline__ void operator()() const {
     pdl_wait();
@@ -144,8 +147,12 @@ __device__ __forceinline__ void attention_block(int blk_idx, int kh_idx, const A
   constexpr int HD = kHeadDim;
   constexpr uint32_t PAGE_BYTES = kPageTokens * HD * 2;  // 4 KB K or V slice of one page
   constexpr int kAttnPagesPerChunk = kAttnChunk / kPageTokens;
-  // The step descriptors come from the H2D copy that completed before the
-  // step's first kernel started, so they are readable before pdl_wait.
+  // Step descriptors are readable before pdl_wait: desc_copy_kernel (the
+  // step's first kernel) writes them, and the kernel after it (embed /
+  // gather_cond, PdlDep) waits for it BEFORE triggering its own dependents,
+  // so every later kernel of the step launches after the copy completed.
+  // Keep that order: a kernel right after desc_copy must use PdlDep (wait,
+  // then trigger), never trigger early (ar_kernels.cu launch_desc_copy).
   const AttnBlockDesc blk = s.attn_blocks[blk_idx];
   const int kh = kh_idx;
   const ArEntryDesc ed = s.entries[blk.entry];

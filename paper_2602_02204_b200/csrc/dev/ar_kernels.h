@@ -91,6 +91,9 @@ struct PageDeltaHeader {
 constexpr int kPageDeltaCap = 1024;
 // Copies the step descriptor blob from pinned staging (UVA loads) and applies
 // the page-table delta (delta_src: header + PageDelta[n], pinned host).
+// Ordering contract: the kernel launched right after it must pdl_wait before
+// pdl_trigger (PdlDep) -- attention and the push GEMM prologues read the
+// descriptors before their own pdl_wait, relying on that chain.
 cudaError_t launch_desc_copy(void* dst, const void* src, size_t bytes, const void* delta_src,
                              int32_t* page_table, cudaStream_t st);
 // Greedy argmax (top_k <= 1) or top-k sampling of each decode row, + top-2 margin.

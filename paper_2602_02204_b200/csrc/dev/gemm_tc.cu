@@ -144,7 +144,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // idle warps: input-RMS scales of this token tile, overlapped with the mainloop
     if constexpr (PUSH && EPI == EPI_ROPE_KV) {
       // positions / KV pages / RoPE rows of this rank's token slice: step
-      // descriptors and static tables, readable before the PDL wait
+      // descriptors (written by desc_copy_kernel, complete before any GEMM
+      // of the step launches -- see launch_desc_copy's ordering contract) and
+      // static tables, readable before the PDL wait
       constexpr int kPer = BN / kPushS;
       const int cb0 = m_tile * BN + split * kPer;
       const int n_me = min(kPer, a.M - cb0);
@@ -369,21 +371,8 @@ cudaError_t launch_bn(const GemmWeight& w, const GemmInput& x, const GemmArgs& a
 template <int EPI>
 cudaError_t launch_epi(const GemmWeight& w, const GemmInput& x, const GemmArgs& a,
                        cudaStream_t st) {
-  // compute-bound weights (DiT, fill_sms): the widest token tile that still
-  // puts >= one CTA on every SM; the per-element result does not depend on BN
-  static const bool dit2 = [] {  // OMNI_DIT_2CTA=1: shallow rings, 2 CTAs/SM for DiT tiles (experiment)
-    const char* e = std::getenv("OMNI_DIT_2CTA");
-    return e && e[0] == '1';
-  }();
-  if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU || EPI == EPI_GATED_RESID || EPI == EPI_F32 ||
-                EPI == EPI_EULER) {
-    if (dit2 && w.fill_sms) {
-      switch (bn_for(w, a.M)) {
-        case 64: return launch_bn<64, EPI, 4>(w, x, a, st);
-        default: return launch_bn<128, EPI, 3>(w, x, a, st);  // ~98 KB: 2 CTAs per SM
-      }
-    }
-  }
+  // compute-bound weights (DiT per-op path, fill_sms): the widest token tile;
+  // the per-element result does not depend on BN
   const bool push = gemm_push_enabled();
   switch (bn_for(w, a.M)) {
     case 16:
@@ -436,22 +425,6 @@ static int bn_for(const GemmWeight& w, int M) {
     if (split) return 128;
   }
   if (w.fill_sms && bn > 64) {
-    static const int forced = [] {  // OMNI_DIT_BN: experiments only
-      const char* e = std::getenv("OMNI_DIT_BN");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (forced == 64 || forced == 128 || forced == 256) return forced;
-    // OMNI_DIT_DEEP_BN=<16|32|64>[:max_rows]: narrower token tiles for the
-    // deep-K DiT weight (MLP down, K = 4d) at small batches, where 8 fat-tile
-    // CTAs each stream 2 MB (per-element results do not depend on BN)
-    static const std::pair<int, int> deep = [] {
-      const char* e = std::getenv("OMNI_DIT_DEEP_BN");
-      if (!e) return std::pair<int, int>{0, 0};
-      int bn = std::atoi(e), mx = 256;
-      if (const char* c = std::strchr(e, ':')) mx = std::atoi(c + 1);
-      return std::pair<int, int>{bn, mx};
-    }();
-    if (deep.first && w.K >= 4096 && M <= deep.second) return deep.first;
     // Widest token tile (fewest CTAs), not the isolated-latency optimum: the
     // DiT shares the GPU with two latency-bound AR chains, and fat tiles leave
     // them SMs -- measured +6.5 % pipeline req/s over a fill-the-SMs cost
