@@ -25,7 +25,10 @@ TALKER_BYTES = 4 * 60_817_408 * 2 + 2048 * 2048 * 2 + 64 * 2048 * 2
 
 def ar_probe(kind: int, batches, prompt: int = 64, steps: int = 12):
     m = D.model_default(kind)
-    st = D.Stage(m, D.StageLimits(256, 64, 512, 0, 512), seed=7)
+    # long contexts (split-KV attention beyond 1024 keys): fewer residents, longer sequences
+    lim = D.StageLimits(256, 64, 512, 0, 512) if prompt + steps <= 448 else \
+        D.StageLimits(256, 16, prompt + steps + 64, 0, 512)
+    st = D.Stage(m, lim, seed=7)
     wbytes = THINKER_BYTES if kind == D.THINKER else TALKER_BYTES
     cond = D.mem_alloc(2 * m.cond_dim * 256) if kind == D.TALKER else 0
     if cond:
