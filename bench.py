@@ -111,10 +111,16 @@ def dist_setup(n_gpus: int):
     return 1, 0, local, None
 
 
-# Device busy time per stage of the 1-GPU bench (ms per 100-request step,
-# profiles/r02_bench_*.json "stages"): what one GPU-worth of each stage costs
-# under the reference workload. placement_for() apportions GPUs by it.
-STAGE_BUSY_MS = {"thinker": 429.0, "talker": 457.0, "vocoder": 484.0}
+# What one GPU-worth of each stage costs per 100-request step of the reference
+# workload when the stage has its GPU to ITSELF (ms): the bench's step counts
+# x uncontended step times (tools/step_probe.py) -- Thinker 439 steps x ~0.33
+# ms (decode ~0.28, mixed prefill ~0.5), Talker 2040 x 0.155 ms, Code2Wav ~213
+# iterations x ~1.2 ms (all 148 SMs, ~85 tokens). On one shared GPU the three
+# are ~400 ms each (the DiT then runs on a 48-SM share), which says nothing
+# about their cost apart. placement_for() apportions GPUs by these: 2 GPUs =
+# Talker alone | Thinker + Code2Wav, 4 = T | Tk x2 | C2W,
+# 8 = T x2 | Tk x3 | C2W x3.
+STAGE_BUSY_MS = {"thinker": 145.0, "talker": 316.0, "vocoder": 255.0}
 
 
 def placement_for(n_gpus: int, busy: dict = STAGE_BUSY_MS) -> dict:
