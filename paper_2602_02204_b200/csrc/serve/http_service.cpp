@@ -159,12 +159,22 @@ void HttpService::stop() {
   if (accept_thread_.joinable()) accept_thread_.join();
   ::close(listen_fd_);
   listen_fd_ = -1;
-  std::list<std::thread> conns;
+  reap(true);
+}
+
+void HttpService::reap(bool all) {
+  std::list<Conn> finished;
   {
     std::lock_guard lk(conn_mu_);
-    conns.swap(conns_);
+    for (auto it = conns_.begin(); it != conns_.end();) {
+      if (all || it->done->load()) {
+        finished.splice(finished.end(), conns_, it++);
+      } else {
+        ++it;
+      }
+    }
   }
-  for (auto& t : conns) t.join();
+  for (auto& c : finished) c.t.join();
 }
 
 void HttpService::accept_loop() {
@@ -173,11 +183,15 @@ void HttpService::accept_loop() {
     if (::poll(&p, 1, 50) <= 0) continue;
     const int c = ::accept4(listen_fd_, nullptr, nullptr, SOCK_CLOEXEC);
     if (c < 0) continue;
+    reap(false);  // a long-running server does not accumulate finished threads
+    auto done = std::make_shared<std::atomic<bool>>(false);
     std::lock_guard lk(conn_mu_);
-    conns_.emplace_back([this, c] {
-      serve(c);
-      ::close(c);
-    });
+    conns_.push_back(Conn{std::thread([this, c, done] {
+                            serve(c);
+                            ::close(c);
+                            done->store(true);
+                          }),
+                          done});
   }
 }
 

@@ -20,6 +20,7 @@
 #include <atomic>
 #include <cstdint>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -56,8 +57,13 @@ class HttpService {
   std::atomic<bool> running_{false};
   std::atomic<uint64_t> next_id_{1};
   std::thread accept_thread_;
+  struct Conn {
+    std::thread t;
+    std::shared_ptr<std::atomic<bool>> done;
+  };
+  void reap(bool all);  // joins finished connection threads (all: every one)
   std::mutex conn_mu_;
-  std::list<std::thread> conns_;
+  std::list<Conn> conns_;
 };
 
 }  // namespace omni
