@@ -137,6 +137,16 @@ omni_status omni_ar_step(omni_stage* st, const omni_ar_batch* batch, int32_t* to
  * the top-2 logit margin. */
 omni_status omni_stage_set_sampling(omni_stage* st, int32_t top_k, uint64_t seed);
 
+/* Prefix cache of a Thinker stage (on by default): full
+ * 16-token prompt pages are keyed by a chained hash of their token prefix and
+ * shared read-only between sequences; a prefill span whose pages are cached
+ * runs only its uncached suffix on the device (prefill emits nothing, so the
+ * caller sees no difference: outputs are bit-identical). Toggle only with no
+ * resident sequence. Stats: prompt tokens served from the cache, pages held,
+ * pages evicted (when the KV pool runs out). */
+omni_status omni_stage_set_prefix_cache(omni_stage* st, int32_t enable);
+omni_status omni_stage_prefix_stats(const omni_stage* st, uint64_t* hit_tokens, uint64_t* cached_pages,
+                                    uint64_t* evicted_pages);
 /* SM share of a DiT stage: its denoise iteration is one persistent kernel that
  * holds whole SMs (192 KB shared memory, all of TMEM) for the iteration, so
  * beside AR stages on the same GPU it must leave them SMs. sms <= 0 = all SMs

@@ -189,6 +189,10 @@ void build_ar(omni_stage* st) {
   }
   st->free_pages.resize(pages);
   for (int i = 0; i < pages; ++i) st->free_pages[i] = pages - 1 - i;
+  // prefix cache: the Thinker's KV is a function of the prompt tokens alone
+  // (the Talker's also of its conditioning rows: never cached)
+  st->prefix.enabled = m.kind == OMNI_MODEL_THINKER;
+  st->prefix.refs.assign(pages, 0);
   st->free_slots.resize(st->lim.max_resident);
   for (int i = 0; i < st->lim.max_resident; ++i) st->free_slots[i] = st->lim.max_resident - 1 - i;
   // RoPE table (theta 10000, rotate-half), computed in double, stored fp32
@@ -372,16 +376,94 @@ SeqSlot& seq_for(omni_stage* st, uint64_t id) {
   return st->seqs.emplace(id, std::move(s)).first->second;
 }
 
+void prefix_evict(omni_stage* st);
+
 void ensure_pages(omni_stage* st, SeqSlot& s, int upto) {
   const int need = (upto + kPageTokens - 1) / kPageTokens;
   OMNI_REQUIRE(need <= st->max_pages, OMNI_E_OOM,
                "sequence longer than max_seq_len (" + std::to_string(st->lim.max_seq_len) + ")");
   while ((int)s.pages.size() < need) {
+    if (st->free_pages.empty()) prefix_evict(st);
     OMNI_REQUIRE(!st->free_pages.empty(), OMNI_E_OOM, "paged-KV pool exhausted");
     const int page = st->free_pages.back();
     st->pending_deltas.push_back(PageDelta{s.slot * st->max_pages + (int)s.pages.size(), page});
     s.pages.push_back(page);
     st->free_pages.pop_back();
+    if (!st->prefix.refs.empty()) st->prefix.refs[page] = 1;
+  }
+}
+
+// ---- prefix cache -------------------------------------------
+uint64_t prefix_page_key(uint64_t prev, const int32_t* t) {
+  uint64_t h = mix64(prev ^ 0x5be0cd19137e2179ull);
+  for (int i = 0; i < kPageTokens; ++i) h = mix64(h ^ (uint64_t)(uint32_t)t[i] ^ ((uint64_t)i << 40));
+  return h | 1;  // never 0
+}
+
+void page_unref(omni_stage* st, int page) {
+  auto& pc = st->prefix;
+  if (pc.refs.empty() || --pc.refs[page] == 0) st->free_pages.push_back(page);
+}
+
+// Drops every cached page no sequence maps (refs == 1: only the cache).
+void prefix_evict(omni_stage* st) {
+  auto& pc = st->prefix;
+  for (auto it = pc.key_of.begin(); it != pc.key_of.end();) {
+    if (pc.refs[it->first] == 1) {
+      pc.page_of.erase(it->second);
+      pc.refs[it->first] = 0;
+      st->free_pages.push_back(it->first);
+      ++pc.evicted_pages;
+      it = pc.key_of.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+// A prefill span of `s`: record its tokens and map every further full
+// prompt page already in the cache (stopping at the first miss).
+void prefix_lookup(omni_stage* st, SeqSlot& s, int pos0, int span, const int32_t* tokens) {
+  auto& pc = st->prefix;
+  if (s.no_cache) return;
+  if (pos0 != (int)s.toks.size()) {  // not a continuation of the recorded prompt
+    s.no_cache = true;
+    return;
+  }
+  s.toks.insert(s.toks.end(), tokens, tokens + span);
+  while (!s.lookup_done && s.pages.size() == s.keys.size() &&
+         (s.keys.size() + 1) * kPageTokens <= s.toks.size()) {
+    const size_t p = s.keys.size();
+    const uint64_t k = prefix_page_key(p ? s.keys.back() : 0, s.toks.data() + p * kPageTokens);
+    auto hit = pc.page_of.find(k);
+    if (hit == pc.page_of.end()) {
+      s.lookup_done = true;
+      break;
+    }
+    ++pc.refs[hit->second];
+    st->pending_deltas.push_back(PageDelta{s.slot * st->max_pages + (int)p, hit->second});
+    s.pages.push_back(hit->second);
+    s.keys.push_back(k);
+    s.cached_upto = (int)(p + 1) * kPageTokens;
+  }
+}
+
+// After a step computed prompt positions below `upto`: key and cache its
+// full pages.
+void prefix_insert(omni_stage* st, SeqSlot& s, int upto) {
+  auto& pc = st->prefix;
+  if (s.no_cache || upto <= s.cached_upto) return;  // this step computed nothing of it
+  s.lookup_done = true;  // computed pages follow: no more lookups for this sequence
+  while ((s.keys.size() + 1) * kPageTokens <= (size_t)std::min<int>(upto, (int)s.toks.size())) {
+    const size_t p = s.keys.size();
+    const uint64_t k = prefix_page_key(p ? s.keys.back() : 0, s.toks.data() + p * kPageTokens);
+    s.keys.push_back(k);
+    const int page = s.pages[p];
+    if (pc.page_of.count(k) || pc.key_of.count(page)) continue;  // already cached (another copy)
+    pc.page_of.emplace(k, page);
+    pc.key_of.emplace(page, k);
+    ++pc.refs[page];
+    ++pc.inserted_pages;
   }
 }
 
@@ -632,6 +714,11 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   OMNI_REQUIRE(ne <= st->lim.max_resident, OMNI_E_BADARG, "more entries than max_resident_requests");
   const ArDescLayout lay = ar_desc_layout(st);
   if (staging_reserve(st->desc, lay.reserve)) drop_graphs(st);
+  // prefix cache: map cached prompt pages before any fresh page is assigned
+  if (st->prefix.enabled)
+    for (int e = 0, i = 0; e < ne; i += b->span[e], ++e)
+      if (b->phase[e] == OMNI_PHASE_PREFILL)
+        prefix_lookup(st, seq_for(st, b->seq_id[e]), b->pos0[e], b->span[e], b->tokens + i);
   // every entry's pages first: a failure leaves the step unlaunched
   for (int e = 0; e < ne; ++e) ensure_pages(st, seq_for(st, b->seq_id[e]), b->pos0[e] + b->span[e]);
   OMNI_REQUIRE(st->pending_deltas.size() <= lay.cap_delta, OMNI_E_OOM,
@@ -644,14 +731,21 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   auto* dl = reinterpret_cast<PageDelta*>(st->desc.host + lay.off_delta + sizeof(PageDeltaHeader));
   int n_blocks = 0, n_groups = 0;
   std::vector<int> dec_list;
-  int r = 0, n_prefill_rows = 0;
-  for (int e = 0; e < ne; ++e) {
+  int r = 0, ir = 0, de = 0, n_prefill_rows = 0;
+  for (int e = 0; e < ne; ++e, ir += b->span[e - 1]) {
     SeqSlot& s = st->seqs.at(b->seq_id[e]);
     const bool is_dec = b->phase[e] == OMNI_PHASE_DECODE;
-    ArEntryDesc& ed = ents[e];
+    // prefill positions below cached_upto come from the prefix cache: the
+    // device runs only [pos0, pos0 + span) past them (prefill emits nothing,
+    // so the trim is invisible to the caller)
+    const int skip = is_dec ? 0 : std::clamp(s.cached_upto - b->pos0[e], 0, b->span[e]);
+    const int pos0 = b->pos0[e] + skip, span = b->span[e] - skip, ir0 = ir + skip;
+    st->prefix.hit_tokens += skip;
+    if (span == 0) continue;  // the whole prefill span was cached
+    ArEntryDesc& ed = ents[de];
     ed.slot = s.slot;
-    ed.q_len = b->span[e];
-    ed.pos0 = b->pos0[e];
+    ed.q_len = span;
+    ed.pos0 = pos0;
     ed.row0 = r;
     ed.is_decode = is_dec ? 1 : 0;
     ed.out_index = is_dec ? b->out_index[e] : -1;
@@ -661,34 +755,35 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       if (!talker)
         OMNI_REQUIRE(ed.out_index >= 0 && ed.out_index < st->ring_rows, OMNI_E_BADARG,
                      "thinker out_index outside the 64-row hidden ring");
-      dec[dec_list.size()] = e;
-      dec_list.push_back(e);
+      dec[dec_list.size()] = de;
+      dec_list.push_back(e);  // results go back to the caller's entry e
     }
-    for (int t0 = 0; t0 < b->span[e]; t0 += kAttnQTok) {
-      const int ntok = std::min(kAttnQTok, b->span[e] - t0);
+    for (int t0 = 0; t0 < span; t0 += kAttnQTok) {
+      const int ntok = std::min(kAttnQTok, span - t0);
       // long contexts: split the keys over P CTAs (flash-decoding), merged
       // in fixed part order by the last arriver. P is a function of this
       // block's own context length only (batch invariance).
-      const int n_chunks = (b->pos0[e] + t0 + ntok + 127) / 128;
+      const int n_chunks = (pos0 + t0 + ntok + 127) / 128;
       const int parts = std::min(kAttnMaxParts, (n_chunks + kAttnSplitChunks - 1) / kAttnSplitChunks);
       if (parts > 1 && st->split_part) {
         OMNI_REQUIRE(n_groups < st->split_groups, OMNI_E_BADARG, "split-KV groups exhausted");
         for (int pp = 0; pp < parts; ++pp)
-          blks[n_blocks++] = AttnBlockDesc{e, t0, ntok, attn_split_pack(pp, parts, n_groups)};
+          blks[n_blocks++] = AttnBlockDesc{de, t0, ntok, attn_split_pack(pp, parts, n_groups)};
         ++n_groups;
       } else {
-        blks[n_blocks++] = AttnBlockDesc{e, t0, ntok, 0};
+        blks[n_blocks++] = AttnBlockDesc{de, t0, ntok, 0};
       }
     }
-    for (int t = 0; t < b->span[e]; ++t, ++r) {
+    for (int t = 0; t < span; ++t, ++r) {
+      const int i = ir0 + t;  // caller's token row
       ArRowDesc& rd = rows[r];
-      rd.entry = e;
-      rd.pos = b->pos0[e] + t;
-      rd.token = b->tokens[r];
-      rd.cond_row = talker ? b->cond_row[r] : 0;
+      rd.entry = de;
+      rd.pos = pos0 + t;
+      rd.token = b->tokens[i];
+      rd.cond_row = talker ? b->cond_row[i] : 0;
       rd.slot = s.slot;
       rd.pad = 0;
-      rd.cond_src = (talker && !is_dec && b->cond_src) ? b->cond_src[r] : 0;
+      rd.cond_src = (talker && !is_dec && b->cond_src) ? b->cond_src[i] : 0;
       if (talker) {
         OMNI_REQUIRE(rd.cond_row >= 0 && rd.cond_row < st->cond_rows, OMNI_E_BADARG,
                      "talker cond_row outside the 64-row conditioning table");
@@ -700,7 +795,14 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
       OMNI_REQUIRE(rd.token >= -1 && rd.token < (talker && is_dec ? st->m.vocab : 256),
                    OMNI_E_BADARG, "input token id out of range");
     }
+    ++de;
   }
+  n_rows = r;
+  // full prompt pages this step computes become cache entries (reads of
+  // them by later steps are ordered on this stream)
+  if (st->prefix.enabled)
+    for (int e = 0; e < ne; ++e)
+      if (b->phase[e] == OMNI_PHASE_PREFILL) prefix_insert(st, st->seqs.at(b->seq_id[e]), b->pos0[e] + b->span[e]);
   // page assignments since the previous step (applied by the step's first kernel)
   dh->n = (int32_t)st->pending_deltas.size();
   for (size_t i = 0; i < st->pending_deltas.size(); ++i) dl[i] = st->pending_deltas[i];
@@ -1178,7 +1280,7 @@ omni_status omni_seq_release(omni_stage* st, uint64_t seq_id) {
     if (it == st->seqs.end()) return;
     // Pages may still be read by an in-flight step on this stage's stream;
     // stream order makes reuse by a later step safe.
-    for (int p : it->second.pages) st->free_pages.push_back(p);
+    for (int p : it->second.pages) page_unref(st, p);
     st->free_slots.push_back(it->second.slot);
     st->seqs.erase(it);
   });
@@ -1341,6 +1443,26 @@ omni_status omni_stage_set_sm_share(omni_stage* st, int32_t sms) {
     if (want != st->dit_ctas) drop_graphs(st);  // the grid size is baked into the step graphs
     st->dit_ctas = want;
     prewarm_dit_graphs(st);
+  });
+}
+
+omni_status omni_stage_set_prefix_cache(omni_stage* st, int32_t enable) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && st->m.kind == OMNI_MODEL_THINKER, OMNI_E_BADARG,
+                 "the prefix cache applies to Thinker stages (KV a function of the prompt alone)");
+    OMNI_REQUIRE(st->seqs.empty(), OMNI_E_BADARG, "toggle the prefix cache with no resident sequence");
+    ensure_idle(st);
+    if (!enable) prefix_evict(st);  // every cached page is held by the cache alone now
+    st->prefix.enabled = enable != 0;
+  });
+}
+
+omni_status omni_stage_prefix_stats(const omni_stage* st, uint64_t* hit_tokens, uint64_t* cached_pages,
+                                    uint64_t* evicted_pages) {
+  return guarded([&] {
+    if (hit_tokens) *hit_tokens = st->prefix.hit_tokens;
+    if (cached_pages) *cached_pages = st->prefix.key_of.size();
+    if (evicted_pages) *evicted_pages = st->prefix.evicted_pages;
   });
 }
 

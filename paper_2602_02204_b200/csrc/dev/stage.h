@@ -38,6 +38,25 @@ struct DitLayer {
 struct SeqSlot {
   int slot = -1;
   std::vector<int> pages;
+  // prefix cache (Thinker prompts): prompt tokens fed so far, chained keys of
+  // its full prompt pages, positions [0, cached_upto) mapped from the cache
+  std::vector<int32_t> toks;
+  std::vector<uint64_t> keys;
+  int cached_upto = 0;
+  bool lookup_done = false;  // the first miss ends lookups (computed positions stay contiguous)
+  bool no_cache = false;     // prompt fed out of order: never keyed
+};
+
+// Prefix cache over full 16-token prompt pages of a stage whose KV depends on
+// the prompt tokens only (the Thinker): chained key of page p = f(key of page
+// p-1, its 16 token ids) -> physical page, shared read-only by every sequence
+// with that prefix. refs[page] = sequences mapping it + 1 while cached.
+struct PrefixCache {
+  bool enabled = false;
+  std::unordered_map<uint64_t, int> page_of;
+  std::unordered_map<int, uint64_t> key_of;
+  std::vector<int> refs;
+  uint64_t hit_tokens = 0, inserted_pages = 0, evicted_pages = 0;
 };
 
 // An instantiated CUDA graph of one step's kernel sequence.
@@ -100,6 +119,7 @@ struct omni_stage {
   omni_dev::GemmInput in_xn, in_attn, in_act, in_hbuf, in_cond;
   std::unordered_map<uint64_t, omni_dev::SeqSlot> seqs;
   std::vector<int> free_slots, free_pages;
+  omni_dev::PrefixCache prefix;
 
   // ---- DiT model ----
   omni_dev::DevTensor w_in, pos_emb, tok_emb, t_emb, w_out, w_mod;

@@ -92,6 +92,14 @@ class Stage:
         """Greedy (top_k <= 1) or top-k sampling of decode rows (omni_stage_set_sampling)."""
         check(self.lib.omni_stage_set_sampling(self.h, top_k, C.c_uint64(seed)))
 
+    def set_prefix_cache(self, enable: bool) -> None:
+        check(self.lib.omni_stage_set_prefix_cache(self.h, 1 if enable else 0))
+
+    def prefix_stats(self) -> dict:
+        h, c, e = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(self.lib.omni_stage_prefix_stats(self.h, C.byref(h), C.byref(c), C.byref(e)))
+        return {"hit_tokens": h.value, "cached_pages": c.value, "evicted_pages": e.value}
+
     def set_sm_share(self, sms: int) -> None:
         """SMs a DiT stage's persistent iteration may hold (<= 0: all; omni_stage_set_sm_share)."""
         check(self.lib.omni_stage_set_sm_share(self.h, sms))
