@@ -1,15 +1,15 @@
 #!/usr/bin/env bash
-# Per-item traces of the fused DiT (all SMs and a 64-SM share) per tile variant + probe.
+# Per-item traces of the fused DiT (all SMs and the 48-SM pipeline share) + probe.
 set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 tag=${1:-dtr}
-for w in ${WIDE:-128 16}; do
-  OMNI_DIT_WIDE_FROM=$w timeout 600 python tools/dit_trace.py 16 96 512 > gpurun_out/${tag}_w${w}_all.jsonl 2>&1; echo "trace w$w rc=$?"
-  OMNI_DIT_WIDE_FROM=$w timeout 600 python tools/dit_trace.py --sms=64 16 96 512 > gpurun_out/${tag}_w${w}_64.jsonl 2>&1; echo "trace64 w$w rc=$?"
+for w in all; do
+  timeout 600 python tools/dit_trace.py 16 96 512 > gpurun_out/${tag}_w${w}_all.jsonl 2>&1; echo "trace rc=$?"
+  timeout 600 python tools/dit_trace.py --sms=48 16 96 512 > gpurun_out/${tag}_w${w}_48.jsonl 2>&1; echo "trace48 rc=$?"
   python - <<PY
 import json
-for f in ["gpurun_out/${tag}_w${w}_all.jsonl", "gpurun_out/${tag}_w${w}_64.jsonl"]:
+for f in ["gpurun_out/${tag}_w${w}_all.jsonl", "gpurun_out/${tag}_w${w}_48.jsonl"]:
     for l in open(f):
         try: d = json.loads(l)
         except Exception: print(l.strip()[:300]); continue
