@@ -8,12 +8,23 @@
 // pack_chunk (reference_pipeline.hpp:113-123) + encode_payload + stash
 // (connector.hpp:214-236).
 //
+// The chunk descriptor and the chunk's token ids live in pinned host memory
+// and are read over UVA (no H2D copy ahead of the pack on the Thinker
+// stream): small reads over PCIe are throughput-limited, so each block reads
+// them ONCE into shared memory and the grid has only a few blocks per chunk
+// (each thread loops over its words). The row of a blob word comes from a
+// float reciprocal with an exact integer correction (no 64-bit division per
+// thread). At 16.8 MB (64 chunks x 64 rows x d 2048) the first version took
+// 52.6 us (0.10 of HBM) with per-thread UVA reads (profiles/r02_pack_large.txt).
+//
 // Every thread produces one aligned 16-byte word of the blob. Interior words
 // (8 hidden elements of one row) are assembled from two 128-bit loads of the
 // 16-B aligned hidden ring with a funnel shift — the row start moves by one
 // u16 per row because of the token column — so both sides of the copy are
 // 128-bit vector accesses; header / token-column / row-crossing words take a
 // scalar path.
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -25,8 +36,17 @@ namespace omni_dev {
 
 namespace {
 
-__device__ __forceinline__ uint32_t u16_at(const PackChunkDesc& c, const __nv_bfloat16* ring, int d,
-                                           int ring_rows, int64_t u) {
+// row of hidden element e (= u16 slot - 5) in a blob of rows of w = d + 1 u16:
+// e / w from a float reciprocal (exact after one correction step: e < 2^24)
+__device__ __forceinline__ uint32_t row_of(uint32_t e, uint32_t w, float inv_w) {
+  uint32_t r = __float2uint_rz((float)e * inv_w);
+  if (r * w > e) --r;
+  else if ((r + 1) * w <= e) ++r;
+  return r;
+}
+
+__device__ __forceinline__ uint32_t u16_at(const PackChunkDesc& c, const int32_t* tok, const __nv_bfloat16* ring,
+                                           int d, int ring_rows, int64_t u) {
   // u = u16 slot index within the blob; slots 0..4 are the 10-byte header.
   if (u < 5) {
     const uint32_t n = (uint32_t)(c.end - c.begin), w = (uint32_t)(d + 1);
@@ -38,9 +58,9 @@ __device__ __forceinline__ uint32_t u16_at(const PackChunkDesc& c, const __nv_bf
       default: return w >> 16;
     }
   }
-  const int64_t e = u - 5;
-  const int64_t r = e / (d + 1), col = e % (d + 1);
-  if (col == 0) return (uint32_t)c.tokens_dev[r] & 0xFFFFu;
+  const uint32_t e = (uint32_t)(u - 5), w = (uint32_t)d + 1;
+  const uint32_t r = row_of(e, w, 1.f / (float)w), col = e - r * w;
+  if (col == 0) return (uint32_t)tok[r] & 0xFFFFu;
   const unsigned short* row =
       reinterpret_cast<const unsigned short*>(ring + ((size_t)c.slot * ring_rows + c.begin + r) * d);
   return row[col - 1];
@@ -51,7 +71,15 @@ __global__ void pack_hidden_kernel(const PackChunkDesc* __restrict__ chunks,
                                    uint8_t* __restrict__ dst_base) {
   pdl_wait();
   pdl_trigger();
-  const PackChunkDesc c = chunks[blockIdx.y];
+  __shared__ PackChunkDesc sc;
+  __shared__ int32_t stok[kPackMaxRows];
+  if (threadIdx.x == 0) sc = chunks[blockIdx.y];  // one UVA read per block
+  __syncthreads();
+  const PackChunkDesc c = sc;
+  for (int i = threadIdx.x; i < c.end - c.begin; i += blockDim.x) stok[i] = c.tokens_dev[i];
+  __syncthreads();
+  const uint32_t wrow = (uint32_t)d + 1;
+  const float inv_w = 1.f / (float)wrow;
   const int64_t rows = c.end - c.begin;
   const int64_t total_u16 = 5 + rows * (d + 1);
   const int64_t words = (total_u16 + 7) / 8;
@@ -62,8 +90,8 @@ __global__ void pack_hidden_kernel(const PackChunkDesc* __restrict__ chunks,
     uint32_t w[4];
     bool fast = false;
     if (u0 >= 5 && u0 + 7 < total_u16) {
-      const int64_t e0 = u0 - 5;
-      const int64_t r = e0 / (d + 1), col0 = e0 % (d + 1);
+      const uint32_t e0 = (uint32_t)(u0 - 5);
+      const uint32_t r = row_of(e0, wrow, inv_w), col0 = e0 - r * wrow;
       if (col0 >= 1 && col0 + 7 <= d) {  // 8 hidden values of one row
         fast = true;
         const int h0 = (int)col0 - 1;
@@ -88,8 +116,8 @@ __global__ void pack_hidden_kernel(const PackChunkDesc* __restrict__ chunks,
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const int64_t ua = u0 + 2 * m, ub = ua + 1;
-        const uint32_t lo16 = ua < total_u16 ? u16_at(c, ring, d, ring_rows, ua) : 0u;
-        const uint32_t hi16 = ub < total_u16 ? u16_at(c, ring, d, ring_rows, ub) : 0u;
+        const uint32_t lo16 = ua < total_u16 ? u16_at(c, stok, ring, d, ring_rows, ua) : 0u;
+        const uint32_t hi16 = ub < total_u16 ? u16_at(c, stok, ring, d, ring_rows, ub) : 0u;
         w[m] = lo16 | (hi16 << 16);
       }
     }
@@ -103,12 +131,17 @@ uint64_t pack_blob_bytes(int rows, int d) { return 10ull + 2ull * (uint64_t)rows
 
 cudaError_t launch_pack_hidden(const PackChunkDesc* chunks_dev, int n_chunks, int max_rows,
                                const __nv_bfloat16* ring, int d, int ring_rows, uint8_t* dst_base,
-                               cudaStream_t st) {
+                               bool desc_on_device, cudaStream_t st) {
   if (n_chunks == 0) return cudaSuccess;
+  if (max_rows > kPackMaxRows) return cudaErrorInvalidValue;
   const int64_t words = (pack_blob_bytes(max_rows, d) + 15) / 16;
   const int threads = 256;
-  const int bx = (int)((words + threads - 1) / threads);
-  dim3 grid(bx < 1 ? 1 : bx, n_chunks);
+  // one word per thread when the descriptors are in device memory; over UVA
+  // (small packs) few blocks per chunk: every block reads them once
+  const int64_t by_words = (words + threads - 1) / threads;
+  const int64_t want = desc_on_device ? by_words : (296 + n_chunks - 1) / n_chunks;
+  const int bx = (int)std::max<int64_t>(1, std::min(by_words, want));
+  dim3 grid(bx, n_chunks);
   return launch_k(pack_hidden_kernel, grid, dim3(threads), 0, st, 1, chunks_dev, ring, d, ring_rows, dst_base);
 }
 

@@ -16,9 +16,11 @@ struct PackChunkDesc {
   const int32_t* tokens_dev;   // [end-begin] token ids (device)
 };
 
+constexpr int kPackMaxRows = 256;
+constexpr int kPackUvaRows = 64;   // packs of more rows copy their descriptors to the device first  // rows of one chunk (the hidden ring holds 64 per sequence)
 uint64_t pack_blob_bytes(int rows, int d);
 cudaError_t launch_pack_hidden(const PackChunkDesc* chunks_dev, int n_chunks, int max_rows,
                                const __nv_bfloat16* ring, int d, int ring_rows, uint8_t* dst_base,
-                               cudaStream_t st);
+                               bool desc_on_device, cudaStream_t st);
 
 }  // namespace omni_dev

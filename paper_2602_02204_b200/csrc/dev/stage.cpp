@@ -1391,10 +1391,13 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
     staging_reserve(src->pack, total);
     auto* cd = reinterpret_cast<PackChunkDesc*>(src->pack.host);
     auto* tk = reinterpret_cast<int32_t*>(src->pack.host + off_tok);
-    // the pack kernel reads its descriptors straight from the pinned staging
-    // buffer (UVA) -- no copy-engine H2D ahead of it on the thinker stream,
-    // where the next Thinker step queues behind it
-    const uint8_t* desc_base = src->pack.host;
+    // Production-size packs (a few rows) read their descriptors straight from
+    // the pinned staging buffer (UVA): no copy-engine H2D ahead of them on the
+    // Thinker stream, where the next step queues behind. Large packs copy
+    // them to the device first: small PCIe reads are throughput-limited
+    // (profiles/r02_pack_large.txt).
+    const bool copy_first = total_rows > kPackUvaRows;
+    const uint8_t* desc_base = copy_first ? src->pack.dev : src->pack.host;
     const auto* tk_dev = reinterpret_cast<const int32_t*>(desc_base + off_tok);
     int at = 0;
     for (int c = 0; c < n_chunks; ++c) {
@@ -1405,9 +1408,10 @@ omni_status omni_pack_hidden(omni_stage* src, int32_t n_chunks, const uint64_t* 
     }
     cudaStream_t s = src->stream;
     counters().h2d_bytes += total;
+    if (copy_first) OMNI_CUDA(cudaMemcpyAsync(src->pack.dev, src->pack.host, total, cudaMemcpyHostToDevice, s));
     OMNI_KERNEL(launch_pack_hidden(reinterpret_cast<const PackChunkDesc*>(desc_base), n_chunks, max_rows,
                                  src->ring, src->m.d_model, src->ring_rows, reinterpret_cast<uint8_t*>(dst_base),
-                                 s));
+                                 copy_first, s));
     OMNI_CUDA(cudaEventRecord(src->pack.in_use, s));  // staging read by the kernel
     // consumers wait for exactly this pack (omni_stage_after_pack), not for
     // whatever the producer enqueues after it (its next step)
