@@ -158,6 +158,11 @@ omni_status omni_stage_set_sm_share(omni_stage* st, int32_t sms);
  * failing the whole batched step (the reference fails per entry,
  * ar_engine.hpp:332-334). omni_ar_step reserves implicitly. */
 omni_status omni_seq_reserve(omni_stage* st, uint64_t seq_id, int32_t upto_tokens);
+/* The same for a PREFILL span [pos0, pos0 + span) with its prompt token ids:
+ * a Thinker stage first maps the span's cached prompt pages (prefix cache),
+ * so reserving ahead of the step does not pre-empt the cache. */
+omni_status omni_seq_reserve_prompt(omni_stage* st, uint64_t seq_id, int32_t pos0, int32_t span,
+                                    const int32_t* tokens);
 
 /* Frees the KV pages / hidden ring / conditioning rows of a sequence
  * (finish, recompute-preemption ar_engine.hpp:233-257, or failure). */

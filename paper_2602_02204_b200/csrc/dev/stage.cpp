@@ -426,11 +426,13 @@ void prefix_evict(omni_stage* st) {
 void prefix_lookup(omni_stage* st, SeqSlot& s, int pos0, int span, const int32_t* tokens) {
   auto& pc = st->prefix;
   if (s.no_cache) return;
-  if (pos0 != (int)s.toks.size()) {  // not a continuation of the recorded prompt
+  if (pos0 > (int)s.toks.size()) {  // a gap: not a continuation of the recorded prompt
     s.no_cache = true;
     return;
   }
-  s.toks.insert(s.toks.end(), tokens, tokens + span);
+  // record the span's new tokens (a span may be seen twice: reserve, then step)
+  const int have = (int)s.toks.size() - pos0;
+  if (have < span) s.toks.insert(s.toks.end(), tokens + have, tokens + span);
   while (!s.lookup_done && s.pages.size() == s.keys.size() &&
          (s.keys.size() + 1) * kPageTokens <= s.toks.size()) {
     const size_t p = s.keys.size();
@@ -1434,6 +1436,17 @@ omni_status omni_seq_reserve(omni_stage* st, uint64_t seq_id, int32_t upto_token
     OMNI_REQUIRE(st && st->m.kind != OMNI_MODEL_DIT, OMNI_E_BADARG, "omni_seq_reserve needs an AR stage");
     OMNI_REQUIRE(upto_tokens >= 0, OMNI_E_BADARG, "negative token count");
     ensure_pages(st, seq_for(st, seq_id), upto_tokens);
+  });
+}
+
+omni_status omni_seq_reserve_prompt(omni_stage* st, uint64_t seq_id, int32_t pos0, int32_t span,
+                                    const int32_t* tokens) {
+  return guarded([&] {
+    OMNI_REQUIRE(st && st->m.kind != OMNI_MODEL_DIT, OMNI_E_BADARG, "omni_seq_reserve_prompt needs an AR stage");
+    OMNI_REQUIRE(pos0 >= 0 && span >= 0 && (span == 0 || tokens), OMNI_E_BADARG, "bad prompt span");
+    SeqSlot& s = seq_for(st, seq_id);
+    if (st->prefix.enabled && span > 0) prefix_lookup(st, s, pos0, span, tokens);
+    ensure_pages(st, s, pos0 + span);
   });
 }
 

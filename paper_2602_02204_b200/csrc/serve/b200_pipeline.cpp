@@ -582,6 +582,14 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
     m.prefill = trace_prefill(s->name);
     m.on_prompt_consumed = trace_consumed(s->name, s->kind == OMNI_MODEL_TALKER);
     m.reserve = [s](const BatchSlot& b) {
+      if (s->kind == OMNI_MODEL_THINKER && b.phase == Phase::PREFILL && b.seq) {
+        // prompt ids of the span: the prefix cache maps cached pages first
+        std::vector<int32_t> ids(b.seq->prompt.begin() + b.pos0, b.seq->prompt.begin() + b.pos0 + b.span);
+        dev_ok(omni_seq_reserve_prompt(s->st, b.request_id, static_cast<int32_t>(b.pos0),
+                                       static_cast<int32_t>(b.span), ids.data()),
+               "omni_seq_reserve_prompt");
+        return;
+      }
       dev_ok(omni_seq_reserve(s->st, b.request_id, static_cast<int32_t>(b.pos0 + b.span)), "omni_seq_reserve");
     };
     m.pack_chunk = [s](const SeqState& q, size_t b, size_t e) { return s->pack_chunk(q, b, e); };

@@ -92,6 +92,10 @@ class Stage:
         """Greedy (top_k <= 1) or top-k sampling of decode rows (omni_stage_set_sampling)."""
         check(self.lib.omni_stage_set_sampling(self.h, top_k, C.c_uint64(seed)))
 
+    def reserve_prompt(self, seq_id: int, pos0: int, tokens) -> None:
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        check(self.lib.omni_seq_reserve_prompt(self.h, C.c_uint64(seq_id), pos0, len(t), _p(t, C.c_int32)))
+
     def set_prefix_cache(self, enable: bool) -> None:
         check(self.lib.omni_stage_set_prefix_cache(self.h, 1 if enable else 0))
 

@@ -15,13 +15,17 @@ pytestmark = pytest.mark.gpu
 SMALL = dict(d_model=512, n_layers=2, n_heads=4, n_kv_heads=1, d_ff=1024)
 
 
-def run(st, prompts, order, n_dec=6, chunk=32):
+def run(st, prompts, order, n_dec=6, chunk=32, reserve=False):
     """Prefill each prompt in `chunk`-token spans (one sequence per step, in
-    `order`), then decode all sequences together. Returns tokens / hidden rows."""
+    `order`), then decode all sequences together. Returns tokens / hidden rows.
+    reserve: admit every prefill span ahead of its step the way the pipeline
+    does (omni_seq_reserve_prompt)."""
     for s in order:
         p = prompts[s]
         for at in range(0, len(p), chunk):
             sp = min(chunk, len(p) - at)
+            if reserve:
+                st.reserve_prompt(s, at, p[at:at + sp])
             st.ar_step([s], [D.PREFILL], [sp], [at], [-1], p[at:at + sp])
     seqs = sorted(prompts)
     toks = {s: [] for s in seqs}
@@ -44,7 +48,8 @@ def prompts_with_shared_prefix(rng, prefix_len=80):
             4: [int(x) for x in rng.integers(1, 256, size=50)]}               # shares nothing
 
 
-def test_prefix_cache_outputs_bit_identical_and_hits_counted():
+@pytest.mark.parametrize("reserve", [False, True])
+def test_prefix_cache_outputs_bit_identical_and_hits_counted(reserve):
     m = D.model_default(D.THINKER, **SMALL)
     rng = np.random.default_rng(5)
     prompts = prompts_with_shared_prefix(rng)
@@ -53,7 +58,7 @@ def test_prefix_cache_outputs_bit_identical_and_hits_counted():
     t0, h0 = run(ref, prompts, [1, 2, 3, 4])
     ref.close()
     st = D.Stage(m, D.StageLimits(256, 8, 256, 0, 64), seed=3)
-    t1, h1 = run(st, prompts, [1, 2, 3, 4])
+    t1, h1 = run(st, prompts, [1, 2, 3, 4], reserve=reserve)
     stats = st.prefix_stats()
     # seq 2 reuses seq 1's 5 full prefix pages (80 tokens), seq 3 two pages (32)
     assert stats["hit_tokens"] == 80 + 32, stats
