@@ -87,12 +87,15 @@ ControlMessage decode_control_frame(std::span<const uint8_t> frame) {
       l.dtype = static_cast<Dtype>(tag);
       l.shape.resize(r.u8());
       uint64_t elems = 1;
+      bool overflow = false;
       for (auto& d : l.shape) {
         d = r.u32();
-        elems *= d;
+        overflow = overflow || __builtin_mul_overflow(elems, (uint64_t)d, &elems);
       }
+      uint64_t body = 0;
+      overflow = overflow || __builtin_mul_overflow(elems, (uint64_t)dtype_width(l.dtype), &body);
       // the blob must hold exactly header + body (payload.hpp:142-166)
-      if (l.length != payload_header_bytes(l.shape.size()) + elems * dtype_width(l.dtype))
+      if (overflow || l.length != payload_header_bytes(l.shape.size()) + body)
         throw ProtocolViolation("device locator length does not match its shape");
       const uint32_t nt = r.u32();
       if (nt > (frame.size() - r.pos) / 4) throw ProtocolViolation("short read");
