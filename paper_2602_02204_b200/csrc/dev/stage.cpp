@@ -282,7 +282,7 @@ void build_dit(omni_stage* st) {
   {
     int sms = 0;
     OMNI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->dev));
-    st->dit_ctas = sms;
+    st->dit_ctas = st->dit_sms_all = sms;
   }
   if (const char* e = std::getenv("OMNI_DIT_TRACE"); e && e[0] == '1') {
     st->dit_trace_items = dit_fused_items(n_rt, kDitTileRows, d, m.n_heads, ff, L, m.dit_steps, st->down_split);
@@ -835,6 +835,20 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
 // ---------------------------------------------------------------------------
 // DiT step
 // ---------------------------------------------------------------------------
+// Persistent grid of a fused DiT iteration of nt (padded) tokens. Beside AR
+// stages the DiT holds `dit_ctas` SMs (its share) for small batches and grows
+// with the batch -- one CTA per kDitTokPerCta tokens, up to every SM --
+// because a big iteration on a small share lands late on every request's tail.
+// A function of nt alone: graphs stay keyed by nt, and outputs do not depend
+// on the grid. Pipeline req/s (profiles/r02_dit_sm_share.txt), fixed share 48
+// vs tokens per CTA 4 / 3 / 2 / 1: c16 216 / 219 / 224-229 / 228 / 207,
+// c64 279 / 346 / 348 / 341 / 314.
+constexpr int kDitTokPerCta = 3;
+int dit_ctas_for(const omni_stage* st, int64_t nt) {
+  if (st->dit_ctas >= st->dit_sms_all) return st->dit_ctas;
+  return (int)std::min<int64_t>(st->dit_sms_all, std::max<int64_t>(st->dit_ctas, nt / kDitTokPerCta));
+}
+
 bool dit_fused_enabled() {  // OMNI_DIT_FUSED=0: one kernel per op (A/B only)
   static const bool on = [] {
     const char* e = std::getenv("OMNI_DIT_FUSED");
@@ -848,7 +862,8 @@ bool dit_fused_enabled() {  // OMNI_DIT_FUSED=0: one kernel per op (A/B only)
 void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
   const auto& m = st->m;
   const int d = m.d_model, L = m.n_layers, C = m.dit_channels, S = kDitSamples;
-  const int tile_rows = dit_tile_rows(n_tok, st->dit_ctas);
+  const int ctas = dit_ctas_for(st, n_tok);
+  const int tile_rows = dit_tile_rows(n_tok, ctas);
   const int n_rt = n_tok * S / tile_rows, nfd = d / kDitFeat;
   cudaStream_t s = st->stream;
   OMNI_KERNEL(dit_noise(toks_dev, n_tok, S, C, st->seed ^ kNoiseSeedSalt, st->dx, st->dxin, s, st->dctl,
@@ -887,7 +902,7 @@ void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int3
   p.dt = 1.f / m.dit_steps;
   p.sample_scale = kSampleScale;
   p.trace = st->dit_trace;
-  OMNI_KERNEL(dit_fused_run(p, st->dit_stages, st->dit_ctas, s));
+  OMNI_KERNEL(dit_fused_run(p, st->dit_stages, ctas, s));
 }
 
 void dit_chunk(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
@@ -956,7 +971,7 @@ constexpr int kDitPadTok = kDitTileTok;  // DiT batches are padded to whole 128-
 int64_t dit_pad_tokens(const omni_stage* st, int64_t n) {
   if (n == 0) return 0;
   const int64_t p8 = (n + kDitPadTok - 1) / kDitPadTok * kDitPadTok;
-  return p8 >= st->dit_ctas ? (n + 15) / 16 * 16 : p8;
+  return p8 >= dit_ctas_for(st, p8) ? (n + 15) / 16 * 16 : p8;
 }
 uint64_t dit_graph_key(int nt, int64_t t0) { return (uint64_t)nt << 20 | (uint64_t)t0; }
 
@@ -1459,6 +1474,7 @@ omni_status omni_stage_set_sm_share(omni_stage* st, int32_t sms) {
     const int want = sms <= 0 ? n : std::min(sms, n);
     if (want != st->dit_ctas) drop_graphs(st);  // the grid size is baked into the step graphs
     st->dit_ctas = want;
+    st->dit_sms_all = n;
     prewarm_dit_graphs(st);
   });
 }

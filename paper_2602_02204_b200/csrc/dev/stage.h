@@ -136,7 +136,8 @@ struct omni_stage {
   float* dpart = nullptr;
   int* dctl = nullptr;
   int dctl_n = 0, down_split = 1, dit_stages = 4;
-  int dit_ctas = 0;  // persistent grid of the fused iteration (omni_stage_set_sm_share)
+  int dit_ctas = 0;  // SM share of the fused iteration (omni_stage_set_sm_share); see dit_ctas_for
+  int dit_sms_all = 0;
   omni_dev::DitMaps* dmaps = nullptr;  // device copy of the fused iteration's TMA descriptors
   unsigned long long* dit_trace = nullptr;  // OMNI_DIT_TRACE=1 (tools/dit_trace.py)
   int dit_trace_items = 0;
