@@ -1175,15 +1175,14 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
     OMNI_CUDA(cudaSetDevice(dev));
     // Stream priority by stage kind when stages share a GPU. OMNI_PRIO = three
     // digits, the urgency rank (0 = most urgent) of thinker / talker / DiT.
-    // Default "101": the Talker's 4L dependent decode steps are the longest
-    // chain of every request; with the split-K push reduction, warp-MMA
-    // attention and prewarmed graphs it now wins 194.6 vs 185.3 req/s (median
-    // of 3) over all-equal (profiles/r01_bench_prio_ab3.txt; before those
-    // changes equal ranks measured best, profiles/r01_bench_prio_ab.txt).
+    // Default "001": both AR chains above the DiT. With the fused DiT on a
+    // batch-sized share, Thinker and Talker at equal rank beat Talker-first
+    // ("101", round 1's winner) by ~4 % at c16 and ~11 % at c64
+    // (profiles/r02_stream_priority.txt).
     int lo = 0, hi = 0;
     OMNI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // hi = numerically lowest = most urgent
     const char* pe = std::getenv("OMNI_PRIO");
-    const char* ranks = (pe && std::strlen(pe) == 3) ? pe : "101";
+    const char* ranks = (pe && std::strlen(pe) == 3) ? pe : "001";
     const int kind_ix = model->kind == OMNI_MODEL_THINKER ? 0 : model->kind == OMNI_MODEL_TALKER ? 1 : 2;
     const int rank = std::clamp(ranks[kind_ix] - '0', 0, 2);
     const int prio = hi + (lo - hi) * rank / 2;
