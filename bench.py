@@ -226,8 +226,10 @@ def cpu_baseline(sample_n: int, small: bool) -> dict:
     if not exe.exists():
         return {"value": None, "unit": "requests/s", "kind": "reference", "cores": os.cpu_count(),
                 "sample": f"unavailable: {exe} not built"}
+    # every host thread (torchrun exports OMP_NUM_THREADS=1 to each rank)
+    env = dict(os.environ, OMP_NUM_THREADS=str(os.cpu_count() or 1))
     r = subprocess.run([str(exe), str(CONFIG), str(sample_n), "7", "16", "1" if small else "0"],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900, env=env)
     if r.returncode != 0:
         return {"value": None, "unit": "requests/s", "kind": "reference", "cores": os.cpu_count(),
                 "sample": f"failed: {r.stderr.strip()[-200:]}"}
