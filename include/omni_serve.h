@@ -93,6 +93,13 @@ omni_status omni_pipeline_serve_start(omni_pipeline* p, const char* listen, int3
 /* Stops accepting, drains in-flight requests, stops the loop. */
 omni_status omni_pipeline_serve_stop(omni_pipeline* p);
 
+/* Stage worker process: listens on the AF_UNIX `socket_path`,
+ * accepts one orchestrator and runs the stages it creates there (steps,
+ * connector arenas exported with CUDA IPC, interprocess events) until it is
+ * told to shut down. A deployment plan places a stage in a worker with
+ * "workers": {"<stage id>": "<socket path>"} (omni_stage_worker.hpp). */
+omni_status omni_worker_serve(const char* socket_path, int32_t accept_timeout_ms);
+
 const char* omni_serve_last_error(void);
 
 #ifdef __cplusplus

@@ -16,9 +16,11 @@
 #include <algorithm>
 #include <cstdlib>
 #include <chrono>
+#include <optional>
 #include <unordered_map>
 
 #include "omni/errors.hpp"
+#include "omni/stage_worker.hpp"
 
 namespace omni {
 
@@ -37,11 +39,24 @@ class Arena {
   Arena(int dev, uint64_t bytes) : dev_(dev), bytes_(bytes) {
     dev_ok(omni_arena_create(dev, bytes, &arena_), "omni_arena_create");
     dev_ok(omni_arena_base(arena_, &base_, nullptr), "omni_arena_base");
+    remote_base_ = base_;
+    free_[0] = bytes;
+  }
+  // An arena a stage worker allocated and exported (CUDA IPC), mapped here:
+  // producers in this process pack into it; addresses handed to the worker
+  // are rebased onto its own mapping.
+  Arena(WorkerClient& w, int dev, uint64_t bytes) : dev_(dev), bytes_(bytes) {
+    omni_ipc_handle h{};
+    w.create_arena(dev, bytes, &h, &remote_base_);
+    dev_ok(omni_arena_import(&h, &arena_), "omni_arena_import");
+    dev_ok(omni_arena_base(arena_, &base_, nullptr), "omni_arena_base");
     free_[0] = bytes;
   }
   ~Arena() { omni_arena_destroy(arena_); }
   uint64_t base() const { return base_; }
   int device() const { return dev_; }
+  // a local address inside the arena -> the same byte in the worker's mapping
+  uint64_t rebase(uint64_t addr) const { return addr ? addr - base_ + remote_base_ : 0; }
   uint64_t alloc(uint64_t rid, uint64_t n) {
     n = (n + 255) & ~uint64_t(255);
     for (auto it = free_.begin(); it != free_.end(); ++it) {
@@ -77,7 +92,7 @@ class Arena {
  private:
   omni_arena* arena_ = nullptr;
   int dev_ = 0;
-  uint64_t base_ = 0, bytes_ = 0;
+  uint64_t base_ = 0, bytes_ = 0, remote_base_ = 0;
   std::map<uint64_t, uint64_t> free_;
   std::unordered_map<uint64_t, std::vector<std::pair<uint64_t, uint64_t>>> owned_;
 };
@@ -125,6 +140,14 @@ struct ArStage {
   Tracer* tracer = nullptr;
   // parity capture (tests): thinker hidden rows per request, [index][d] bf16 bits
   std::map<uint64_t, std::vector<uint16_t>>* capture = nullptr;
+  // stage hosted by a worker process (omni_stage calls become requests)
+  WorkerClient* remote = nullptr;
+  uint64_t remote_id = 0, remote_weight_bytes = 0;
+  Arena* own_arena = nullptr;             // remote talker: its connector arena (rebase)
+  std::vector<uint64_t> wait_events;      // remote talker: upstream pack events (worker ids)
+  omni_ipc_event* pack_event = nullptr;   // thinker packing into a worker's arena
+  bool pack_remote = false;
+  std::optional<WorkerClient::StepReply> reply;
   // step arrays (kept alive until the step completes)
   std::vector<uint64_t> seq_id, cond_src;
   std::vector<int32_t> phase, span, pos0, out_index, tokens, cond_row, tok_out;
@@ -144,6 +167,8 @@ struct ArStage {
 
   ~ArStage() {
     if (st) omni_stage_destroy(st);
+    if (remote && remote_id) remote->destroy_stage(remote_id);
+    if (pack_event) omni_ipc_event_destroy(pack_event);
   }
 
   void launch(std::vector<BatchSlot>& slots) {
@@ -194,7 +219,7 @@ struct ArStage {
     }
     // order this step after the packs that wrote its rows (possibly on other
     // GPUs) -- only the packs, not the producers' later steps
-    if (reads_rows)
+    if (reads_rows && !remote)
       for (ArStage* up : upstreams) dev_ok(omni_stage_after_pack(st, up->st), "omni_stage_after_pack");
     omni_ar_batch batch{};
     batch.n_entries = static_cast<int32_t>(n);
@@ -208,11 +233,23 @@ struct ArStage {
       batch.cond_src = cond_src.data();
       batch.cond_row = cond_row.data();
     }
-    dev_ok(omni_ar_step(st, &batch, tok_out.data(), margin_out.data()), "omni_ar_step");
     in_flight = true;
+    if (remote) {
+      if (talker)  // hidden-row addresses in the worker's mapping of its arena
+        for (auto& a : cond_src) a = own_arena->rebase(a);
+      static const std::vector<uint64_t> none;
+      reply.reset();
+      remote->ar_step(remote_id, reads_rows ? wait_events : none, batch, static_cast<int>(tokens.size()));
+      return;
+    }
+    dev_ok(omni_ar_step(st, &batch, tok_out.data(), margin_out.data()), "omni_ar_step");
   }
 
   bool ready() {
+    if (remote) {
+      if (!reply) reply = remote->poll(remote_id);
+      return reply.has_value();
+    }
     const omni_status s = omni_stage_query(st);
     if (s == OMNI_EAGAIN) return false;
     dev_ok(s, "omni_stage_query");
@@ -220,11 +257,20 @@ struct ArStage {
   }
 
   void collect(std::vector<BatchSlot>& slots, std::vector<int32_t>& out) {
-    dev_ok(omni_stage_wait(st), "omni_stage_wait");
+    float us = 0;
+    if (remote) {
+      if (!reply) reply = remote->wait(remote_id);
+      if (reply->status != OMNI_OK) throw DeviceError("remote omni_ar_step: " + reply->error);
+      std::copy(reply->tokens.begin(), reply->tokens.end(), tok_out.begin());
+      std::copy(reply->margins.begin(), reply->margins.end(), margin_out.begin());
+      us = reply->step_us;
+      reply.reset();
+    } else {
+      dev_ok(omni_stage_wait(st), "omni_stage_wait");
+      omni_stage_last_step_us(st, &us);
+    }
     ht.ready();
     in_flight = false;
-    float us = 0;
-    omni_stage_last_step_us(st, &us);
     dev_ms += us / 1e3;
     ++steps;
     for (size_t i = 0; i < slots.size(); ++i) {
@@ -284,6 +330,8 @@ struct ArStage {
     dev_ok(omni_pack_hidden(st, static_cast<int32_t>(packs.size()), sid.data(), b.data(), e.data(),
                             pack_tokens.data(), 0, off.data()),
            "omni_pack_hidden");
+    // consumers in worker processes wait on this interprocess event
+    if (pack_remote) dev_ok(omni_stage_record_pack(st, pack_event), "omni_stage_record_pack");
     packs.clear();
     pack_tokens.clear();
   }
@@ -304,8 +352,12 @@ struct DitStage {
   double dev_ms = 0;
   uint64_t steps = 0;
   HostTimer ht;
+  WorkerClient* remote = nullptr;
+  uint64_t remote_id = 0, remote_weight_bytes = 0;
+  std::optional<WorkerClient::StepReply> reply;
   ~DitStage() {
     if (st) omni_stage_destroy(st);
+    if (remote && remote_id) remote->destroy_stage(remote_id);
   }
   void launch(const std::vector<DiffusionJob>& jobs) {
     HostTimer::Scope hs(ht);
@@ -326,18 +378,36 @@ struct DitStage {
     b.token_offset = off.data();
     b.n_tokens = ntok.data();
     b.tokens = tokens.data();
+    if (remote) {
+      reply.reset();
+      remote->dit_step(remote_id, b);
+      return;
+    }
     dev_ok(omni_dit_step(st, &b, samples.data()), "omni_dit_step");
   }
   bool ready() {
+    if (remote) {
+      if (!reply) reply = remote->poll(remote_id);
+      return reply.has_value();
+    }
     const omni_status s = omni_stage_query(st);
     if (s == OMNI_EAGAIN) return false;
     dev_ok(s, "omni_stage_query");
     return true;
   }
   std::vector<Payload> collect() {
-    dev_ok(omni_stage_wait(st), "omni_stage_wait");
     float us = 0;
-    omni_stage_last_step_us(st, &us);
+    if (remote) {
+      if (!reply) reply = remote->wait(remote_id);
+      if (reply->status != OMNI_OK) throw DeviceError("remote omni_dit_step: " + reply->error);
+      if (reply->tokens.size() != samples.size()) throw ProtocolViolation("remote DiT returned a wrong sample count");
+      samples = std::move(reply->tokens);
+      us = reply->step_us;
+      reply.reset();
+    } else {
+      dev_ok(omni_stage_wait(st), "omni_stage_wait");
+      omni_stage_last_step_us(st, &us);
+    }
     ht.ready();
     dev_ms += us / 1e3;
     ++steps;
@@ -378,6 +448,9 @@ omni_model_desc model_for(int kind, bool small) {
 
 struct B200Pipeline::Impl {
   B200Options opt;
+  // declared first: destroyed last, after every stage / arena that uses them
+  std::map<std::string, std::unique_ptr<WorkerClient>> clients;  // by worker socket
+  std::vector<std::unique_ptr<Arena>> remote_arenas;             // exported by workers, mapped here
   std::map<uint64_t, std::vector<uint16_t>> captured;
   // keyed by registry name: the forward name for replica 0, "name#r" after
   std::map<std::string, std::unique_ptr<ArStage>> ar;
@@ -397,6 +470,13 @@ struct B200Pipeline::Impl {
     auto& a = arenas[dev];
     if (!a) a = std::make_unique<Arena>(dev, opt.arena_bytes);
     return *a;
+  }
+  WorkerClient* worker_for(const std::string& name) {
+    auto it = opt.workers.find(name);
+    if (it == opt.workers.end()) return nullptr;
+    auto& c = clients[it->second];
+    if (!c) c = std::make_unique<WorkerClient>(IpcChannel::connect(it->second, 60000));
+    return c.get();
   }
 
   std::vector<ArStage*> make_ar(const std::string& name, int kind, uint64_t seed_salt) {
@@ -425,7 +505,12 @@ struct B200Pipeline::Impl {
         lim.kv_pages = static_cast<int32_t>((tokens + 15) / 16 + ec.max_resident_requests);
       }
       // identical weights on every replica (same seed)
-      dev_ok(omni_stage_create(&s->model, &lim, s->dev, opt.weight_seed + seed_salt, &s->st), "omni_stage_create");
+      if ((s->remote = worker_for(name)))
+        s->remote_id = s->remote->create_stage(s->model, lim, s->dev, opt.weight_seed + seed_salt,
+                                               &s->remote_weight_bytes);
+      else
+        dev_ok(omni_stage_create(&s->model, &lim, s->dev, opt.weight_seed + seed_salt, &s->st),
+               "omni_stage_create");
       out.push_back(s.get());
       ar[replica_name(name, r)] = std::move(s);
     }
@@ -455,6 +540,9 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
                           " device(s) are visible");
   dev_ok(omni_init(static_cast<int32_t>(devs.size()), devs.data()), "omni_init");
   auto& I = *impl_;
+  if (I.opt.workers.count("thinker_forward"))
+    throw ConfigInvalid("the Thinker packs the connector and stays in the orchestrator process; "
+                        "place its consumers in workers instead");
   auto want = [&I](const std::string& n) { return I.opt.needed.empty() || I.opt.needed.count(n) != 0; };
   // weight seeds: thinker / ar share the thinker model family, talker and DiT own seeds
   std::vector<ArStage*> thinkers, talkers;
@@ -469,7 +557,26 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
   // connector arenas live on the consumer's GPU; with no talker in the graph
   // the thinker's chunks stay on its own GPU
   std::vector<Arena*> dst;
-  for (ArStage* t : talkers) dst.push_back(&I.arena_on(t->dev));
+  for (ArStage* t : talkers) {
+    if (t->remote) {  // the arena belongs to the worker; producers here map it (CUDA IPC)
+      I.remote_arenas.push_back(std::make_unique<Arena>(*t->remote, t->dev, I.opt.arena_bytes));
+      t->own_arena = I.remote_arenas.back().get();
+    } else {
+      t->own_arena = &I.arena_on(t->dev);
+    }
+    dst.push_back(t->own_arena);
+  }
+  // a worker's talker waits for the packs through one interprocess event per thinker
+  for (ArStage* th : thinkers) {
+    bool any = false;
+    for (ArStage* t : talkers) any = any || t->remote;
+    if (!any) continue;
+    omni_ipc_event_handle h{};
+    dev_ok(omni_ipc_event_create(th->dev, &th->pack_event, &h), "omni_ipc_event_create");
+    th->pack_remote = true;
+    for (ArStage* t : talkers)
+      if (t->remote) t->wait_events.push_back(t->remote->open_event(t->dev, h));
+  }
   for (ArStage* t : thinkers) t->dst_arenas = dst.empty() ? std::vector<Arena*>{&I.arena_on(t->dev)} : dst;
   if (want("ar_forward")) I.make_ar("ar_forward", OMNI_MODEL_THINKER, 0);
   for (const char* dn : {"denoise", "dit_image"}) {
@@ -484,9 +591,11 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
       omni_stage_limits lim{};
       lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
       lim.dit_max_tokens = 512;
-      dev_ok(omni_stage_create(&d->model, &lim, d->dev, I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3),
-                               &d->st),
-             "omni_stage_create(dit)");
+      const uint64_t seed = I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3);
+      if ((d->remote = I.worker_for(dn)))
+        d->remote_id = d->remote->create_stage(d->model, lim, d->dev, seed, &d->remote_weight_bytes);
+      else
+        dev_ok(omni_stage_create(&d->model, &lim, d->dev, seed, &d->st), "omni_stage_create(dit)");
       I.dit[replica_name(dn, r)] = std::move(d);
     }
   }
@@ -496,7 +605,10 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
   for (auto& [_, d] : I.dit) {
     bool shared = false;
     for (const auto& [__, a] : I.ar) shared = shared || a->dev == d->dev;
-    dev_ok(omni_stage_set_sm_share(d->st, shared ? kDitSharedSms : 0), "omni_stage_set_sm_share");
+    if (d->remote)
+      d->remote->set_sm_share(d->remote_id, shared ? kDitSharedSms : 0);
+    else
+      dev_ok(omni_stage_set_sm_share(d->st, shared ? kDitSharedSms : 0), "omni_stage_set_sm_share");
   }
 }
 
@@ -547,9 +659,11 @@ std::map<std::string, uint64_t> B200Pipeline::step_counts() const {
 uint64_t B200Pipeline::weight_bytes() const {
   uint64_t t = 0, b = 0;
   for (const auto& [_, s] : impl_->ar)
-    if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
+    if (s->remote) t += s->remote_weight_bytes;
+    else if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
   for (const auto& [_, s] : impl_->dit)
-    if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
+    if (s->remote) t += s->remote_weight_bytes;
+    else if (omni_stage_weight_bytes(s->st, &b) == OMNI_OK) t += b;
   return t;
 }
 void B200Pipeline::reset_counters() {
@@ -581,7 +695,7 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
     StageModel m;
     m.prefill = trace_prefill(s->name);
     m.on_prompt_consumed = trace_consumed(s->name, s->kind == OMNI_MODEL_TALKER);
-    m.reserve = [s](const BatchSlot& b) {
+    if (!s->remote) m.reserve = [s](const BatchSlot& b) {
       if (s->kind == OMNI_MODEL_THINKER && b.phase == Phase::PREFILL && b.seq) {
         // prompt ids of the span: the prefix cache maps cached pages first
         std::vector<int32_t> ids(b.seq->prompt.begin() + b.pos0, b.seq->prompt.begin() + b.pos0 + b.span);
@@ -596,7 +710,10 @@ void B200Pipeline::register_into(FunctionRegistry& reg) {
     m.launch_batch = [s](std::vector<BatchSlot>& slots) { s->launch(slots); };
     m.batch_ready = [s] { return s->ready(); };
     m.collect_batch = [s](std::vector<BatchSlot>& slots, std::vector<int32_t>& out) { s->collect(slots, out); };
-    m.release = [s](uint64_t rid) { dev_ok(omni_seq_release(s->st, rid), "omni_seq_release"); };
+    m.release = [s](uint64_t rid) {
+      if (s->remote) s->remote->release(s->remote_id, rid);
+      else dev_ok(omni_seq_release(s->st, rid), "omni_seq_release");
+    };
     m.flush = [s] { s->flush(); };
     m.cleanup = [s](uint64_t rid) {
       for (Arena* a : s->dst_arenas) a->release(rid);  // idempotent; arenas may be shared

@@ -11,6 +11,7 @@
 #include "omni/bench.hpp"
 #include "omni/config.hpp"
 #include "omni/http_service.hpp"
+#include "omni/stage_worker.hpp"
 #include "omni_serve.h"
 
 namespace {
@@ -85,11 +86,17 @@ omni_status omni_pipeline_create(const char* config_json, const omni_pipeline_op
       o.small_models = opts->small_models != 0;
     }
     const int dev = opts ? opts->device : 0;
+    for (const auto& [id, _] : p->plan.workers) {
+      bool known = false;
+      for (const auto& n : p->plan.graph.nodes) known = known || n.id == id;
+      if (!known) throw omni::ConfigInvalid("workers names unknown stage '" + id + "'");
+    }
     for (const auto& n : p->plan.graph.nodes) {
       const std::string fn = n.kind == omni::StageKind::AR ? n.forward_ref
                                                            : (n.forward_ref.empty() ? "denoise" : n.forward_ref);
       // the plan's placement (stage -> "cuda:N[,cuda:M...]"), else opts->device
       o.devices[fn] = omni::placement_devices(p->plan, n.id, dev);
+      if (auto w = p->plan.workers.find(n.id); w != p->plan.workers.end()) o.workers[fn] = w->second;
       o.engines[fn] = p->plan.engines.at(n.id);
       o.needed.insert(fn);
     }
@@ -119,6 +126,13 @@ omni_status omni_pipeline_serve_stop(omni_pipeline* p) {
     if (p->orch) p->orch->shutdown(true);
     p->http.reset();
     p->orch.reset();
+  });
+}
+
+omni_status omni_worker_serve(const char* socket_path, int32_t accept_timeout_ms) {
+  return guard([&] {
+    omni::IpcChannel ch = omni::IpcChannel::listen_accept(socket_path, static_cast<uint64_t>(accept_timeout_ms));
+    omni::run_stage_worker(ch);
   });
 }
 

@@ -33,6 +33,9 @@ struct B200Options {
   uint64_t arena_bytes = 256ull << 20;     // hidden-state connector arena per producer
   std::map<std::string, EngineConfig> engines;  // stage limits keyed by forward name
   std::set<std::string> needed;                 // forward / denoiser names to build (empty = all)
+  // forward / denoiser name -> AF_UNIX socket of the stage worker process that
+  // hosts its stages (stage_worker.hpp); absent = this process
+  std::map<std::string, std::string> workers;
 };
 
 class B200Pipeline {

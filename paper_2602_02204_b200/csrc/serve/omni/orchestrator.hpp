@@ -47,6 +47,9 @@ struct DeploymentPlan {
   // reads it (orchestrator.hpp:37); here R devices = R engine replicas of the
   // stage, requests routed by replica_for(rid, R).
   std::map<StageId, std::string> placement;
+  // B200 multi-process placement: stage -> AF_UNIX socket of the stage worker
+  // process (omni_worker_serve) that hosts its device stages
+  std::map<StageId, std::string> workers;
   std::string clock_kind = "virtual";                 // virtual | wall | device
   ServerOptions server;
   std::string server_id = "0";
