@@ -21,6 +21,12 @@ one process drives all N GPUs: launched plainly (`python bench.py --gpus N`)
 it is that process; under torchrun rank 0 is, and ranks 1..N-1 only join the
 barriers (gloo) and report zero device time, so max over ranks = rank 0's.
 
+--procs (under torchrun): one process per GPU -- rank r >= 1 is a stage
+worker (omni_worker_serve) hosting the stages placed on cuda:r, rank 0 the
+control plane + the Thinker; steps cross processes as control-frame requests,
+hidden rows as CUDA-IPC packs. Off by default: the single
+driving process avoids a request round trip per step.
+
 --impl reference: the reference's own control plane (compiled from its
 headers, oracle/_ref/ref_cpu_pipeline) with CPU fp32 model hooks on the host
 cores, over a bounded sample of the same workload; rank 0 only.
@@ -281,6 +287,8 @@ def main() -> None:
     ap.add_argument("--small", action="store_true", help="reduced model dims (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--placement", default="", help='JSON stage->devices override, e.g. \'{"talker": "cuda:1,cuda:2"}\'')
+    ap.add_argument("--procs", action="store_true",
+                    help="under torchrun: ranks >= 1 are stage worker processes for their GPU")
     ap.add_argument("--fold-devices", action="store_true",
                     help="debug: map cuda:i -> cuda:(i mod visible) to exercise the N-GPU code path on fewer "
                          "GPUs (the line is marked folded and is not an N-GPU measurement)")
@@ -295,12 +303,22 @@ def main() -> None:
             dist.destroy_process_group()
         return
 
+    sock = lambda r: f"/tmp/omni_bench_{os.environ.get('MASTER_PORT', '0')}_w{r}.sock"
     if rank != 0:
         # rank 0 drives the whole stage graph over all N GPUs; this rank only
-        # brackets the timed region and reports zero device time
+        # brackets the timed region and reports zero device time -- or, with
+        # --procs, serves the stages placed on its GPU meanwhile
+        worker = None
+        if args.procs:
+            from paper_2602_02204_b200 import serve_lib
+            lib = serve_lib()
+            worker = threading.Thread(target=lambda: lib.omni_worker_serve(sock(rank).encode(), 600000), daemon=True)
+            worker.start()
         dist.barrier()
         dist.barrier()
         aggregate(0, 0.0, 0.0, dist)
+        if worker is not None:
+            worker.join(timeout=600)
         dist.destroy_process_group()
         return
 
@@ -316,12 +334,24 @@ def main() -> None:
     placement = placement_for(n_gpus)
     if args.placement:
         placement.update(json.loads(args.placement))
+    workers = {}
+    if args.procs and world > 1:
+        # stage -> worker of the rank its GPU belongs to (the Thinker packs: stays here)
+        for k, v in placement.items():
+            ranks = {int(d.split(":")[1]) for d in v.split(",")}
+            if k != "thinker" and len(ranks) == 1 and min(ranks) != 0:
+                workers[k] = sock(min(ranks))
+            elif k != "thinker" and not args.fold_devices:
+                for r in ranks - {0}:
+                    workers[f"cuda:{r}"] = sock(r)
     if args.fold_devices:
         placement = {k: ",".join(f"cuda:{int(d.split(':')[1]) % visible}" for d in v.split(","))
                      for k, v in placement.items()}
     gpus_used = sorted({int(d.split(":")[1]) for v in placement.values() for d in v.split(",")})
     cfg = json.loads(CONFIG.read_text())
     cfg["placement"] = placement
+    if workers:
+        cfg["workers"] = workers
     n_req = args.n * n_gpus
     conc = args.concurrency * n_gpus
     pipe = Pipeline(json.dumps(cfg), weight_seed=1234, small_models=args.small, device=0)
@@ -350,6 +380,8 @@ def main() -> None:
         wall = time.perf_counter() - t0
     if dist is not None:
         dist.barrier()
+    if workers:
+        pipe.close()  # shuts the stage workers down (their ranks are waiting for them)
     l1, h1, d1 = C.c_uint64(), C.c_uint64(), C.c_uint64()
     lib.omni_dev_counters(C.byref(l1), C.byref(h1), C.byref(d1))
     gc1, gr1 = C.c_uint64(), C.c_uint64()
@@ -409,7 +441,8 @@ def main() -> None:
                       if args.fold_devices else {}),
                    "models": "thinker 8L d2048 (16q/4kv heads, ffn 8192, V256); talker 4L d2048 (V64); "
                              "code2wav DiT 4L d1024 T4 S16",
-                   "parallelism": "stage-per-GPU " + " ".join(f"{k}x{len(v.split(','))}" for k, v in placement.items())
+                   "parallelism": ("stage-per-GPU " + " ".join(f"{k}x{len(v.split(','))}" for k, v in placement.items())
+                                   + (" (one process per GPU: stage workers)" if workers else ""))
                                   if n_gpus > 1 else "all stages on cuda:0",
                    "l2": "weights 1.4 GB per AR step set >> 126 MB L2 (no flush needed)"},
         "mean_jct_us": round(mean_jct, 1),

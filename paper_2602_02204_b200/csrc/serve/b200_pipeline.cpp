@@ -471,8 +471,11 @@ struct B200Pipeline::Impl {
     if (!a) a = std::make_unique<Arena>(dev, opt.arena_bytes);
     return *a;
   }
-  WorkerClient* worker_for(const std::string& name) {
+  // the worker hosting stage `name`'s replica on `dev`: by stage, else by
+  // device ("cuda:N" keys) -- the Thinker always stays here (it packs)
+  WorkerClient* worker_for(const std::string& name, int dev) {
     auto it = opt.workers.find(name);
+    if (it == opt.workers.end() && name != "thinker_forward") it = opt.workers.find("cuda:" + std::to_string(dev));
     if (it == opt.workers.end()) return nullptr;
     auto& c = clients[it->second];
     if (!c) c = std::make_unique<WorkerClient>(IpcChannel::connect(it->second, 60000));
@@ -505,7 +508,7 @@ struct B200Pipeline::Impl {
         lim.kv_pages = static_cast<int32_t>((tokens + 15) / 16 + ec.max_resident_requests);
       }
       // identical weights on every replica (same seed)
-      if ((s->remote = worker_for(name)))
+      if ((s->remote = worker_for(name, s->dev)))
         s->remote_id = s->remote->create_stage(s->model, lim, s->dev, opt.weight_seed + seed_salt,
                                                &s->remote_weight_bytes);
       else
@@ -592,7 +595,7 @@ B200Pipeline::B200Pipeline(B200Options opt) : impl_(std::make_unique<Impl>()) {
       lim.max_resident = static_cast<int32_t>(ec.max_resident_requests);
       lim.dit_max_tokens = 512;
       const uint64_t seed = I.opt.weight_seed + (std::string(dn) == "denoise" ? 2 : 3);
-      if ((d->remote = I.worker_for(dn)))
+      if ((d->remote = I.worker_for(dn, d->dev)))
         d->remote_id = d->remote->create_stage(d->model, lim, d->dev, seed, &d->remote_weight_bytes);
       else
         dev_ok(omni_stage_create(&d->model, &lim, d->dev, seed, &d->st), "omni_stage_create(dit)");

@@ -86,7 +86,11 @@ omni_status omni_pipeline_create(const char* config_json, const omni_pipeline_op
       o.small_models = opts->small_models != 0;
     }
     const int dev = opts ? opts->device : 0;
-    for (const auto& [id, _] : p->plan.workers) {
+    for (const auto& [id, w] : p->plan.workers) {
+      if (id.rfind("cuda:", 0) == 0) {  // device-keyed: every stage replica there but the Thinker
+        o.workers[id] = w;
+        continue;
+      }
       bool known = false;
       for (const auto& n : p->plan.graph.nodes) known = known || n.id == id;
       if (!known) throw omni::ConfigInvalid("workers names unknown stage '" + id + "'");
