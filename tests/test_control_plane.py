@@ -25,9 +25,8 @@ MOCK = ROOT / "oracle" / "_build" / "liboracle_mock.so"
 
 @pytest.fixture(scope="module")
 def mock():
-    if not MOCK.exists():
-        import subprocess
-        subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "_build/liboracle_mock.so"], check=True)
+    import subprocess  # make: rebuilds when libomni_serve.so or its headers changed
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle"), "_build/liboracle_mock.so"], check=True)
     lib = C.CDLL(str(MOCK))
     lib.oracle_mock_trace.restype = C.c_long
     lib.oracle_mock_trace.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int,
