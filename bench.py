@@ -282,7 +282,7 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=100)
+    ap.add_argument("--n", "--requests", dest="n", type=int, default=100)  # --requests: torchrun-safe spelling
     ap.add_argument("--concurrency", type=int, default=16)
     ap.add_argument("--small", action="store_true", help="reduced model dims (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -59,3 +59,23 @@ def test_thinker_in_a_worker_is_rejected():
     with pytest.raises(OmniError) as e:
         Pipeline(json.dumps(dict(CFG, workers={"thinker": "/tmp/none.sock"})), weight_seed=1, small_models=True)
     assert "Thinker" in str(e.value)
+
+
+@pytest.mark.parametrize("procs", [False, True])
+def test_bench_two_ranks_under_torchrun(procs):
+    """bench.py --gpus 2 under torchrun on this box (the 2-GPU placement folded
+    onto its GPU): rank 0 drives the stage graph; with --procs rank 1 is the
+    stage worker hosting the Talker. One JSON line, every request completed."""
+    port = 29600 + (1 if procs else 0) + os.getpid() % 200
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", "2",
+           "--fold-devices", "--small", "--requests", "12", "--steps", "1", "--warmup", "1", "--no-cpu-baseline"]
+    if procs:
+        cmd.append("--procs")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(line) == 1, r.stdout[-2000:]
+    d = json.loads(line[0])
+    assert d["n_gpus"] == 2 and d["completed"] == 24
+    assert ("stage workers" in d["config"]["parallelism"]) == procs
