@@ -561,10 +561,13 @@ struct ArDescLayout {
 ArDescLayout ar_desc_layout(const omni_stage* st) {
   const size_t cap_e = (size_t)st->lim.max_resident, cap_r = (size_t)st->rows_cap;
   ArDescLayout l;
+  // the attention blocks come last: a step graph (keyed by n_blocks) copies
+  // only [0, off_blk + n_blocks) -- the block region is sized for split-KV
+  // worst cases (kAttnMaxParts per block) that ordinary steps never use
   l.off_dec = align16(cap_e * sizeof(ArEntryDesc));
-  l.off_blk = l.off_dec + align16(cap_e * sizeof(int32_t));
-  l.off_rows = l.off_blk + align16((cap_r + cap_e) * kAttnMaxParts * sizeof(AttnBlockDesc));
-  l.off_delta = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
+  l.off_rows = l.off_dec + align16(cap_e * sizeof(int32_t));
+  l.off_blk = l.off_rows + align16(cap_r * sizeof(ArRowDesc));
+  l.off_delta = l.off_blk + align16((cap_r + cap_e) * kAttnMaxParts * sizeof(AttnBlockDesc));
   l.cap_delta = kPageDeltaCap;
   l.reserve = l.off_delta + sizeof(PageDeltaHeader) + l.cap_delta * sizeof(PageDelta);
   return l;
@@ -601,7 +604,8 @@ void launch_ar_kernels(omni_stage* st, const ArStepDev& sd, int n_rows, int n_bl
   cudaStream_t s = st->stream;
   {
     const ArDescLayout lay = ar_desc_layout(st);
-    OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, lay.off_delta, st->desc.host + lay.off_delta,
+    OMNI_KERNEL(launch_desc_copy(st->desc.dev, st->desc.host, align16(lay.off_blk + (size_t)n_blocks * sizeof(AttnBlockDesc)),
+                                 st->desc.host + lay.off_delta,
                                  st->page_table, s));
   }
   int trace_slot = 0;  // OMNI_STEP_TRACE: one slot per GEMM launch, in launch order
@@ -812,7 +816,8 @@ void ar_step(omni_stage* st, const omni_ar_batch* b, int32_t* tok_out, float* ma
   const int n_dec = (int)dec_list.size();
   cudaStream_t s = st->stream;
   OMNI_CUDA(cudaEventRecord(st->ev_start, s));
-  counters().h2d_bytes += lay.off_delta + sizeof(PageDeltaHeader) + dh->n * sizeof(PageDelta);
+  counters().h2d_bytes += align16(lay.off_blk + (size_t)n_blocks * sizeof(AttnBlockDesc)) + sizeof(PageDeltaHeader) +
+                          dh->n * sizeof(PageDelta);
   const ArStepDev sd = ar_step_dev(st, lay);
   if (n_rows > 0) {
     const uint64_t key = ar_graph_key(n_rows, n_blocks, n_dec, talker && n_prefill_rows > 0);
