@@ -50,11 +50,9 @@ def _compile(src: Path, obj: Path, headers: list[Path], extra: list[str]) -> Pat
     inc = ["-I", str(ROOT / "include"), "-I", str(CSRC / "dev"), "-I", str(CSRC / "serve"),
            "-I", JSON_INC]
     if src.suffix == ".cu":
-        # OMNI_NVCC_DEFS: extra -D definitions for A/B builds (tools/, never the default build)
-        defs = os.environ.get("OMNI_NVCC_DEFS", "").split()
         cmd = [NVCC, *ARCH, "-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if os.environ.get("OMNI_PTXAS_V") else "-O3",
-               "--expt-relaxed-constexpr", *inc, *defs, *extra, "-c", str(src), "-o", str(obj)]
+               "--expt-relaxed-constexpr", *inc, *extra, "-c", str(src), "-o", str(obj)]
     else:
         cmd = [CXX, "-std=c++20", "-O2", "-g", "-fPIC", "-Wall", "-Wno-unused-function",
                "-I", f"{CUDA_HOME}/include", *inc, *extra, "-c", str(src), "-o", str(obj)]

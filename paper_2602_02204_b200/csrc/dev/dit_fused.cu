@@ -57,31 +57,25 @@
 namespace omni_dev {
 namespace {
 
-#ifndef OMNI_DIT_EPI_WARPS
-#define OMNI_DIT_EPI_WARPS 8
-#endif
-constexpr int kEpiWarps = OMNI_DIT_EPI_WARPS;  // kSub warps per TMEM lane quadrant, each 1/kSub of an item's chunks
-constexpr int kSub = kEpiWarps / 4;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, each half of an item's 16-row chunks
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kThreadsF = 64 + kEpiThreads;
 constexpr int kQ = 1;  // item ring depth: fetch item i+1 once item i started (deeper run-ahead
                        // strands short LN / attention items behind long GEMM items of the same CTA)
 constexpr int kABytes = kDitFeat * 64 * 2;  // weight tile (128 features x 64 k)
-static_assert(16 % kEpiWarps == 0 && kEpiWarps % 4 == 0, "LN rows per warp / quadrant warps");
+static_assert(16 % kEpiWarps == 0, "LN rows per warp");
 
 // Row-tile geometry: TR rows = TR / 16 tokens = MMA N (128 or 256).
 template <int TR>
 struct Tile {
   static constexpr int rows = TR, tok = TR / 16;
   static constexpr int chunks = TR / 16;                  // 16-row chunks (one token each) per item
-  static constexpr int my_chunks = chunks / kSub;            // chunks per epilogue warp
+  static constexpr int my_chunks = chunks / (kEpiWarps / 4);  // chunks per epilogue warp
   static constexpr int b_bytes = TR * 64 * 2;             // row tile (TR rows x 64 k)
   static constexpr int stage_bytes = kABytes + b_bytes;
-  // attention item = a warp per (token, head): att_tok tokens x att_heads heads
-  static constexpr int att_tok = tok < kEpiWarps ? tok : kEpiWarps;
-  static constexpr int att_heads = kEpiWarps / att_tok;
+  static constexpr int att_groups = tok / kEpiWarps;      // attention items per head (a warp per token)
   static constexpr uint32_t idesc = idesc_bf16_f32(kDitFeat, TR);
-  static_assert(tok % att_tok == 0 && chunks % kSub == 0, "attention groups / chunk split");
+  static_assert(tok % kEpiWarps == 0 && chunks % 2 == 0, "attention groups / chunk halves");
 };
 
 enum Kind : int { K_IN = 0, K_LN1, K_QKV, K_ATT, K_O, K_LN2, K_UP, K_DOWN, K_LNF, K_OUT, K_END };
@@ -99,29 +93,22 @@ struct PhaseInfo {
 };
 
 // Phase ph of one Euler step (P = 3 + 7 L phases); items / units per row tile.
-// A unit is one CTA's share: a 128-feature block, a token (LN), an attention
-// group. With CTA pairs (PAIR) an item is two units, one per CTA of the pair
-// (OUT: both CTAs count one, the second one's features are padding).
-template <int TR, bool PAIR = false>
+template <int TR>
 __device__ __forceinline__ PhaseInfo phase_info(const DitFusedParams& p, int ph) {
   using T = Tile<TR>;
-  constexpr int f = PAIR ? 2 : 1;
   const int nf = p.d / kDitFeat, P = 3 + 7 * p.L;
-  if (ph == 0) return {K_IN, 0, nf / f, nf};
-  if (ph == P - 2) return {K_LNF, 0, T::tok / f, T::tok};
-  if (ph == P - 1) return {K_OUT, 0, 1, f};
+  if (ph == 0) return {K_IN, 0, nf, nf};
+  if (ph == P - 2) return {K_LNF, 0, T::tok, T::tok};
+  if (ph == P - 1) return {K_OUT, 0, 1, 1};
   const int l = (ph - 1) / 7;
   switch ((ph - 1) % 7) {
-    case 0: return {K_LN1, l, T::tok / f, T::tok};
-    case 1: return {K_QKV, l, 3 * nf / f, 3 * nf};
-    case 2: {  // (head group, token group)
-      const int n = p.H * T::tok / kEpiWarps;
-      return {K_ATT, l, n / f, n};
-    }
-    case 3: return {K_O, l, nf / f, nf};
-    case 4: return {K_LN2, l, T::tok / f, T::tok};
-    case 5: return {K_UP, l, p.ff / kDitFeat / f, p.ff / kDitFeat};
-    default: return {K_DOWN, l, nf * p.down_split / f, nf};
+    case 0: return {K_LN1, l, T::tok, T::tok};
+    case 1: return {K_QKV, l, 3 * nf, 3 * nf};
+    case 2: return {K_ATT, l, p.H * T::att_groups, p.H * T::att_groups};  // (head, 8-token group)
+    case 3: return {K_O, l, nf, nf};
+    case 4: return {K_LN2, l, T::tok, T::tok};
+    case 5: return {K_UP, l, p.ff / kDitFeat, p.ff / kDitFeat};
+    default: return {K_DOWN, l, nf * p.down_split, nf};
   }
 }
 
@@ -178,16 +165,15 @@ __device__ __forceinline__ void ln_rows(const float* hr, bool mod, const float4 
                                          __nv_bfloat16* out_row, int lane) {
   constexpr int d = PER * 128;
 #pragma unroll 1
-  constexpr int QN = NR >= 2 ? 2 : 1;
-  for (int q0 = 0; q0 < NR; q0 += QN) {
-    float4 x[QN][PER];
+  for (int q0 = 0; q0 < NR; q0 += 2) {
+    float4 x[2][PER];
 #pragma unroll
-    for (int q = 0; q < QN; ++q)
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
       for (int k = 0; k < PER; ++k)
         x[q][k] = __ldcg(reinterpret_cast<const float4*>(hr + (size_t)(q0 + q) * d) + lane + 32 * k);
 #pragma unroll
-    for (int q = 0; q < QN; ++q) {
+    for (int q = 0; q < 2; ++q) {
       float sum = 0.f;
 #pragma unroll
       for (int k = 0; k < PER; ++k) sum += (x[q][k].x + x[q][k].y) + (x[q][k].z + x[q][k].w);
@@ -349,13 +335,13 @@ __device__ __forceinline__ void attn_token_head(const __nv_bfloat16* qkv, int to
 // token c (rotated one per chunk).
 template <int TR, int KIND, int MODE>
 __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta, int row0, int ft, const float* s1b,
-                                           const float* s2b, float* dstb, int quad, int sub, int lane,
+                                           const float* s2b, float* dstb, int quad, int half, int lane,
                                            float (&aux)[16], int step) {
   constexpr bool kGated = KIND == K_O || KIND == K_DOWN;
   const int g4 = lane >> 2, t4 = lane & 3;
   const int fw = ft * kDitFeat + quad * 32 + 4 * g4;  // first of my 4 features after the transpose
   const int d = p.d;
-  if (KIND == K_OUT && ft * kDitFeat + quad * 32 >= p.C) return;  // OUT: the C channels are the first C features
+  if (KIND == K_OUT && quad * 32 >= p.C) return;  // OUT: the C channels are the first C lanes
   constexpr int kChunks = Tile<TR>::chunks, kMyChunks = Tile<TR>::my_chunks;
   const int off4 = quad * 32 + 4 * g4;  // my 4 features within the 128-feature partial tile
   const float* s1 = s1b + off4;
@@ -377,24 +363,24 @@ __device__ __forceinline__ void epi_chunks(const DitFusedParams& p, uint32_t ta,
       for (int m = 0; m < 4; ++m)
         dst2[m] = __ldcg(reinterpret_cast<const float4*>(s2 + (size_t)(cc * 16 + 4 * m + t4) * kDitFeat));
   };
-  // this warp's chunks: c = sub, sub + kSub, ... (its quadrant partners take the
+  // this warp's chunks: c = half, half + 2, ... (its quadrant partner takes the
   // others); the next chunk's TMEM load and side inputs are in flight while
   // this one is processed
   float4 nx[4] = {}, nx2[4] = {};
-  load_side(sub, nx, nx2);
+  load_side(half, nx, nx2);
   uint32_t tr[16];
-  tmem_ld16_issue(ta + sub * 16, tr);
+  tmem_ld16_issue(ta + half * 16, tr);
 #pragma unroll 1
-  for (int c = sub; c < kChunks; c += kSub) {
+  for (int c = half; c < kChunks; c += 2) {
     float4 ld[4], ld2[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) ld[m] = nx[m], ld2[m] = nx2[m];
-    if (c + kSub < kChunks) load_side(c + kSub, nx, nx2);
+    if (c + 2 < kChunks) load_side(c + 2, nx, nx2);
     tmem_ld16_wait(tr);
     float v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(tr[i]);
-    if (c + kSub < kChunks) tmem_ld16_issue(ta + (c + kSub) * 16, tr);
+    if (c + 2 < kChunks) tmem_ld16_issue(ta + (c + 2) * 16, tr);
     const int rb = row0 + c * 16;  // rows of token row0 / 16 + c
     if constexpr (KIND == K_IN) {
 #pragma unroll
@@ -464,27 +450,12 @@ struct Smem {
   int unit_cum[kDitMaxPhases + 1];    // per-tile units completed before tp
 };
 
-// Activation (MMA B) map with `rows`-row boxes.
-__device__ __forceinline__ int x_map_index(int rows) { return rows == 256 ? 1 : rows == 128 ? 0 : 2; }
-
-// PAIR: the persistent grid is made of 2-CTA clusters; a GEMM item is 256
-// output features x TR rows, one tcgen05.mma.cta_group::2 per k-step issued
-// by the leader (rank 0). Each CTA streams its own 128 weight rows and HALF
-// of the row tile (TR / 2 rows), so a CTA moves 128 + TR / 2 instead of
-// 128 + TR rows of operands per 128 x TR outputs: the mainloop was bound by
-// per-SM L2 -> shared-memory ingress (~125 GB/s per SM against a ~4.3 us MMA
-// time for a 128 x 256 x 1024 item, profiles/r02_dit_fused_pair.txt). The
-// leader's scheduler hands every item to both CTAs (its ring + the peer's
-// over DSMEM); each CTA's epilogue drains its own TMEM half (its 128
-// features), LN / attention items split into one unit per CTA.
-template <int PER, int STAGES, int TR, bool PAIR>
+template <int PER, int STAGES, int TR>
 __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_constant__ DitFusedParams p) {
   static_assert(STAGES <= 8, "barrier slots");
   using Tl = Tile<TR>;
-  constexpr int kBRows = PAIR ? TR / 2 : TR;  // row-tile rows this CTA loads (MMA B)
-  constexpr int kBBytes = kBRows * 64 * 2, kStageBytes = kABytes + kBBytes;
-  constexpr uint32_t kIdesc = idesc_bf16_f32(PAIR ? 2 * kDitFeat : kDitFeat, TR);
-  constexpr int kF = PAIR ? 2 : 1;  // feature blocks per GEMM item
+  constexpr int kBBytes = Tl::b_bytes, kStageBytes = Tl::stage_bytes;
+  constexpr uint32_t kIdesc = Tl::idesc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = base;
@@ -493,19 +464,14 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
   const int warp = warp_id(), lane = lane_id();
   const int P = 3 + 7 * p.L, TP = p.T * P;
   const int nf = p.d / kDitFeat;
-  const uint32_t rank = PAIR ? cluster_rank() : 0;
-  const bool leader = rank == 0;
-  unsigned long long* const trace = leader ? p.trace : nullptr;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&sm.full[s], 1), mbar_init(&sm.empty[s], 1);
-    for (int a = 0; a < 2; ++a) mbar_init(&sm.acc_full[a], 1), mbar_init(&sm.acc_empty[a], kF * kEpiWarps);
-    // consumers of a ring slot: the MMA warp + the epilogue warps (+ the
-    // peer's producer and epilogue warps, which arrive remotely)
-    for (int q = 0; q < kQ; ++q) mbar_init(&sm.q_full[q], 1), mbar_init(&sm.q_empty[q], kF * (1 + kEpiWarps));
+    for (int a = 0; a < 2; ++a) mbar_init(&sm.acc_full[a], 1), mbar_init(&sm.acc_empty[a], kEpiWarps);
+    for (int q = 0; q < kQ; ++q) mbar_init(&sm.q_full[q], 1), mbar_init(&sm.q_empty[q], 1 + kEpiWarps);
     int items = 0, units = 0;
     for (int tp = 0; tp < TP; ++tp) {
-      const PhaseInfo ph = phase_info<TR, PAIR>(p, tp % P);
+      const PhaseInfo ph = phase_info<TR>(p, tp % P);
       sm.item_start[tp] = items;
       sm.unit_cum[tp] = units;
       items += ph.items * p.n_rt;
@@ -515,126 +481,98 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
     sm.unit_cum[TP] = units;
     fence_barrier_init();
   }
-  if (warp == 1) {
-    if constexpr (PAIR) tmem_alloc2<512>(&sm.tmem);
-    else tmem_alloc<512>(&sm.tmem);
-  }
+  if (warp == 1) tmem_alloc<512>(&sm.tmem);
   tc_fence_before();
-  if constexpr (PAIR) cluster_sync();  // the peer's barriers are initialised before any remote arrive
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = sm.tmem;
   pdl_wait();  // descriptors / noise / counters of this iteration are written by the predecessors
 
-  // GEMM geometry of an item for this CTA: its 128-feature block and K range
-  auto feat_block = [&](const Item& it) {
-    const int b = it.kind == K_DOWN ? it.j / p.down_split : it.kind == K_OUT ? 0 : it.j;
-    return kF * b + (int)rank;
-  };
-  auto n_kblocks = [&](int kind) {
-    return kind == K_IN ? p.C / 64 : kind == K_DOWN ? p.ff / 64 / p.down_split : p.d / 64;
-  };
-
   if (warp == 0) {
-    // ---------------- scheduler (leader) + TMA producer (both CTAs) ----------------
+    // ---------------- scheduler + TMA producer ----------------
     if (lane == 0) {
       const DitMaps* mp = p.maps;
-      constexpr int ti = TR == 256 ? (PAIR ? 0 : 1) : (PAIR ? 2 : 0);  // maps with kBRows-row boxes
-      static_assert(kBRows == 64 || kBRows == 128 || kBRows == 256, "B box");
+      constexpr int ti = TR == 256 ? 1 : 0;  // activation maps with TR-row boxes
       const uint64_t pol = policy_evict_last();  // weights re-read by every row tile; activations hot
       int tp = 0;
       uint32_t qi = 0, kbi = 0;
       const int total = sm.item_start[TP];
       for (;;) {
+        const int idx = atomicAdd(p.next_item, 1);
         const int slot = qi % kQ;
+        mbar_wait_sleep(&sm.q_empty[slot], ((qi / kQ) & 1) ^ 1);
         Item it;
-        if (leader) {
-          const int idx = atomicAdd(p.next_item, 1);
-          mbar_wait_sleep(&sm.q_empty[slot], ((qi / kQ) & 1) ^ 1);
-          it.kind = K_END;
-          if (idx < total) {
-            while (idx >= sm.item_start[tp + 1]) ++tp;
-            const PhaseInfo ph = phase_info<TR, PAIR>(p, tp % P);
-            const int local = idx - sm.item_start[tp];
-            it.kind = ph.kind;
-            it.layer = ph.layer;
-            it.step = tp / P;
-            it.tp = tp;
-            it.r = local / ph.items;
-            it.j = local % ph.items;
-            it.idx = idx;
-            if (trace) {
-              unsigned int smid;
-              asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-              trace[(size_t)idx * 8 + 0] = globaltimer();
-              trace[(size_t)idx * 8 + 4] = smid;
-            }
+        it.kind = K_END;
+        if (idx < total) {
+          while (idx >= sm.item_start[tp + 1]) ++tp;
+          const PhaseInfo ph = phase_info<TR>(p, tp % P);
+          const int local = idx - sm.item_start[tp];
+          it.kind = ph.kind;
+          it.layer = ph.layer;
+          it.step = tp / P;
+          it.tp = tp;
+          it.r = local / ph.items;
+          it.j = local % ph.items;
+          it.idx = idx;
+          if (p.trace) {
+            unsigned int smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            p.trace[(size_t)idx * 8 + 0] = globaltimer();
+            p.trace[(size_t)idx * 8 + 4] = smid;
           }
-          sm.ring[slot] = it;
-          if constexpr (PAIR) {  // the same item to the peer: its ring copy, then its q_full
-            const uint32_t dst = dsmem_map(smem_addr(&sm.ring[slot]), 1);
-            const int* w = reinterpret_cast<const int*>(&it);
-#pragma unroll
-            for (int i = 0; i < (int)(sizeof(Item) / 4); ++i) st_cluster_u32(dst + 4 * i, (uint32_t)w[i]);
-            mbar_arrive_cluster(dsmem_map(smem_addr(&sm.q_full[slot]), 1));
-          }
-          mbar_arrive(&sm.q_full[slot]);
-        } else {
-          mbar_wait_sleep_cluster(&sm.q_full[slot], (qi / kQ) & 1);
-          it = sm.ring[slot];
-          mbar_arrive_cluster(dsmem_map(smem_addr(&sm.q_empty[slot]), 0));
         }
+        sm.ring[slot] = it;
+        mbar_arrive(&sm.q_full[slot]);
         ++qi;
         if (it.kind == K_END) break;
         if (!is_gemm(it.kind)) continue;
         const CUtensorMap* wm;
         const CUtensorMap* xm;
-        const int nkb = n_kblocks(it.kind);
-        const int kb0 = it.kind == K_DOWN ? (it.j % p.down_split) * nkb : 0;
-        const int wrow = feat_block(it) * kDitFeat;
+        int nkb, kb0 = 0, wrow = it.j * kDitFeat;
         switch (it.kind) {
-          case K_IN: wm = &mp->w_in; xm = &mp->x_x[ti]; break;
-          case K_QKV: wm = &mp->wqkv[it.layer]; xm = &mp->x_a[ti]; break;
-          case K_O: wm = &mp->wo[it.layer]; xm = &mp->x_o[ti]; break;
-          case K_UP: wm = &mp->w1[it.layer]; xm = &mp->x_a[ti]; break;
-          case K_DOWN: wm = &mp->w2[it.layer]; xm = &mp->x_u[ti]; break;
-          default: wm = &mp->w_out; xm = &mp->x_a[ti]; break;  // OUT: rows >= 128 of w_out are OOB -> zeros
+          case K_IN: wm = &mp->w_in; xm = &mp->x_x[ti]; nkb = p.C / 64; break;
+          case K_QKV: wm = &mp->wqkv[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
+          case K_O: wm = &mp->wo[it.layer]; xm = &mp->x_o[ti]; nkb = p.d / 64; break;
+          case K_UP: wm = &mp->w1[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
+          case K_DOWN:
+            wm = &mp->w2[it.layer];
+            xm = &mp->x_u[ti];
+            nkb = p.ff / 64 / p.down_split;
+            kb0 = (it.j % p.down_split) * nkb;
+            wrow = (it.j / p.down_split) * kDitFeat;
+            break;
+          default: wm = &mp->w_out; xm = &mp->x_a[ti]; nkb = p.d / 64; wrow = 0; break;
         }
-        const int xrow = it.r * TR + (int)rank * kBRows;
-        // stage s completes on the leader's full[s]: the leader arms it with both CTAs' bytes
-        auto load = [&](int s, void* dst, const CUtensorMap* m, int x, int y) {
-          if constexpr (PAIR) tma_load_2d_pair(dst, m, dsmem_map(smem_addr(&sm.full[s]), 0), x, y, pol);
-          else tma_load_2d(dst, m, &sm.full[s], x, y, pol);
-        };
+        const int xrow = it.r * TR;
         const int pre = nkb < STAGES ? nkb : STAGES;
         for (int i = 0; i < pre; ++i) {  // weights first: they never depend on another item
           const uint32_t k = kbi + i;
           const int s = k % STAGES;
           mbar_wait_sleep(&sm.empty[s], ((k / STAGES) & 1) ^ 1);
-          if (leader) mbar_expect_tx(&sm.full[s], kF * kStageBytes);
-          load(s, sA + s * kABytes, wm, (kb0 + i) * 64, wrow);
+          mbar_expect_tx(&sm.full[s], kStageBytes);
+          tma_load_2d(sA + s * kABytes, wm, &sm.full[s], (kb0 + i) * 64, wrow, pol);
         }
-        wait_ge(p.progress + it.r, sm.unit_cum[it.tp]);
+        wait_ge(p.progress + it.r, sm.unit_cum[tp]);
         fence_proxy_async_global();
-        if (trace) trace[(size_t)it.idx * 8 + 1] = globaltimer();
+        if (p.trace) p.trace[(size_t)idx * 8 + 1] = globaltimer();
         for (int i = 0; i < pre; ++i) {
           const int s = (kbi + i) % STAGES;
-          load(s, sB + s * kBBytes, xm, (kb0 + i) * 64, xrow);
+          tma_load_2d(sB + s * kBBytes, xm, &sm.full[s], (kb0 + i) * 64, xrow, pol);
         }
         for (int i = pre; i < nkb; ++i) {
           const uint32_t k = kbi + i;
           const int s = k % STAGES;
           mbar_wait_sleep(&sm.empty[s], ((k / STAGES) & 1) ^ 1);
-          if (leader) mbar_expect_tx(&sm.full[s], kF * kStageBytes);
-          load(s, sA + s * kABytes, wm, (kb0 + i) * 64, wrow);
-          load(s, sB + s * kBBytes, xm, (kb0 + i) * 64, xrow);
+          mbar_expect_tx(&sm.full[s], kStageBytes);
+          tma_load_2d(sA + s * kABytes, wm, &sm.full[s], (kb0 + i) * 64, wrow, pol);
+          tma_load_2d(sB + s * kBBytes, xm, &sm.full[s], (kb0 + i) * 64, xrow, pol);
         }
         kbi += nkb;
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (the leader's, for the pair) ----------------
-    if (lane == 0 && leader) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
       uint32_t qi = 0, kbi = 0, gi = 0;
       for (;;) {
         const int slot = qi % kQ;
@@ -644,9 +582,9 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         ++qi;
         if (it.kind == K_END) break;
         if (!is_gemm(it.kind)) continue;
-        const int nkb = n_kblocks(it.kind);
+        const int nkb = it.kind == K_IN ? p.C / 64 : it.kind == K_DOWN ? p.ff / 64 / p.down_split : p.d / 64;
         const int acc = gi & 1;
-        mbar_wait_sleep(&sm.acc_empty[acc], ((gi >> 1) & 1) ^ 1);  // both CTAs drained this buffer
+        mbar_wait_sleep(&sm.acc_empty[acc], ((gi >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t td = tmem + acc * TR;
         for (int i = 0; i < nkb; ++i) {
@@ -657,38 +595,29 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
           const uint64_t ad = sdesc_k_sw128(smem_addr(sA + s * kABytes));
           const uint64_t bd = sdesc_k_sw128(smem_addr(sB + s * kBBytes));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            if constexpr (PAIR) tc_mma_bf16_pair(td, ad + 2 * kk, bd + 2 * kk, kIdesc, (i | kk) != 0);
-            else tc_mma_bf16(td, ad + 2 * kk, bd + 2 * kk, kIdesc, (i | kk) != 0);
-          }
-          if constexpr (PAIR) tc_commit_pair(&sm.empty[s], 3);
-          else tc_commit(&sm.empty[s]);
+          for (int kk = 0; kk < 4; ++kk) tc_mma_bf16(td, ad + 2 * kk, bd + 2 * kk, kIdesc, (i | kk) != 0);
+          tc_commit(&sm.empty[s]);
         }
-        if constexpr (PAIR) tc_commit_pair(&sm.acc_full[acc], 3);
-        else tc_commit(&sm.acc_full[acc]);
+        tc_commit(&sm.acc_full[acc]);
         kbi += nkb;
         ++gi;
       }
     }
   } else {
-    // ---------------- epilogue / LN / attention (warps 2..9) ----------------
-    const int ew = warp - 2;          // 0..kEpiWarps-1 worker index
-    const int sub = ew >> 2;          // which 1/kSub of the item's chunks (quadrant partners: ew ^ 4k)
+    // ---------------- epilogue / LN / attention (warps 2..5) ----------------
+    const int ew = warp - 2;          // 0..7 worker index
+    const int half = ew >> 2;         // which half of the item's chunks (quadrant partner: ew ^ 4)
     const int quad = warp & 3;        // TMEM lane quadrant this warp may access
-    const int et = ew * 32 + lane;    // 0..kEpiThreads-1
+    const int et = ew * 32 + lane;    // 0..255
     const int fl = quad * 32 + lane;  // output feature (TMEM lane) of this thread within a tile
     const int ld_mod = p.L * 6 * p.d;
     uint32_t qi = 0, gi = 0;
     for (;;) {
       const int slot = qi % kQ;
-      if (leader) mbar_wait_sleep(&sm.q_full[slot], (qi / kQ) & 1);
-      else mbar_wait_sleep_cluster(&sm.q_full[slot], (qi / kQ) & 1);
+      mbar_wait_sleep(&sm.q_full[slot], (qi / kQ) & 1);
       const Item it = sm.ring[slot];
       __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(&sm.q_empty[slot]);
-        else mbar_arrive_cluster(dsmem_map(smem_addr(&sm.q_empty[slot]), 0));
-      }
+      if (lane == 0) mbar_arrive(&sm.q_empty[slot]);
       ++qi;
       if (it.kind == K_END) break;
       const float* mod_t = p.mod_table + (size_t)it.step * p.vocab * ld_mod;
@@ -696,7 +625,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
       const int tok0 = it.r * Tl::tok;
       if (is_gemm(it.kind)) {
         const bool gated = it.kind == K_O || it.kind == K_DOWN;
-        const int ft = feat_block(it);
+        const int ft = it.kind == K_DOWN ? it.j / p.down_split : it.kind == K_OUT ? 0 : it.j;
         const int f = ft * kDitFeat + fl;  // this thread's output feature
         const int tix = it.r * nf + ft;
         // static side inputs first, overlapping the item's mainloop: the adaLN
@@ -709,7 +638,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
           const int goff = it.layer * 6 * p.d + (it.kind == K_O ? 2 : 5) * p.d + f;
           int id[Tile<TR>::my_chunks];
 #pragma unroll
-          for (int c = 0; c < Tl::my_chunks; ++c) id[c] = p.toks[tok0 + sub + kSub * c].id;  // my chunks' tokens
+          for (int c = 0; c < Tl::my_chunks; ++c) id[c] = p.toks[tok0 + half + 2 * c].id;  // my chunks' tokens
 #pragma unroll
           for (int c = 0; c < Tl::my_chunks; ++c) aux[c] = mod_t[(size_t)id[c] * ld_mod + goff];
         }
@@ -717,7 +646,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         mbar_wait_sleep(&sm.acc_full[acc], (gi >> 1) & 1);
         tc_fence_after();
         ++gi;
-        if (trace && et == 0) trace[(size_t)it.idx * 8 + 2] = globaltimer();
+        if (p.trace && et == 0) p.trace[(size_t)it.idx * 8 + 2] = globaltimer();
         // split MLP-down: parts meet pairwise, (p0 + p1) [+ (p2 + p3)]; in
         // each pair / between the pairs the first arriver writes its partial
         // and the second adds it (commutative: arrival order never changes bits)
@@ -749,44 +678,40 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         float* part2 = p.part2 + (size_t)tix * TR * kDitFeat;        // the first pair sum
         const uint32_t ta = tmem + acc * TR + (static_cast<uint32_t>(quad * 32) << 16);
         switch (it.kind) {  // once per item: the chunk loop is specialised per kind (no jump table inside)
-          case K_IN: epi_chunks<TR, K_IN, 0>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-          case K_QKV: epi_chunks<TR, K_QKV, 0>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-          case K_UP: epi_chunks<TR, K_UP, 0>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-          case K_OUT: epi_chunks<TR, K_OUT, 0>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-          case K_O: epi_chunks<TR, K_O, 0>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
+          case K_IN: epi_chunks<TR, K_IN, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_QKV: epi_chunks<TR, K_QKV, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_UP: epi_chunks<TR, K_UP, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_OUT: epi_chunks<TR, K_OUT, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+          case K_O: epi_chunks<TR, K_O, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
           default:
             switch (mode) {
-              case 1: epi_chunks<TR, K_DOWN, 1>(p, ta, row0, ft, part1, part2, const_cast<float*>(part1), quad, sub, lane, aux, it.step); break;
-              case 2: epi_chunks<TR, K_DOWN, 2>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-              case 3: epi_chunks<TR, K_DOWN, 3>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-              case 4: epi_chunks<TR, K_DOWN, 4>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
-              default: epi_chunks<TR, K_DOWN, 0>(p, ta, row0, ft, part1, part2, part2, quad, sub, lane, aux, it.step); break;
+              case 1: epi_chunks<TR, K_DOWN, 1>(p, ta, row0, ft, part1, part2, const_cast<float*>(part1), quad, half, lane, aux, it.step); break;
+              case 2: epi_chunks<TR, K_DOWN, 2>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+              case 3: epi_chunks<TR, K_DOWN, 3>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+              case 4: epi_chunks<TR, K_DOWN, 4>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
+              default: epi_chunks<TR, K_DOWN, 0>(p, ta, row0, ft, part1, part2, part2, quad, half, lane, aux, it.step); break;
             }
             break;
         }
-        if (trace && et == 0) trace[(size_t)it.idx * 8 + 5] = globaltimer();
+        if (p.trace && et == 0) p.trace[(size_t)it.idx * 8 + 5] = globaltimer();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          if (leader) mbar_arrive(&sm.acc_empty[acc]);
-          else mbar_arrive_cluster(dsmem_map(smem_addr(&sm.acc_empty[acc]), 0));
-        }
+        if (lane == 0) mbar_arrive(&sm.acc_empty[acc]);
         if (mode == 1 || mode == 3) {
           ep_bar();
           if (et == 0) {
             __threadfence();
             atomicAdd(mode == 1 ? p.ready + tix2 : p.ready2 + tix, 1);
-            if (trace) trace[(size_t)it.idx * 8 + 3] = globaltimer();
+            if (p.trace) p.trace[(size_t)it.idx * 8 + 3] = globaltimer();
           }
           continue;  // no unit of progress: the final sum completes the tile
         }
       } else {
         // LN / attention items: wait for the tile's earlier phases
-        const int ju = kF * it.j + (int)rank;  // this CTA's unit of the item
         float4 sc[PER], sh[PER];
         const bool mod = it.kind == K_LN1 || it.kind == K_LN2;
         if (mod) {  // the token's adaLN rows are static: load them before the wait
-          const float* mr = mod_t + (size_t)p.toks[tok0 + ju].id * ld_mod + it.layer * 6 * p.d;
+          const float* mr = mod_t + (size_t)p.toks[tok0 + it.j].id * ld_mod + it.layer * 6 * p.d;
           const int sh_off = it.kind == K_LN1 ? 0 : 3 * p.d, sc_off = it.kind == K_LN1 ? p.d : 4 * p.d;
 #pragma unroll
           for (int k = 0; k < PER; ++k) {
@@ -796,16 +721,15 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         }
         if (et == 0) {
           wait_ge(p.progress + it.r, sm.unit_cum[it.tp]);
-          if (trace) trace[(size_t)it.idx * 8 + 1] = trace[(size_t)it.idx * 8 + 2] = globaltimer();
+          if (p.trace) p.trace[(size_t)it.idx * 8 + 1] = p.trace[(size_t)it.idx * 8 + 2] = globaltimer();
         }
         ep_bar();
         if (it.kind == K_ATT) {
-          const int hgs = p.H / Tl::att_heads, hg = ju % hgs, grp = ju / hgs;
-          attn_token_head(p.qkv, tok0 + grp * Tl::att_tok + ew % Tl::att_tok, hg * Tl::att_heads + ew / Tl::att_tok,
-                          p.d, p.o, lane);
+          const int h = it.j % p.H, grp = it.j / p.H;  // item = (head, group of kEpiWarps tokens)
+          attn_token_head(p.qkv, tok0 + grp * kEpiWarps + ew, h, p.d, p.o, lane);
         } else {
           constexpr int kRows = 16 / kEpiWarps;  // rows of the token per warp
-          const int row = (tok0 + ju) * 16 + ew * kRows;
+          const int row = (tok0 + it.j) * 16 + ew * kRows;
           ln_rows<PER, kRows>(p.h + (size_t)row * p.d, mod, sc, sh, p.a + (size_t)row * p.d, lane);
         }
       }
@@ -814,72 +738,38 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
       fence_proxy_async_global();
       ep_bar();
       if (et == 0) {
-        if (trace) trace[(size_t)it.idx * 8 + 6] = globaltimer();
+        if (p.trace) p.trace[(size_t)it.idx * 8 + 6] = globaltimer();
         __threadfence();
         atomicAdd(p.progress + it.r, 1);
-        if (trace) trace[(size_t)it.idx * 8 + 3] = globaltimer();
+        if (p.trace) p.trace[(size_t)it.idx * 8 + 3] = globaltimer();
       }
     }
   }
   tc_fence_before();
-  if constexpr (PAIR) {
-    cluster_sync();  // no remote arrive / multicast commit targets a CTA that has exited
-    if (warp == 1) tmem_free2<512>(tmem);
-  } else {
-    __syncthreads();
-    if (warp == 1) tmem_free<512>(tmem);
-  }
+  __syncthreads();
+  if (warp == 1) tmem_free<512>(tmem);
 }
 
-template <int STAGES, int TR, bool PAIR>
+template <int STAGES, int TR>
 constexpr size_t smem_bytes() {
-  constexpr int b_rows = PAIR ? TR / 2 : TR;
-  return 1024 + (size_t)STAGES * (kABytes + b_rows * 64 * 2) + sizeof(Smem);
+  return 1024 + (size_t)STAGES * Tile<TR>::stage_bytes + sizeof(Smem);
 }
-static_assert(smem_bytes<4, 256, false>() <= 227 * 1024, "4-stage 256-row ring must fit");
-static_assert(smem_bytes<6, 256, true>() <= 227 * 1024, "6-stage 256-row pair ring must fit");
+static_assert(smem_bytes<4, 256>() <= 227 * 1024, "4-stage 256-row ring must fit");
 
-template <int PER, int STAGES, int TR, bool PAIR>
+template <int PER, int STAGES, int TR>
 cudaError_t launch_fused(const DitFusedParams& p, int ctas, cudaStream_t st) {
-  auto kern = dit_fused_kernel<PER, STAGES, TR, PAIR>;
-  constexpr size_t smem = smem_bytes<STAGES, TR, PAIR>();
+  auto kern = dit_fused_kernel<PER, STAGES, TR>;
+  constexpr size_t smem = smem_bytes<STAGES, TR>();
   static std::atomic<uint64_t> configured{0};
   if (cudaError_t e = smem_attr_once(kern, smem, configured); e != cudaSuccess) return e;
-  if constexpr (PAIR) {  // 2-clusters along x (a (1, 1, ctas) grid with z-clusters is rejected at launch)
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(ctas);
-    cfg.blockDim = dim3(kThreadsF);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kern, p);
-  }
   return launch_k(kern, dim3(ctas), dim3(kThreadsF), smem, st, 1, p);
-}
-
-template <int PER>
-cudaError_t launch_per(const DitFusedParams& p, int ctas, cudaStream_t st) {
-  const bool wide = p.tile_rows == 256;
-  if (p.pair)  // 6-stage rings: a pair stage is 24 / 32 KB
-    return wide ? launch_fused<PER, 6, 256, true>(p, ctas, st) : launch_fused<PER, 6, 128, true>(p, ctas, st);
-  // 4-stage rings for both tiles (128 rows: 32 KB stages -- 6 stages measured slower, r02_dit_fused_v7.txt)
-  return wide ? launch_fused<PER, 4, 256, false>(p, ctas, st) : launch_fused<PER, 4, 128, false>(p, ctas, st);
 }
 
 }  // namespace
 
-int dit_fused_items(int n_rt, int tile_rows, int d, int H, int ff, int L, int T, int down_split, bool pair) {
-  const int f = pair ? 2 : 1;
+int dit_fused_items(int n_rt, int tile_rows, int d, int H, int ff, int L, int T, int down_split) {
   const int nf = d / kDitFeat, tok = tile_rows / 16, att = H * tok / kEpiWarps;
-  const int per_step = (nf + L * (tok + 3 * nf + att + nf + tok + ff / kDitFeat + nf * down_split) + tok) / f + 1;
+  const int per_step = nf + L * (tok + 3 * nf + att + nf + tok + ff / kDitFeat + nf * down_split) + tok + 1;
   return per_step * T * n_rt;
 }
 
@@ -890,15 +780,16 @@ bool dit_fused_supported(int d, int C, int H, int ff, int L, int T) {
 
 cudaError_t dit_fused_run(const DitFusedParams& p, int stages, int ctas, cudaStream_t st) {
   if (!dit_fused_supported(p.d, p.C, p.H, p.ff, p.L, p.T) || (p.down_split != 1 && p.down_split != 2 && p.down_split != 4) ||
-      (p.ff / 64) % p.down_split != 0 || p.n_rt <= 0 ||
-      (p.pair && (ctas % 2 != 0 || p.ff % (2 * kDitFeat) != 0)))
+      (p.ff / 64) % p.down_split != 0 || p.n_rt <= 0)
     return cudaErrorInvalidValue;
-  if (p.tile_rows != 256 && p.tile_rows != 128) return cudaErrorInvalidValue;
+  // 4-stage rings for both tiles (128 rows: 32 KB stages -- 6 stages measured slower, r02_dit_fused_v7.txt)
+  const bool wide = p.tile_rows == 256;
+  if (!wide && p.tile_rows != 128) return cudaErrorInvalidValue;
   (void)stages;
   switch (p.d / 128) {
-    case 2: return launch_per<2>(p, ctas, st);
-    case 4: return launch_per<4>(p, ctas, st);
-    case 8: return launch_per<8>(p, ctas, st);
+    case 2: return wide ? launch_fused<2, 4, 256>(p, ctas, st) : launch_fused<2, 4, 128>(p, ctas, st);
+    case 4: return wide ? launch_fused<4, 4, 256>(p, ctas, st) : launch_fused<4, 4, 128>(p, ctas, st);
+    case 8: return wide ? launch_fused<8, 4, 256>(p, ctas, st) : launch_fused<8, 4, 128>(p, ctas, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -25,8 +25,7 @@ struct DitMaps {
   // weights (MMA A operand), 128-row boxes; w_out is [C_pad 128, d]
   CUtensorMap w_in, w_out;
   CUtensorMap wqkv[kDitMaxLayers], wo[kDitMaxLayers], w1[kDitMaxLayers], w2[kDitMaxLayers];
-  // activations (MMA B operand), [0] 128- / [1] 256- / [2] 64-row boxes (CTA pairs load half a tile)
-  CUtensorMap x_x[3], x_a[3], x_o[3], x_u[3];
+  CUtensorMap x_x[2], x_a[2], x_o[2], x_u[2];  // activations (MMA B operand), [0] 128- / [1] 256-row boxes
 };
 
 // Everything else one iteration needs (a small __grid_constant__ parameter).
@@ -50,12 +49,11 @@ struct DitFusedParams {
   int* next_item;                  // global item counter (zeroed per launch)
   unsigned long long* trace;       // optional [items][5]: fetch, dep ok, mma done, done, smid
   int n_rt, tile_rows, d, C, H, ff, L, T, vocab, down_split;
-  int pair;  // 2-CTA clusters, one tcgen05.mma.cta_group::2 per k-step (ctas even)
   float dt, sample_scale;
 };
 
 // Total items of one launch (tests / tools).
-int dit_fused_items(int n_rt, int tile_rows, int d, int H, int ff, int L, int T, int down_split, bool pair = false);
+int dit_fused_items(int n_rt, int tile_rows, int d, int H, int ff, int L, int T, int down_split);
 // Row tile of a batch of n_tok (padded) tokens on a persistent grid of
 // `ctas`: 128 rows (more, shorter items: the per-layer dependency chain of a
 // tile is the iteration's latency floor) until the batch has as many tokens

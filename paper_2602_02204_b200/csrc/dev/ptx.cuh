@@ -306,69 +306,6 @@ __device__ __forceinline__ float dsmem_ld_f32(uint32_t cluster_saddr) {
   return v;
 }
 
-// ---- CTA pairs (cta_group::2) ------------------------------------------------
-// Two CTAs of a 2-cluster share one tcgen05.mma.cta_group::2 (M = 256): each
-// holds its 128 rows of A and N/2 rows of B in its own shared memory (same
-// offsets), each receives its 128 accumulator lanes x N columns in its own
-// TMEM. Only the leader (rank 0) issues the MMA; both CTAs load their halves
-// by TMA, completing on the LEADER's mbarrier.
-template <uint32_t kCols>
-__device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem) {  // one warp in EACH CTA of the pair
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(dst_smem)),
-               "n"(kCols)
-               : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-}
-template <uint32_t kCols>
-__device__ __forceinline__ void tmem_free2(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
-}
-__device__ __forceinline__ void tc_mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                                 uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Arrive on the mbarrier at the same offset in every CTA of `mask` once the
-// pair's previously issued MMAs completed.
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_addr(bar)),
-      "h"(mask)
-      : "memory");
-}
-// 2-D TMA load into this CTA's shared memory that completes on an mbarrier
-// given by its shared::cluster address (the leader's, in a pair).
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m, uint32_t cluster_bar, int x, int y,
-                                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_addr(dst)),
-      "l"(m), "r"(cluster_bar), "r"(x), "r"(y), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
-}
-// Blocking wait with cluster-scope acquire (the phase was completed by a
-// remote CTA's release.cluster arrive).
-__device__ __forceinline__ void mbar_wait_sleep_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "OMNI_WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra OMNI_WAITC_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity), "r"(0x989680)
-      : "memory");
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t cluster_saddr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_saddr), "r"(v) : "memory");
-}
-
 // ---- programmatic dependent launch (PDL) -----------------------------------
 // Every kernel of a stage step is launched with programmatic stream
 // serialization: it may start while its predecessor is still running, and

@@ -284,10 +284,6 @@ void build_dit(omni_stage* st) {
     OMNI_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->dev));
     st->dit_ctas = st->dit_sms_all = sms;
   }
-  {  // OMNI_DIT_PAIR=1 at stage creation: 2-CTA clusters (cta_group::2 items of 256 features)
-    const char* e = std::getenv("OMNI_DIT_PAIR");
-    st->dit_pair = e && e[0] == '1' && ff % (2 * kDitFeat) == 0;
-  }
   if (const char* e = std::getenv("OMNI_DIT_TRACE"); e && e[0] == '1') {
     st->dit_trace_items = dit_fused_items(n_rt, kDitTileRows, d, m.n_heads, ff, L, m.dit_steps, st->down_split);
     st->dit_trace = dev_alloc<unsigned long long>(st, (size_t)st->dit_trace_items * 8);
@@ -311,12 +307,11 @@ void build_dit(omni_stage* st) {
       mp.w1[l] = ly.g1.tmap;
       mp.w2[l] = ly.g2.tmap;
     }
-    for (int i = 0; i < 3; ++i) {  // 128- / 256-row boxes (dit_tile_rows), 64 (half a 128-row tile, CTA pairs)
-      const int rows = i == 2 ? 64 : 128 << i;
-      mp.x_x[i] = st->din_x.tmap_for(rows);
-      mp.x_a[i] = st->din_a.tmap_for(rows);
-      mp.x_o[i] = st->din_o.tmap_for(rows);
-      mp.x_u[i] = st->din_u.tmap_for(rows);
+    for (int i = 0; i < 2; ++i) {  // 128- and 256-row boxes (dit_tile_rows)
+      mp.x_x[i] = st->din_x.tmap_for(128 << i);
+      mp.x_a[i] = st->din_a.tmap_for(128 << i);
+      mp.x_o[i] = st->din_o.tmap_for(128 << i);
+      mp.x_u[i] = st->din_u.tmap_for(128 << i);
     }
     st->dmaps = dev_alloc<DitMaps>(st, 1);
     OMNI_CUDA(cudaMemcpyAsync(st->dmaps, &mp, sizeof(mp), cudaMemcpyHostToDevice, st->stream));
@@ -872,8 +867,7 @@ bool dit_fused_enabled() {  // OMNI_DIT_FUSED=0: one kernel per op (A/B only)
 void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int32_t* samples_dev) {
   const auto& m = st->m;
   const int d = m.d_model, L = m.n_layers, C = m.dit_channels, S = kDitSamples;
-  const bool pair = st->dit_pair;
-  const int ctas = dit_ctas_for(st, n_tok) & (pair ? ~1 : ~0);
+  const int ctas = dit_ctas_for(st, n_tok);
   const int tile_rows = dit_tile_rows(n_tok, ctas);
   const int n_rt = n_tok * S / tile_rows, nfd = d / kDitFeat;
   cudaStream_t s = st->stream;
@@ -910,7 +904,6 @@ void dit_chunk_fused(omni_stage* st, const DitTokDesc* toks_dev, int n_tok, int3
   p.T = m.dit_steps;
   p.vocab = m.vocab;
   p.down_split = st->down_split;
-  p.pair = pair;
   p.dt = 1.f / m.dit_steps;
   p.sample_scale = kSampleScale;
   p.trace = st->dit_trace;

@@ -138,7 +138,6 @@ struct omni_stage {
   int dctl_n = 0, down_split = 1, dit_stages = 4;
   int dit_ctas = 0;  // SM share of the fused iteration (omni_stage_set_sm_share); see dit_ctas_for
   int dit_sms_all = 0;
-  bool dit_pair = false;  // fused iteration on 2-CTA clusters (dit_fused.h DitFusedParams::pair)
   omni_dev::DitMaps* dmaps = nullptr;  // device copy of the fused iteration's TMA descriptors
   unsigned long long* dit_trace = nullptr;  // OMNI_DIT_TRACE=1 (tools/dit_trace.py)
   int dit_trace_items = 0;

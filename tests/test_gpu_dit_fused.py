@@ -59,46 +59,3 @@ def test_fused_batching_and_grid_invariance_default_dims():
         assert np.array_equal(st.dit_step([9], [0], [n], codec), whole), sms
     st.set_sm_share(0)
     st.close()
-
-
-@pytest.mark.parametrize("n", [40, 200])
-def test_pair_clusters_match_single_cta(monkeypatch, n):
-    """2-CTA clusters (OMNI_DIT_PAIR=1: tcgen05.mma.cta_group::2, 256-feature
-    items, each CTA loading half the row tile) against the single-CTA kernel:
-    the same K order per output, so the same samples and latents; n = 200
-    takes 256-row tiles (n >= the grid), n = 40 128-row tiles."""
-    m = D.model_default(D.DIT)
-    rng = np.random.default_rng(5)
-    codec = [int(x) for x in rng.integers(0, 64, size=n)]
-    out = {}
-    for pair in ("0", "1"):
-        monkeypatch.setenv("OMNI_DIT_PAIR", pair)
-        st = D.Stage(m, D.StageLimits(256, 8, 256, 0, 256), seed=41)
-        st.set_sm_share(148 if n >= 148 else 0)
-        s = st.dit_step([9], [0], [n], codec)
-        lat = D.d2h(st.tensor("buf.dit_x")[0], (n * 16 * m.dit_channels,), np.float32)
-        out[pair] = (s, lat)
-        if pair == "1":  # grid invariance holds for pairs too
-            st.set_sm_share(38)
-            assert np.array_equal(st.dit_step([9], [0], [n], codec), s)
-        st.close()
-    assert np.array_equal(out["0"][0], out["1"][0])
-    err = np.abs(out["0"][1] - out["1"][1])
-    assert err.max() <= 1e-5, f"pair latent diff {err.max()}"
-
-
-def test_pair_clusters_match_oracle(monkeypatch):
-    monkeypatch.setenv("OMNI_DIT_PAIR", "1")
-    m = D.model_default(D.DIT, d_model=256, n_layers=2, n_heads=2, n_kv_heads=2, d_ff=512)
-    st = D.Stage(m, D.StageLimits(256, 8, 256, 0, 96), seed=77)
-    om = oracle.Model(m, 77)
-    rng = np.random.default_rng(11)
-    n = 53
-    codec = [int(x) for x in rng.integers(0, 64, size=n)]
-    g = st.dit_step([4], [3], [n], codec)
-    c, lat = om.dit([4] * n, list(range(3, 3 + n)), codec, with_latents=True)
-    gl = D.d2h(st.tensor("buf.dit_x")[0], (n * 16 * m.dit_channels,), np.float32)
-    err = np.abs(gl - lat)
-    assert np.all(err <= LAT_ATOL + LAT_RTOL * np.abs(lat)), f"latent err {err.max():.4f}"
-    check_samples(g, c)
-    st.close()

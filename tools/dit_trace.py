@@ -52,8 +52,6 @@ def main():
         ph = phases(L)
         items_pp = {"IN": nf, "LN1": tok, "QKV": 3 * nf, "ATT": H * tok // 8, "O": nf, "LN2": tok, "UP": ff // 128,
                     "DOWN": nf * ds, "LNF": tok, "OUT": 1}
-        if os.environ.get("OMNI_DIT_PAIR") == "1":  # CTA pairs: two units per item (OUT stays one item)
-            items_pp = {k: (v if k == "OUT" else v // 2) for k, v in items_pp.items()}
         total = sum(items_pp[k] for k in ph) * T * n_rt
         tr = D.d2h(ptr, (total, 8), np.uint64).astype(np.int64)
         t0 = tr[:, 0].min()
