@@ -3,7 +3,9 @@ reference's property test (test_properties.cpp:139-154: 150 random
 schedules, batched output == solo output) restated for the B200 pipeline.
 
 Every trial draws a random engine configuration (token budget, prefill
-chunk, resident cap per AR stage, streaming chunk sizes of both edges),
+chunk, resident cap per AR stage, in some trials tight KV budgets that force
+admission blocking and recompute preemption, streaming chunk sizes of both
+edges),
 concurrency and clock, runs the same workload through the full
 Thinker -> Talker -> Code2Wav pipeline and compares EVERY request's text
 tokens, codec tokens, waveform samples and Thinker hidden rows with a solo
@@ -26,6 +28,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 N_REQ, SEED, WEIGHTS = 14, 21, 5
 OUTS = {"text": 1, "codec": 2, "wave": 3, "hidden": 4}
+PREEMPTIONS = []  # per trial, to check the tight-budget trials really preempt
 
 
 def outputs(p, n):
@@ -39,6 +42,9 @@ def random_config(rng: random.Random) -> tuple[str, dict]:
         e["max_batch_tokens"] = rng.choice([32, 48, 64, 100, 160, 256])
         e["prefill_chunk"] = min(rng.choice([1, 5, 16, 33, 64]), e["max_batch_tokens"])  # registry.cpp rule
         e["max_resident_requests"] = rng.choice([2, 3, 5, 8, 64])
+    if rng.random() < 0.3:  # tight KV budgets: admission blocking and recompute preemption (omni3_tight)
+        cfg["engines"]["thinker"]["kv_budget_tokens"] = rng.choice([256, 320, 400])
+        cfg["engines"]["talker"]["kv_budget_tokens"] = rng.choice([384, 512, 640])
     cfg["engines"]["vocoder"]["max_resident_requests"] = rng.choice([1, 2, 7, 64])
     cfg["graph"]["edges"][0]["chunk_size"] = rng.choice([1, 2, 4, 7])
     cfg["graph"]["edges"][1]["chunk_size"] = rng.choice([1, 3, 8, 16])
@@ -73,6 +79,7 @@ def check_trial(solo, trial, small):
     p = Pipeline(text, weight_seed=WEIGHTS, small_models=small)
     r = p.bench(n=N_REQ, seed=SEED, concurrency=run["concurrency"], clock=run["clock"], capture=True)
     assert r["completed"] == N_REQ and r["failed"] == 0, (run, r)
+    PREEMPTIONS.append(r["preemptions"])
     got = outputs(p, N_REQ)
     p.close()
     for rid in range(1, N_REQ + 1):
@@ -92,3 +99,9 @@ def test_batched_equals_solo_full_size(solo_full, trial):
     """The bench's model dimensions (every GEMM tile / split / attention path
     the bench uses) under four random schedules."""
     check_trial(solo_full, 1000 + trial, False)
+
+
+def test_tight_budget_trials_preempted():
+    if not PREEMPTIONS:
+        pytest.skip("no trial ran in this session")
+    assert sum(1 for x in PREEMPTIONS if x > 0) >= 5, PREEMPTIONS
