@@ -97,7 +97,11 @@ omni_status omni_stage_create(const omni_model_desc* model, const omni_stage_lim
                               int32_t dev, uint64_t weight_seed, omni_stage** out);
 omni_status omni_stage_destroy(omni_stage* st);
 omni_status omni_stage_weight_bytes(const omni_stage* st, uint64_t* bytes);
-/* Raw device address of a named weight tensor (tests / oracle checks). */
+/* Raw device address of a named weight tensor (tests / oracle checks).
+ * Row-major [rows, cols] bf16, except names ending in ".tiled" (the AR
+ * stages' gate-up / down weights, "L<l>.wgu.tiled", "L<l>.wd.tiled"): those
+ * hold [rows/128][cols/64] blocks of 16 KB, each the SWIZZLE_128B shared-
+ * memory image of its 128 x 64 tile (gemm_tc.cu block_weight_kernel). */
 omni_status omni_stage_tensor(const omni_stage* st, const char* name, uint64_t* dev_ptr,
                               int64_t* rows, int64_t* cols);
 

@@ -195,6 +195,16 @@ omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, i
     e.ldo = ldo;
     cudaStream_t cs;
     OMNI_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    // decode weights as the stages store them (pre-tiled when gemm_decode_weights_blocked)
+    std::vector<void*> blks;
+    if (!fill && gemm_decode_weights_blocked())
+      for (auto& w : ws) {
+        void* p = nullptr;
+        OMNI_CUDA(cudaMalloc(&p, (size_t)N_pad * K * 2));
+        blks.push_back(p);
+        OMNI_CUDA(gemm_block_weight(w.ptr, N_pad, K, static_cast<uint8_t*>(p), cs));
+        w.blk = static_cast<const uint8_t*>(p);
+      }
     for (int i = 0; i < n_w; ++i) OMNI_CUDA(gemm_run(ws[i], x, M, epi, e, cs));
     OMNI_CUDA(cudaStreamSynchronize(cs));
     cudaGraph_t g;
@@ -220,6 +230,7 @@ omni_status omni_k_gemm_time_multi(const uint64_t* Ws, int32_t n_w, int32_t N, i
     cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
     cudaStreamDestroy(cs);
+    for (void* p : blks) cudaFree(p);
   });
 }
 

@@ -43,6 +43,10 @@ struct GemmWeight {
   int splits = 1;
   bool fill_sms = false;  // compute-bound (DiT): pick the token tile to fill 148 SMs
   CUtensorMap tmap;
+  // optional pre-tiled copy: [N_pad/128][K/64] blocks of 16 KB, each the
+  // SWIZZLE_128B shared-memory image of its 128 x 64 tile (gemm_block_weight);
+  // loaded with 1-D bulk copies instead of strided 2-D TMA boxes
+  const uint8_t* blk = nullptr;
 };
 
 // An activation buffer X[rows_cap, K] bf16 row-major; one TMA descriptor per
@@ -113,9 +117,15 @@ struct GemmArgs {
   unsigned long long* trace;
   float dt, sample_scale;
   int32_t* samples;
+  const uint8_t* w_blk;  // GemmWeight::blk (nullptr: 2-D TMA of the row-major weight)
 };
 
 int gemm_block_n(int M);
+// The AR stages' streaming weights (gate-up, down) are stored pre-tiled
+// (default; OMNI_WBLOCK=0 keeps them row-major).
+bool gemm_decode_weights_blocked();
+// Writes the pre-tiled copy of a row-major weight [N_pad, K] (GemmWeight::blk).
+cudaError_t gemm_block_weight(const __nv_bfloat16* w, int N_pad, int K, uint8_t* blk, cudaStream_t st);
 // Split-K reduction by st.async push (decode tiles BN <= 32, 2- or 8-way
 // splits); OMNI_SPLITK_PUSH=0 selects the cluster-barrier pull variant.
 bool gemm_push_enabled();

@@ -88,6 +88,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const long long c0 = clock64();
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   const int kb0 = split * kb_per;
+  // weight tile (n_tile, kb): a 16 KB block of the pre-tiled copy, or a 2-D TMA box
+  auto load_w = [&](uint8_t* dst, uint64_t* bar, int kb, uint64_t pol) {
+    if (a.w_blk)
+      bulk_load_hint(dst, a.w_blk + ((size_t)n_tile * (a.K / kBlockK) + kb) * kABytes, kABytes, bar, pol);
+    else
+      tma_load_2d(dst, &tmW, bar, kb * kBlockK, n_tile * kBlockM, pol);
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmW);
@@ -118,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int pre = kb_per < STAGES ? kb_per : STAGES;
       for (int i = 0; i < pre; ++i) {
         mbar_expect_tx(&full[i], kABytes + kBBytes);
-        tma_load_2d(sA + i * kABytes, &tmW, &full[i], (kb0 + i) * kBlockK, n_tile * kBlockM, pol_w);
+        load_w(sA + i * kABytes, &full[i], kb0 + i, pol_w);
       }
       pdl_wait();
       if (g_gemm_marks && EPI == EPI_RESID_NORM && a.K == 2048) atomicMax(g_gemm_marks + 1, globaltimer());
@@ -131,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], kABytes + kBBytes);
         const int kx = (kb0 + i) * kBlockK;
-        tma_load_2d(sA + s * kABytes, &tmW, &full[s], kx, n_tile * kBlockM, pol_w);
+        load_w(sA + s * kABytes, &full[s], kb0 + i, pol_w);
         tma_load_2d(sB + s * kBBytes, &tmX, &full[s], kx, m_tile * BN, pol_x);
       }
       if (tr) tr[3] = clock64() - c0;
@@ -435,6 +442,36 @@ static int bn_for(const GemmWeight& w, int M) {
   return bn;
 }
 
+// dst 16-byte chunk (tile, kb, row r, position j') <- source chunk
+// j = j' ^ (r & 7) of row tile*128 + r, columns kb*64 + 8j .. +7: the
+// SWIZZLE_128B image TMA would write for a 1024-byte aligned box.
+__global__ void block_weight_kernel(const uint4* __restrict__ w, int K, int64_t n_chunks, uint4* __restrict__ blk) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= n_chunks) return;
+  const int kbt = K / kBlockK;
+  const int jp = (int)(q & 7), r = (int)((q >> 3) & 127);
+  const int64_t box = q >> 10;  // 1024 chunks of 16 B per 16 KB block
+  const int64_t tile = box / kbt, kb = box % kbt;
+  const int j = jp ^ (r & 7);
+  blk[q] = w[((tile * kBlockM + r) * (int64_t)K + kb * kBlockK) / 8 + j];
+}
+
+bool gemm_decode_weights_blocked() {  // OMNI_WBLOCK=0: row-major weights, 2-D TMA boxes (A/B)
+  static const bool on = [] {
+    const char* e = std::getenv("OMNI_WBLOCK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+cudaError_t gemm_block_weight(const __nv_bfloat16* w, int N_pad, int K, uint8_t* blk, cudaStream_t st) {
+  if (N_pad % kBlockM != 0 || K % kBlockK != 0) return cudaErrorInvalidValue;
+  const int64_t n_chunks = (int64_t)N_pad * K / 8;
+  block_weight_kernel<<<(unsigned)((n_chunks + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(w), K, n_chunks, reinterpret_cast<uint4*>(blk));
+  return cudaGetLastError();
+}
+
 int gemm_block_n(int M) {
   return M <= 16 ? 16 : M <= 32 ? 32 : M <= 64 ? 64 : M <= 128 ? 128 : 256;
 }
@@ -475,6 +512,7 @@ cudaError_t gemm_make_args(const GemmWeight& w, const GemmInput& x, int M, int e
   a.row_bias = e.row_bias;
   a.bias_period = e.bias_period > 0 ? e.bias_period : 1;
   if (e.row_bias && (epi != EPI_F32 || w.N != w.N_pad)) return cudaErrorInvalidValue;
+  a.w_blk = w.blk;
   a.pf_ptr = e.pf_ptr;
   a.pf_bytes = e.pf_bytes & ~uint64_t(15);
   if (epi == EPI_RESID_NORM && (e.xb == nullptr || e.ss_out == nullptr || w.N != w.N_pad))

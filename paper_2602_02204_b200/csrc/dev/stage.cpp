@@ -38,28 +38,54 @@ T* dev_alloc(omni_stage* st, size_t count) {
   return static_cast<T*>(p);
 }
 
+// A streaming decode weight is stored pre-tiled (gemm_decode_weights_blocked):
+// generated row-major into a scratch buffer, rewritten as 16 KB tile images.
+template <class Fill>
+void materialise(omni_stage* st, DevTensor& t, Fill fill) {
+  const size_t n = (size_t)t.rows_pad * t.cols;
+  t.p = dev_alloc<__nv_bfloat16>(st, n);
+  if (!t.tiled) {
+    OMNI_KERNEL(fill(t.p));
+    return;
+  }
+  __nv_bfloat16* tmp = nullptr;
+  OMNI_CUDA(cudaMalloc(&tmp, n * sizeof(__nv_bfloat16)));
+  const cudaError_t e1 = fill(tmp);
+  const cudaError_t e2 = e1 == cudaSuccess ? gemm_block_weight(tmp, (int)t.rows_pad, (int)t.cols,
+                                                               reinterpret_cast<uint8_t*>(t.p), st->stream)
+                                           : e1;
+  const cudaError_t e3 = cudaStreamSynchronize(st->stream);
+  cudaFree(tmp);
+  OMNI_CUDA(e2);
+  OMNI_CUDA(e3);
+}
+
 DevTensor make_weight(omni_stage* st, const std::string& name, int64_t rows, int64_t rows_pad,
-                      int64_t cols, uint32_t tid, float scale) {
+                      int64_t cols, uint32_t tid, float scale, bool tiled = false) {
   DevTensor t;
   t.rows = rows;
   t.rows_pad = rows_pad;
   t.cols = cols;
-  t.p = dev_alloc<__nv_bfloat16>(st, (size_t)rows_pad * cols);
-  OMNI_KERNEL(fill_weights(t.p, rows_pad, rows, cols, st->seed, tid, scale, st->stream));
+  t.tiled = tiled;
+  materialise(st, t, [&](__nv_bfloat16* dst) {
+    return fill_weights(dst, rows_pad, rows, cols, st->seed, tid, scale, st->stream);
+  });
   st->weight_bytes += (uint64_t)rows * cols * 2;
-  st->named[name] = t;
+  st->named[tiled ? name + ".tiled" : name] = t;
   return t;
 }
 
 DevTensor make_swiglu(omni_stage* st, const std::string& name, int64_t ff, int64_t cols,
-                      uint32_t tid_gate, uint32_t tid_up, float scale) {
+                      uint32_t tid_gate, uint32_t tid_up, float scale, bool tiled = false) {
   DevTensor t;
   t.rows = t.rows_pad = 2 * ff;
   t.cols = cols;
-  t.p = dev_alloc<__nv_bfloat16>(st, (size_t)2 * ff * cols);
-  OMNI_KERNEL(fill_swiglu(t.p, ff, cols, st->seed, tid_gate, tid_up, scale, st->stream));
+  t.tiled = tiled;
+  materialise(st, t, [&](__nv_bfloat16* dst) {
+    return fill_swiglu(dst, ff, cols, st->seed, tid_gate, tid_up, scale, st->stream);
+  });
   st->weight_bytes += (uint64_t)2 * ff * cols * 2;
-  st->named[name] = t;
+  st->named[tiled ? name + ".tiled" : name] = t;
   return t;
 }
 
@@ -67,6 +93,7 @@ GemmWeight gemm_of(const DevTensor& t, int max_splits, int target_ctas = 192) {
   GemmWeight g;
   OMNI_REQUIRE(gemm_make_weight(g, t.p, (int)t.rows, (int)t.rows_pad, (int)t.cols, max_splits, target_ctas),
                OMNI_E_BADARG, "weight tensor map encode failed");
+  if (t.tiled) g.blk = reinterpret_cast<const uint8_t*>(t.p);
   return g;
 }
 
@@ -143,8 +170,14 @@ void build_ar(omni_stage* st) {
     const std::string p = "L" + std::to_string(l) + ".";
     ly.wqkv = make_weight(st, p + "wqkv", qkv_rows, qkv_rows, d, b + 0, s_d);
     ly.wo = make_weight(st, p + "wo", d, d, H * kHeadDim, b + 1, 1.f / std::sqrt((float)(H * kHeadDim)));
-    ly.wgu = make_swiglu(st, p + "wgu", ff, d, b + 2, b + 3, s_d);
-    ly.wd = make_weight(st, p + "wd", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
+    // the two streaming weights (67 + 33.5 MB per Thinker layer) are stored
+    // pre-tiled: one contiguous 16 KB bulk copy per tile instead of a 2-D box
+    // of 128 strided 128-byte rows (in-chain gate-up 12.2 -> 11.8 us, down
+    // 7.8 -> 7.3 us at 16 rows; QKV / O measured ~3 % slower pre-tiled, their
+    // slices sit in the prefetch ring: profiles/r02_weight_tiles.txt)
+    const bool tiled = gemm_decode_weights_blocked();
+    ly.wgu = make_swiglu(st, p + "wgu", ff, d, b + 2, b + 3, s_d, tiled);
+    ly.wd = make_weight(st, p + "wd", d, d, ff, b + 4, 1.f / std::sqrt((float)ff), tiled);
     ly.gqkv = gemm_of(ly.wqkv, 8);
     ly.go = gemm_of(ly.wo, 8);
     ly.ggu = gemm_of(ly.wgu, 1);  // 128 n-tiles: no split-K (a 2-way split measured neutral)

@@ -23,6 +23,7 @@ constexpr int kStepTraceCtas = 512;     // CTA slots per traced launch
 struct DevTensor {
   __nv_bfloat16* p = nullptr;
   int64_t rows = 0, rows_pad = 0, cols = 0;
+  bool tiled = false;  // stored as 16 KB SWIZZLE_128B tile images (GemmWeight::blk), not row-major
 };
 
 struct ArLayer {
