@@ -528,21 +528,31 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
         if (!is_gemm(it.kind)) continue;
         const CUtensorMap* wm;
         const CUtensorMap* xm;
-        int nkb, kb0 = 0, wrow = it.j * kDitFeat;
+        const uint8_t* wb;  // pre-tiled weight (or nullptr)
+        int nkb, kb0 = 0, wrow = it.j * kDitFeat, kbt = p.d / 64;  // kbt: k-blocks of the whole weight
         switch (it.kind) {
-          case K_IN: wm = &mp->w_in; xm = &mp->x_x[ti]; nkb = p.C / 64; break;
-          case K_QKV: wm = &mp->wqkv[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
-          case K_O: wm = &mp->wo[it.layer]; xm = &mp->x_o[ti]; nkb = p.d / 64; break;
-          case K_UP: wm = &mp->w1[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
+          case K_IN: wm = &mp->w_in; wb = mp->b_in; xm = &mp->x_x[ti]; nkb = kbt = p.C / 64; break;
+          case K_QKV: wm = &mp->wqkv[it.layer]; wb = mp->b_qkv[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
+          case K_O: wm = &mp->wo[it.layer]; wb = mp->b_o[it.layer]; xm = &mp->x_o[ti]; nkb = p.d / 64; break;
+          case K_UP: wm = &mp->w1[it.layer]; wb = mp->b_1[it.layer]; xm = &mp->x_a[ti]; nkb = p.d / 64; break;
           case K_DOWN:
             wm = &mp->w2[it.layer];
+            wb = mp->b_2[it.layer];
             xm = &mp->x_u[ti];
-            nkb = p.ff / 64 / p.down_split;
+            kbt = p.ff / 64;
+            nkb = kbt / p.down_split;
             kb0 = (it.j % p.down_split) * nkb;
             wrow = (it.j / p.down_split) * kDitFeat;
             break;
-          default: wm = &mp->w_out; xm = &mp->x_a[ti]; nkb = p.d / 64; wrow = 0; break;
+          default: wm = &mp->w_out; wb = mp->b_out; xm = &mp->x_a[ti]; nkb = p.d / 64; wrow = 0; break;
         }
+        auto load_a = [&](int s, int kb) {
+          if (wb)
+            bulk_load_hint(sA + s * kABytes, wb + ((size_t)(wrow / kDitFeat) * kbt + kb) * kABytes, kABytes,
+                           &sm.full[s], pol);
+          else
+            tma_load_2d(sA + s * kABytes, wm, &sm.full[s], kb * 64, wrow, pol);
+        };
         const int xrow = it.r * TR;
         const int pre = nkb < STAGES ? nkb : STAGES;
         for (int i = 0; i < pre; ++i) {  // weights first: they never depend on another item
@@ -550,7 +560,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
           const int s = k % STAGES;
           mbar_wait_sleep(&sm.empty[s], ((k / STAGES) & 1) ^ 1);
           mbar_expect_tx(&sm.full[s], kStageBytes);
-          tma_load_2d(sA + s * kABytes, wm, &sm.full[s], (kb0 + i) * 64, wrow, pol);
+          load_a(s, kb0 + i);
         }
         wait_ge(p.progress + it.r, sm.unit_cum[tp]);
         fence_proxy_async_global();
@@ -564,7 +574,7 @@ __global__ void __launch_bounds__(kThreadsF, 1) dit_fused_kernel(const __grid_co
           const int s = k % STAGES;
           mbar_wait_sleep(&sm.empty[s], ((k / STAGES) & 1) ^ 1);
           mbar_expect_tx(&sm.full[s], kStageBytes);
-          tma_load_2d(sA + s * kABytes, wm, &sm.full[s], (kb0 + i) * 64, wrow, pol);
+          load_a(s, kb0 + i);
           tma_load_2d(sB + s * kBBytes, xm, &sm.full[s], (kb0 + i) * 64, xrow, pol);
         }
         kbi += nkb;

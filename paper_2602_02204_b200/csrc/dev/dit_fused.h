@@ -26,6 +26,10 @@ struct DitMaps {
   CUtensorMap w_in, w_out;
   CUtensorMap wqkv[kDitMaxLayers], wo[kDitMaxLayers], w1[kDitMaxLayers], w2[kDitMaxLayers];
   CUtensorMap x_x[2], x_a[2], x_o[2], x_u[2];  // activations (MMA B operand), [0] 128- / [1] 256-row boxes
+  // pre-tiled weight copies (16 KB SWIZZLE_128B tile images, gemm_block_weight),
+  // nullptr: load the 128-row boxes of the maps above
+  const uint8_t *b_in, *b_out;
+  const uint8_t *b_qkv[kDitMaxLayers], *b_o[kDitMaxLayers], *b_1[kDitMaxLayers], *b_2[kDitMaxLayers];
 };
 
 // Everything else one iteration needs (a small __grid_constant__ parameter).

@@ -121,8 +121,8 @@ struct GemmArgs {
 };
 
 int gemm_block_n(int M);
-// The AR stages' streaming weights (gate-up, down) are stored pre-tiled
-// (default; OMNI_WBLOCK=0 keeps them row-major).
+// The AR stages' streaming weights (gate-up, down) and the DiT's GEMM weights
+// are stored pre-tiled (default; OMNI_WBLOCK=0 keeps them row-major).
 bool gemm_decode_weights_blocked();
 // Writes the pre-tiled copy of a row-major weight [N_pad, K] (GemmWeight::blk).
 cudaError_t gemm_block_weight(const __nv_bfloat16* w, int N_pad, int K, uint8_t* blk, cudaStream_t st);

@@ -264,11 +264,15 @@ void build_dit(omni_stage* st) {
   OMNI_REQUIRE(m.dit_channels % 64 == 0 && m.dit_channels <= 128, OMNI_E_BADARG, "DiT channels");
   const int d = m.d_model, L = m.n_layers, C = m.dit_channels, ff = m.d_ff;
   const float s_d = 1.f / std::sqrt((float)d);
-  st->w_in = make_weight(st, "w_in", d, d, C, 1, 1.f / std::sqrt((float)C));
+  // the DiT's GEMM weights pre-tiled like the AR streaming weights: each
+  // item's weight tiles are single 16 KB bulk copies (isolated iteration
+  // 1018 -> 998 us at 8 tokens, within 1 % at 64-512; profiles/r02_weight_tiles.txt)
+  const bool dt = gemm_decode_weights_blocked();
+  st->w_in = make_weight(st, "w_in", d, d, C, 1, 1.f / std::sqrt((float)C), dt);
   st->pos_emb = make_weight(st, "pos_emb", kDitSamples, kDitSamples, d, 2, 0.5f);
   st->tok_emb = make_weight(st, "tok_emb", m.vocab, m.vocab, d, 3, 1.0f);
   st->t_emb = make_weight(st, "t_emb", m.dit_steps, m.dit_steps, d, 4, 1.0f);
-  st->w_out = make_weight(st, "w_out", C, round_up(C, 128), d, 5, s_d);
+  st->w_out = make_weight(st, "w_out", C, round_up(C, 128), d, 5, s_d, dt);
   st->w_mod = make_weight(st, "w_mod", (int64_t)L * 6 * d, (int64_t)L * 6 * d, d, 6, 0.5f * s_d);
   st->g_in = gemm_of(st->w_in, 1);
   st->g_in.fill_sms = true;
@@ -280,10 +284,10 @@ void build_dit(omni_stage* st) {
     auto& ly = st->dlayers[l];
     const uint32_t b = 16u * (l + 1);
     const std::string p = "L" + std::to_string(l) + ".";
-    ly.wqkv = make_weight(st, p + "wqkv", 3 * d, 3 * d, d, b + 1, s_d);
-    ly.wo = make_weight(st, p + "wo", d, d, d, b + 2, s_d);
-    ly.w1 = make_weight(st, p + "w1", ff, ff, d, b + 3, s_d);
-    ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff));
+    ly.wqkv = make_weight(st, p + "wqkv", 3 * d, 3 * d, d, b + 1, s_d, dt);
+    ly.wo = make_weight(st, p + "wo", d, d, d, b + 2, s_d, dt);
+    ly.w1 = make_weight(st, p + "w1", ff, ff, d, b + 3, s_d, dt);
+    ly.w2 = make_weight(st, p + "w2", d, d, ff, b + 4, 1.f / std::sqrt((float)ff), dt);
     ly.gqkv = gemm_of(ly.wqkv, 1);
     ly.gqkv.fill_sms = true;
     ly.go = gemm_of(ly.wo, 1, 64);
@@ -333,12 +337,18 @@ void build_dit(omni_stage* st) {
     DitMaps mp{};
     mp.w_in = st->g_in.tmap;  // 128-row boxes: MMA A (swap-AB)
     mp.w_out = st->g_out.tmap;
+    mp.b_in = st->g_in.blk;
+    mp.b_out = st->g_out.blk;
     for (int l = 0; l < L; ++l) {
       const auto& ly = st->dlayers[l];
       mp.wqkv[l] = ly.gqkv.tmap;
       mp.wo[l] = ly.go.tmap;
       mp.w1[l] = ly.g1.tmap;
       mp.w2[l] = ly.g2.tmap;
+      mp.b_qkv[l] = ly.gqkv.blk;
+      mp.b_o[l] = ly.go.blk;
+      mp.b_1[l] = ly.g1.blk;
+      mp.b_2[l] = ly.g2.blk;
     }
     for (int i = 0; i < 2; ++i) {  // 128- and 256-row boxes (dit_tile_rows)
       mp.x_x[i] = st->din_x.tmap_for(128 << i);
